@@ -1,0 +1,184 @@
+/*
+ * rootbox_b200.h -- C ABI of the B200 (sm_100a) engine for the rootbox solver
+ * hot path: global interval branch-and-bound with Hansen-Sengupta contraction.
+ *
+ * The library (paper_1802_00330_b200/librootbox_b200.so) replaces the
+ * internals of the reference entry point
+ *
+ *     rootbox.bnb.solve(s: PolySystem, cfg: SolverConfig) -> SolveResult
+ *                                       (rootbox/bnb.py:224-354, __init__.py:12)
+ *
+ * and its two per-round operators
+ *
+ *     bnb._chunk_batch((cs, lo, hi)) -> (lo, hi)                 (bnb.py:161-165)
+ *     bnb._hs_pass(s, jac, lo, hi, contract_output) -> (lo, hi, cert)  (bnb.py:190-218)
+ *
+ * Plain C types only: pointers, sizes, IEEE binary64.  Box arrays crossing
+ * the ABI are row-major (N x n), exactly the numpy layout of the reference
+ * (_batch.py:9).  Every call is synchronous w.r.t. the caller's buffers,
+ * thread-safe per handle (calls on one handle serialise), and does not hold
+ * the Python GIL when invoked through ctypes.
+ *
+ * Return codes: 0 = ok; negative = error, message in rb_last_error().
+ */
+#ifndef ROOTBOX_B200_H
+#define ROOTBOX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RB_OK 0
+#define RB_ERR_ARG -1      /* invalid argument (reference: ValueError)        */
+#define RB_ERR_CUDA -2     /* CUDA runtime error                             */
+#define RB_ERR_NOMEM -3    /* device memory exhausted (reference: MemoryError) */
+#define RB_ERR_LIMIT -4    /* system exceeds the compiled table limits        */
+#define RB_ERR_STATE -5    /* call out of sequence (e.g. fetch before solve)  */
+
+#define RB_MAX_DIM 16
+
+/* status codes == bnb.py:40-42 */
+#define RB_NO_REAL_SOLUTION 0 /* "no_real_solution" */
+#define RB_WIDTH_REACHED 1    /* "width_reached"    */
+#define RB_BUDGET_EXHAUSTED 2 /* "budget_exhausted" */
+
+/* A compiled polynomial system (the flat form of _batch.compile_system,
+ * _batch.py:156-164, extended with the Jacobian of PolySystem.jacobian,
+ * poly.py:284-291).  Polynomials 0..n-1 are F in equation order; polynomial
+ * n + i*n + j is dF_i/dx_j.  Terms of each polynomial are in the canonical
+ * order of poly.py:159 (descending (degree, exponents)); factors of a term
+ * are its nonzero (variable, exponent) pairs in ascending variable order. */
+typedef struct rb_system {
+    int32_t n;                /* dimension, 1..RB_MAX_DIM                 */
+    int32_t n_polys;          /* n + n*n                                  */
+    const int32_t* poly_off;  /* [n_polys + 1] term ranges                */
+    const double* coeff;      /* [T] coefficients                         */
+    const int32_t* fac_off;   /* [T + 1] factor ranges                    */
+    const uint8_t* fac_var;   /* [Fc] variable index                      */
+    const uint8_t* fac_exp;   /* [Fc] exponent >= 1                       */
+    const double* init_lo;    /* [n] initial box (PolySystem.initial_box) */
+    const double* init_hi;    /* [n]                                      */
+} rb_system;
+
+/* SolverConfig (bnb.py:49-86).  None is encoded as noted. worker_count,
+ * batch_size and engine do not change results (bnb.py:9-11) and are not
+ * passed. */
+typedef struct rb_config {
+    double target_width;      /* <= 0 or NaN: None (2^-10 x initial width) */
+    int32_t hs_enable_round;  /* < 0: None                                  */
+    int32_t hs_contract;      /* bool                                       */
+    double hs_enable_width;   /* NaN: None                                  */
+    int32_t max_rounds;
+    int32_t exact_round_dedup;/* 1: exact per-round dedup (bnb.py:322-326)  */
+    int64_t max_boxes;
+    double max_seconds;       /* < 0 or NaN: None                           */
+} rb_config;
+
+/* RoundStats (bnb.py:89-96) plus engine counters. */
+typedef struct rb_round_stats {
+    int32_t round;
+    int32_t hs_on;
+    int64_t boxes_in;
+    int64_t boxes_after_filter;
+    int64_t boxes_after_hs;
+    double width;
+    double elapsed_seconds;
+    int64_t children;          /* active parents x 2^n evaluated by the filter */
+    int64_t hs_calls;          /* boxes contracted                              */
+    int64_t filter_ops;        /* algorithmic directed ops in the filter        */
+    int64_t hs_ops;            /* algorithmic directed ops in HS                */
+    int64_t dups;              /* exact duplicates removed                      */
+    int64_t exact_boxes;       /* boxes evaluated on the exact (guarded) path   */
+    double filter_ms;          /* device time of the filter kernel(s)           */
+    double hs_ms;              /* device time of the HS kernel(s)               */
+    double classify_ms;        /* device time of the classify/compaction kernel */
+    int64_t classify_bytes;    /* algorithmic HBM bytes of the classify kernel  */
+} rb_round_stats;
+
+typedef struct rb_result_info {
+    int32_t status;            /* RB_NO_REAL_SOLUTION / RB_WIDTH_REACHED / RB_BUDGET_EXHAUSTED */
+    int32_t nrounds;
+    int64_t nboxes;
+    double solve_seconds;      /* host wall time inside rb_solve */
+} rb_result_info;
+
+typedef struct rb_handle rb_handle;
+
+/* Library version string. */
+const char* rb_version(void);
+
+/* Number of visible CUDA devices (>= 0), or a negative error code. */
+int rb_device_count(void);
+
+/* Create an engine for one system on one CUDA device (one handle per GPU /
+ * per rank).  Copies the tables; the caller keeps ownership of `sys`.
+ * Replaces: compile_system + PolySystem.jacobian setup in bnb.solve
+ * (bnb.py:236-238). */
+int rb_create(const rb_system* sys, int device, rb_handle** out);
+
+/* Run bnb.solve (bnb.py:224-354) on the device.  Results stay on the device
+ * until rb_fetch.  Replaces the whole round loop. */
+int rb_solve(rb_handle* h, const rb_config* cfg, rb_result_info* info);
+
+/* Copy the last solve's result into caller-allocated host buffers:
+ * lo/hi [nboxes x n] row-major in canonical order (_batch.canonical_order,
+ * _batch.py:244-250), cert/unsplit [nboxes] (RootBox.certified/unsplittable,
+ * bnb.py:99-103), stats [nrounds].  Any pointer may be NULL to skip it. */
+int rb_fetch(rb_handle* h, double* lo, double* hi, uint8_t* cert, uint8_t* unsplit,
+             rb_round_stats* stats);
+
+/* bnb._chunk_batch (bnb.py:161-165) on P parents (row-major P x n, all
+ * non-degenerate): writes the feasible children, in the reference's order
+ * (parents in input order, children in binary-counting order), to olo/ohi
+ * (capacity `cap` rows); *M receives the survivor count even if > cap. */
+int rb_filter(rb_handle* h, const double* plo, const double* phi, int64_t P, double* olo,
+              double* ohi, int64_t cap, int64_t* M);
+
+/* bnb._hs_pass (bnb.py:190-218) on M rows: writes the surviving rows in the
+ * reference's order (forks as two consecutive rows) and their certified flags;
+ * *M2 receives the output count even if > cap. */
+int rb_hs(rb_handle* h, const double* lo, const double* hi, int64_t M, int contract_output,
+          double* olo, double* ohi, uint8_t* cert, int64_t cap, int64_t* M2);
+
+/* Last error message of this handle (or of the last failed rb_create when h is NULL). */
+const char* rb_last_error(rb_handle* h);
+
+void rb_destroy(rb_handle* h);
+
+/* ---- sharded (multi-GPU) round protocol -------------------------------------
+ * One handle per rank; the host performs the tiny per-round exchanges
+ * (torch.distributed / NCCL) between the calls.  The same kernels as rb_solve. */
+
+/* Load a shard of the frontier (row-major, host) as the current round input. */
+int rb_shard_load(rb_handle* h, const double* lo, const double* hi, const uint8_t* cert,
+                  const uint8_t* unsplit, int64_t N, double target_width);
+
+/* Round part 1: classify + bisect + filter.  Outputs the local survivor
+ * count and max child width (for the global HS trigger, bnb.py:289-296). */
+int rb_round_filter(rb_handle* h, int32_t round_no, int64_t* carried, int64_t* survivors,
+                    double* child_width, int64_t* children);
+
+/* Round part 2: HS (hs_on decided globally by the caller) + per-shard dedup.
+ * Outputs the local frontier size and max width. */
+int rb_round_hs(rb_handle* h, int32_t hs_on, int32_t hs_contract, int64_t* n_out,
+                double* width, int64_t* hs_calls);
+
+/* Copy `count` rows starting at `start` of the current frontier to host
+ * buffers (any order; used for rebalancing and the final gather). */
+int rb_shard_export(rb_handle* h, int64_t start, int64_t count, double* lo, double* hi,
+                    uint8_t* cert, uint8_t* unsplit);
+
+/* Keep only rows [0, keep) of the current frontier and append `count` rows
+ * from host buffers (rebalancing receive). */
+int rb_shard_import(rb_handle* h, int64_t keep, const double* lo, const double* hi,
+                    const uint8_t* cert, const uint8_t* unsplit, int64_t count);
+
+/* Current frontier size of the shard. */
+int64_t rb_shard_size(rb_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROOTBOX_B200_H */

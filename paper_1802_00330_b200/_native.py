@@ -1,0 +1,204 @@
+"""ctypes binding of the in-tree C-ABI library librootbox_b200.so (include/rootbox_b200.h).
+
+There is no CPU fallback: if the library is missing or no sm_100 device is
+visible, every entry point raises.  ctypes releases the GIL for the duration
+of each call, so concurrent solves on different handles run in parallel.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "librootbox_b200.so")
+
+RB_NO_REAL_SOLUTION, RB_WIDTH_REACHED, RB_BUDGET_EXHAUSTED = 0, 1, 2
+STATUS_NAMES = {0: "no_real_solution", 1: "width_reached", 2: "budget_exhausted"}
+RB_ERR_ARG, RB_ERR_CUDA, RB_ERR_NOMEM, RB_ERR_LIMIT, RB_ERR_STATE = -1, -2, -3, -4, -5
+
+
+class RbSystem(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32), ("n_polys", C.c_int32),
+        ("poly_off", C.c_void_p), ("coeff", C.c_void_p), ("fac_off", C.c_void_p),
+        ("fac_var", C.c_void_p), ("fac_exp", C.c_void_p),
+        ("init_lo", C.c_void_p), ("init_hi", C.c_void_p),
+    ]
+
+
+class RbConfig(C.Structure):
+    _fields_ = [
+        ("target_width", C.c_double), ("hs_enable_round", C.c_int32), ("hs_contract", C.c_int32),
+        ("hs_enable_width", C.c_double), ("max_rounds", C.c_int32), ("exact_round_dedup", C.c_int32),
+        ("max_boxes", C.c_int64), ("max_seconds", C.c_double),
+    ]
+
+
+class RbRoundStats(C.Structure):
+    _fields_ = [
+        ("round", C.c_int32), ("hs_on", C.c_int32),
+        ("boxes_in", C.c_int64), ("boxes_after_filter", C.c_int64), ("boxes_after_hs", C.c_int64),
+        ("width", C.c_double), ("elapsed_seconds", C.c_double),
+        ("children", C.c_int64), ("hs_calls", C.c_int64), ("filter_ops", C.c_int64), ("hs_ops", C.c_int64),
+        ("dups", C.c_int64), ("exact_boxes", C.c_int64),
+        ("filter_ms", C.c_double), ("hs_ms", C.c_double), ("classify_ms", C.c_double),
+        ("classify_bytes", C.c_int64),
+    ]
+
+
+class RbResultInfo(C.Structure):
+    _fields_ = [("status", C.c_int32), ("nrounds", C.c_int32), ("nboxes", C.c_int64),
+                ("solve_seconds", C.c_double)]
+
+
+STATS_FIELDS = [f for f, _ in RbRoundStats._fields_]
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load the engine library; raises ImportError when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(make -C paper_1802_00330_b200/csrc).  There is no CPU fallback.")
+    L = C.CDLL(LIB_PATH)
+    P, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+    L.rb_version.restype = C.c_char_p
+    L.rb_device_count.restype = i32
+    L.rb_create.argtypes = [C.POINTER(RbSystem), i32, C.POINTER(P)]
+    L.rb_create.restype = i32
+    L.rb_solve.argtypes = [P, C.POINTER(RbConfig), C.POINTER(RbResultInfo)]
+    L.rb_solve.restype = i32
+    L.rb_fetch.argtypes = [P, P, P, P, P, P]
+    L.rb_fetch.restype = i32
+    L.rb_filter.argtypes = [P, P, P, i64, P, P, i64, C.POINTER(i64)]
+    L.rb_filter.restype = i32
+    L.rb_hs.argtypes = [P, P, P, i64, i32, P, P, P, i64, C.POINTER(i64)]
+    L.rb_hs.restype = i32
+    L.rb_last_error.argtypes = [P]
+    L.rb_last_error.restype = C.c_char_p
+    L.rb_destroy.argtypes = [P]
+    L.rb_shard_load.argtypes = [P, P, P, P, P, i64, C.c_double]
+    L.rb_shard_load.restype = i32
+    L.rb_round_filter.argtypes = [P, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(C.c_double),
+                                  C.POINTER(i64)]
+    L.rb_round_filter.restype = i32
+    L.rb_round_hs.argtypes = [P, i32, i32, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(i64)]
+    L.rb_round_hs.restype = i32
+    L.rb_shard_export.argtypes = [P, i64, i64, P, P, P, P]
+    L.rb_shard_export.restype = i32
+    L.rb_shard_import.argtypes = [P, i64, P, P, P, P, i64]
+    L.rb_shard_import.restype = i32
+    L.rb_shard_size.argtypes = [P]
+    L.rb_shard_size.restype = i64
+    _lib = L
+    return L
+
+
+EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch", "rb_filter", "rb_hs",
+            "rb_last_error", "rb_destroy", "rb_shard_load", "rb_round_filter", "rb_round_hs",
+            "rb_shard_export", "rb_shard_import", "rb_shard_size"]
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _check(rc, h, what):
+    if rc != 0:
+        msg = lib().rb_last_error(h)
+        msg = msg.decode() if msg else ""
+        if rc == RB_ERR_NOMEM:
+            raise MemoryError(f"{what}: {msg}")
+        if rc in (RB_ERR_ARG, RB_ERR_LIMIT):
+            raise ValueError(f"{what}: {msg}")
+        raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+class Engine:
+    """One device-resident engine for one compiled system (rb_handle)."""
+
+    def __init__(self, tables, device: int = 0):
+        L = lib()
+        self.n = tables.n
+        self.device = device
+        self._keep = (tables.poly_off, tables.coeff, tables.fac_off, tables.fac_var, tables.fac_exp,
+                      tables.init_lo, tables.init_hi)
+        sysd = RbSystem(
+            n=tables.n, n_polys=len(tables.poly_off) - 1,
+            poly_off=_p(tables.poly_off), coeff=_p(tables.coeff), fac_off=_p(tables.fac_off),
+            fac_var=_p(tables.fac_var if tables.fac_var.size else np.zeros(1, np.uint8)),
+            fac_exp=_p(tables.fac_exp if tables.fac_exp.size else np.zeros(1, np.uint8)),
+            init_lo=_p(tables.init_lo), init_hi=_p(tables.init_hi))
+        h = C.c_void_p()
+        rc = L.rb_create(C.byref(sysd), int(device), C.byref(h))
+        _check(rc, None, "rb_create")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().rb_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def solve(self, cfg: RbConfig):
+        L = lib()
+        info = RbResultInfo()
+        _check(L.rb_solve(self.h, C.byref(cfg), C.byref(info)), self.h, "rb_solve")
+        N, n = int(info.nboxes), self.n
+        lo = np.empty((N, n)); hi = np.empty((N, n))
+        cert = np.empty(N, np.uint8); uns = np.empty(N, np.uint8)
+        stats = (RbRoundStats * max(1, info.nrounds))()
+        _check(L.rb_fetch(self.h, _p(lo), _p(hi), _p(cert), _p(uns), C.cast(stats, C.c_void_p)), self.h,
+               "rb_fetch")
+        st = [{f: getattr(stats[i], f) for f in STATS_FIELDS} for i in range(info.nrounds)]
+        return {"status": STATUS_NAMES[info.status], "lo": lo, "hi": hi, "cert": cert.astype(bool),
+                "unsplit": uns.astype(bool), "stats": st, "solve_seconds": info.solve_seconds}
+
+    def filter(self, plo, phi):
+        plo = np.ascontiguousarray(plo, np.float64); phi = np.ascontiguousarray(phi, np.float64)
+        P = plo.shape[0]
+        cap = max(1, P * 64)
+        for _ in range(2):
+            olo = np.empty((cap, self.n)); ohi = np.empty((cap, self.n))
+            M = C.c_int64()
+            _check(lib().rb_filter(self.h, _p(plo), _p(phi), P, _p(olo), _p(ohi), cap, C.byref(M)), self.h,
+                   "rb_filter")
+            if M.value <= cap:
+                return olo[:M.value].copy(), ohi[:M.value].copy()
+            cap = M.value
+        raise NativeError("rb_filter: capacity retry failed")
+
+    def hs(self, lo, hi, contract_output=True):
+        lo = np.ascontiguousarray(lo, np.float64); hi = np.ascontiguousarray(hi, np.float64)
+        M = lo.shape[0]
+        cap = max(1, 2 * M)
+        olo = np.empty((cap, self.n)); ohi = np.empty((cap, self.n)); oc = np.empty(cap, np.uint8)
+        M2 = C.c_int64()
+        _check(lib().rb_hs(self.h, _p(lo), _p(hi), M, int(bool(contract_output)), _p(olo), _p(ohi), _p(oc), cap,
+                           C.byref(M2)), self.h, "rb_hs")
+        m = M2.value
+        return olo[:m].copy(), ohi[:m].copy(), oc[:m].astype(bool)
+
+
+def device_count() -> int:
+    return int(lib().rb_device_count())
+
+
+def version() -> str:
+    return lib().rb_version().decode()

@@ -1,0 +1,252 @@
+"""Drop-in ``solve`` for the reference solver entry point, on the B200 engine.
+
+Mirrors rootbox.bnb (bnb.py:40-114, 224-361): same names, same fields, same
+argument meaning, same ``ValueError`` from ``SolverConfig.validate``, same
+statuses and the same canonically ordered ``SolveResult.boxes``.  The round
+loop runs inside librootbox_b200.so (one rb_solve call); this module only
+converts types.
+
+If the system passed in is a reference ``rootbox.poly.PolySystem`` (and the
+reference package is importable), the result is built from the reference's
+own classes (``rootbox.bnb.SolveResult``/``RootBox``/``RoundStats``,
+``rootbox.poly.Box``, ``rootbox.interval.Interval``) so downstream reference
+code (backtrack.snap_to_grid, cli.RunReport) consumes it unchanged.
+Otherwise the lightweight mirror types below are returned.
+"""
+from __future__ import annotations
+
+import math
+import os
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .system import SystemSpec, as_spec, compile_tables
+
+__all__ = ["SolverConfig", "RoundStats", "RootBox", "SolveResult", "Interval", "Box", "solve",
+           "solve_arrays", "NO_REAL_SOLUTION", "WIDTH_REACHED", "BUDGET_EXHAUSTED"]
+
+NO_REAL_SOLUTION = "no_real_solution"
+WIDTH_REACHED = "width_reached"
+BUDGET_EXHAUSTED = "budget_exhausted"
+
+
+class Interval:
+    """Closed interval container (the arithmetic runs on the device)."""
+
+    __slots__ = ("lo", "hi")
+
+    def __init__(self, lo, hi):
+        lo = float(lo)
+        hi = float(hi)
+        if lo != lo or hi != hi:
+            raise ValueError(f"NaN bound in [{lo}, {hi}]")
+        if lo > hi:
+            raise ValueError(f"lower bound {lo!r} exceeds upper bound {hi!r}")
+        object.__setattr__(self, "lo", lo)
+        object.__setattr__(self, "hi", hi)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("Interval is immutable")
+
+    def __repr__(self):
+        f = lambda v: "inf" if v == math.inf else ("-inf" if v == -math.inf else repr(v))  # noqa: E731
+        return f"[{f(self.lo)},{f(self.hi)}]"
+
+    def __eq__(self, other):
+        return isinstance(other, Interval) and self.lo == other.lo and self.hi == other.hi
+
+    def __hash__(self):
+        return hash((self.lo, self.hi))
+
+
+@dataclass(frozen=True)
+class Box:
+    intervals: tuple
+
+    @classmethod
+    def from_bounds(cls, los, his):
+        return cls(tuple(Interval(lo, hi) for lo, hi in zip(los, his)))
+
+    def __len__(self):
+        return len(self.intervals)
+
+    def __iter__(self):
+        return iter(self.intervals)
+
+    def __getitem__(self, i):
+        return self.intervals[i]
+
+    @property
+    def dimension(self):
+        return len(self.intervals)
+
+    def sort_key(self):
+        return tuple(iv.lo for iv in self.intervals) + tuple(iv.hi for iv in self.intervals)
+
+    def contains_point(self, point):
+        return all(iv.lo <= float(v) <= iv.hi for iv, v in zip(self.intervals, point))
+
+    def __str__(self):
+        return " x ".join(str(iv) for iv in self.intervals)
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """bnb.py:49-86.  worker_count / batch_size / engine are accepted and
+    validated for drop-in compatibility; results do not depend on them
+    (bnb.py:9-11) and the B200 engine ignores them."""
+
+    target_width: float | None = None
+    hs_enable_round: int | None = None
+    hs_enable_width: float | None = 1.0
+    max_rounds: int = 24
+    max_boxes: int = 200_000_000
+    max_seconds: float | None = None
+    worker_count: int = 1
+    batch_size: int = 4096
+    hs_contract: bool = True
+    engine: str = "batch"
+
+    def validate(self) -> None:
+        validate_config(self)
+
+
+def validate_config(cfg) -> None:
+    """SolverConfig.validate (bnb.py:72-86), for our config or the reference's."""
+    if cfg.target_width is not None and not cfg.target_width > 0:
+        raise ValueError("target_width must be positive")
+    if cfg.max_boxes < 1:
+        raise ValueError("max_boxes must be at least 1")
+    if cfg.max_rounds < 1:
+        raise ValueError("max_rounds must be at least 1")
+    if cfg.worker_count < 1:
+        raise ValueError("worker_count must be at least 1")
+    if cfg.batch_size < 1:
+        raise ValueError("batch_size must be at least 1")
+    if cfg.hs_enable_round is not None and cfg.hs_enable_round < 0:
+        raise ValueError("hs_enable_round must be >= 0")
+    if cfg.engine not in ("batch", "scalar"):
+        raise ValueError(f"unknown engine {cfg.engine!r}")
+
+
+@dataclass(frozen=True)
+class RoundStats:
+    round: int
+    boxes_in: int
+    boxes_after_filter: int
+    boxes_after_hs: int
+    width: float
+    elapsed_seconds: float
+
+
+@dataclass(frozen=True)
+class RootBox:
+    box: Box
+    certified: bool = False
+    unsplittable: bool = False
+
+
+@dataclass(frozen=True)
+class SolveResult:
+    status: str
+    boxes: tuple = ()
+    stats: tuple = field(default=())
+
+    @property
+    def reached_width(self) -> bool:
+        return self.status == WIDTH_REACHED
+
+
+# ---------------------------------------------------------------- engine cache
+
+_ENGINES: dict = {}
+_LOCK = threading.Lock()
+_MAX_ENGINES = 8
+
+
+def default_device() -> int:
+    for k in ("RB_DEVICE", "LOCAL_RANK"):
+        v = os.environ.get(k)
+        if v is not None and v.strip().isdigit():
+            return int(v)
+    return 0
+
+
+def _key(spec: SystemSpec):
+    t = compile_tables(spec)
+    h = (t.n, t.poly_off.tobytes(), t.coeff.tobytes(), t.fac_off.tobytes(), t.fac_var.tobytes(),
+         t.fac_exp.tobytes(), t.init_lo.tobytes(), t.init_hi.tobytes())
+    return h, t
+
+
+def engine_for(spec: SystemSpec, device: int | None = None) -> _native.Engine:
+    """Cached device engine for a system (device buffers persist across solves)."""
+    device = default_device() if device is None else device
+    key, tables = _key(spec)
+    with _LOCK:
+        e = _ENGINES.get((key, device))
+        if e is None:
+            if len(_ENGINES) >= _MAX_ENGINES:
+                _ENGINES.pop(next(iter(_ENGINES))).close()
+            e = _native.Engine(tables, device)
+            _ENGINES[(key, device)] = e
+        return e
+
+
+def native_config(cfg, exact_round_dedup: bool = True) -> _native.RbConfig:
+    return _native.RbConfig(
+        target_width=-1.0 if cfg.target_width is None else float(cfg.target_width),
+        hs_enable_round=-1 if cfg.hs_enable_round is None else int(cfg.hs_enable_round),
+        hs_contract=1 if cfg.hs_contract else 0,
+        hs_enable_width=math.nan if cfg.hs_enable_width is None else float(cfg.hs_enable_width),
+        max_rounds=int(cfg.max_rounds),
+        exact_round_dedup=1 if exact_round_dedup else 0,
+        max_boxes=int(cfg.max_boxes),
+        max_seconds=-1.0 if cfg.max_seconds is None else float(cfg.max_seconds),
+    )
+
+
+def solve_arrays(s, cfg=None, device: int | None = None) -> dict:
+    """solve() without Python object materialisation: returns the canonical
+    row-major arrays (lo, hi, cert, unsplit), status and per-round stats
+    (including device kernel times and algorithmic op counts)."""
+    cfg = cfg or SolverConfig()
+    validate_config(cfg)
+    spec = as_spec(s)
+    eng = engine_for(spec, device)
+    return eng.solve(native_config(cfg))
+
+
+def _reference_types(s):
+    mod = type(s).__module__
+    if not mod.startswith("rootbox"):
+        return None
+    try:
+        from rootbox import bnb as rbnb  # type: ignore
+        from rootbox import poly as rpoly  # type: ignore
+        from rootbox.interval import Interval as RInterval  # type: ignore
+    except Exception:
+        return None
+    return rbnb.SolveResult, rbnb.RootBox, rbnb.RoundStats, rpoly.Box, RInterval
+
+
+def solve(s, cfg=None) -> SolveResult:
+    """Isolate all real roots of the system inside its initial box (bnb.py:224)."""
+    out = solve_arrays(s, cfg)
+    types = _reference_types(s)
+    if types is None:
+        SR, RB, RS, BX, IV = SolveResult, RootBox, RoundStats, Box, Interval
+    else:
+        SR, RB, RS, BX, IV = types
+    lo, hi, cert, uns = out["lo"], out["hi"], out["cert"], out["unsplit"]
+    boxes = tuple(
+        RB(BX(tuple(IV(a, b) for a, b in zip(lo[r].tolist(), hi[r].tolist()))), bool(cert[r]), bool(uns[r]))
+        for r in range(lo.shape[0]))
+    stats = tuple(RS(round=int(st["round"]), boxes_in=int(st["boxes_in"]),
+                     boxes_after_filter=int(st["boxes_after_filter"]), boxes_after_hs=int(st["boxes_after_hs"]),
+                     width=float(st["width"]), elapsed_seconds=float(st["elapsed_seconds"]))
+                  for st in out["stats"])
+    return SR(out["status"], boxes, stats)

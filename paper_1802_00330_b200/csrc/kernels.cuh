@@ -1,0 +1,1027 @@
+// kernels.cuh -- the device side of the B200 engine (sm_100a, FP64 SIMT).
+//
+//   K3 k_classify   done / degenerate / active split of the frontier + compaction
+//                   (bnb.py:249-269), parent exponent guards.
+//   K1 k_filter     implicit 2^n bisection + inclusion-function filter + compaction
+//                   (bnb.py:161-165, _batch.py:167-238), thread per child.
+//   K2 k_hs         Hansen-Sengupta contraction (hansen.py:56-138, bnb.py:190-218),
+//                   G lanes per box (G = 2n rounded up to a power of two).
+//   k_dedup_*       exact duplicate removal with flag OR (_batch.py:253-266).
+//   k_sort_*        canonical order keys + gather (_batch.py:244-250).
+//
+// Frontier layout in HBM: structure of arrays, component-major:
+//   lo[j * cap + row], hi[j * cap + row] (float64), cert[row], unsplit[row] (u8).
+// Consecutive threads touch consecutive rows -> fully coalesced 8-byte lanes.
+#pragma once
+#include <cstdint>
+#include "interval.cuh"
+
+namespace rb {
+
+constexpr int MAX_N = 16;
+
+// ------------------------------------------------------------------ tables
+
+// Device copy of the compiled system (rb_system), one contiguous global buffer:
+//   double   coeff[T]
+//   uint16_t poly_off[P + 1]       P = n + n*n
+//   uint16_t fac_off[T + 1]
+//   uint16_t fac[Fc]               var | exp << 8
+struct TabMeta {
+    int n, T, Fc, P;
+    int TF, FcF;                    // F-only prefix sizes
+    int off_poly, off_fac_off, off_fac, bytes;   // byte offsets in the global buffer
+    int f_ecmin, f_ecmax, f_deg;    // guard constants: coefficient exponent range, max degree
+    int j_ecmin, j_ecmax, j_deg;
+    int ops_eq[MAX_N];              // algorithmic ops per equation
+    int ops_hs_pre;                 // ops of HS preconditioning per box
+    int ops_hs_row;                 // ops of one sweep row
+};
+
+struct STab {
+    const double* coeff;
+    const uint16_t* poly_off;
+    const uint16_t* fac_off;
+    const uint16_t* fac;
+};
+
+__host__ __device__ inline int align8(int x) { return (x + 7) & ~7; }
+
+// bytes of the shared-memory copy (F only when f_only)
+__host__ __device__ inline int stab_bytes(const TabMeta& m, bool f_only) {
+    const int T = f_only ? m.TF : m.T;
+    const int P = f_only ? m.n : m.P;
+    const int Fc = f_only ? m.FcF : m.Fc;
+    return align8(8 * T) + align8(2 * (P + 1)) + align8(2 * (T + 1)) + align8(2 * Fc);
+}
+
+__device__ inline STab load_stab(const TabMeta& m, const uint8_t* g, uint8_t* s, bool f_only) {
+    const int T = f_only ? m.TF : m.T;
+    const int P = f_only ? m.n : m.P;
+    const int Fc = f_only ? m.FcF : m.Fc;
+    STab t;
+    double* c = reinterpret_cast<double*>(s);
+    uint16_t* po = reinterpret_cast<uint16_t*>(s + align8(8 * T));
+    uint16_t* fo = reinterpret_cast<uint16_t*>(s + align8(8 * T) + align8(2 * (P + 1)));
+    uint16_t* fa = reinterpret_cast<uint16_t*>(s + align8(8 * T) + align8(2 * (P + 1)) + align8(2 * (T + 1)));
+    const double* gc = reinterpret_cast<const double*>(g);
+    const uint16_t* gpo = reinterpret_cast<const uint16_t*>(g + m.off_poly);
+    const uint16_t* gfo = reinterpret_cast<const uint16_t*>(g + m.off_fac_off);
+    const uint16_t* gfa = reinterpret_cast<const uint16_t*>(g + m.off_fac);
+    for (int i = threadIdx.x; i < T; i += blockDim.x) c[i] = gc[i];
+    for (int i = threadIdx.x; i <= P; i += blockDim.x) po[i] = gpo[i];
+    for (int i = threadIdx.x; i <= T; i += blockDim.x) fo[i] = gfo[i];
+    for (int i = threadIdx.x; i < Fc; i += blockDim.x) fa[i] = gfa[i];
+    t.coeff = c;
+    t.poly_off = po;
+    t.fac_off = fo;
+    t.fac = fa;
+    return t;
+}
+
+// Polynomial.eval_interval (poly.py:187-203) / _batch.eval_poly (_batch.py:167-186):
+// acc = [0,0]; per term in canonical order: t = [c,c] * x_j1^e1 * ... ; acc += t.
+// x component j is at xlo[j*stride], xhi[j*stride].
+template <class A>
+__device__ __forceinline__ ival eval_poly(const STab& t, int p, const double* xlo, const double* xhi,
+                                          int stride) {
+    ival acc = mk(0.0, 0.0);
+    const int t0 = t.poly_off[p], t1 = t.poly_off[p + 1];
+    for (int q = t0; q < t1; ++q) {
+        const double c = t.coeff[q];
+        const int f0 = t.fac_off[q], f1 = t.fac_off[q + 1];
+        ival term;
+        if (f0 == f1) {
+            term = mk(c, c);
+        } else {
+            uint32_t fv = t.fac[f0];
+            int j = fv & 0xff, k = fv >> 8;
+            term = A::mul_point(c, A::pow(mk(xlo[j * stride], xhi[j * stride]), k));
+            for (int f = f0 + 1; f < f1; ++f) {
+                fv = t.fac[f];
+                j = fv & 0xff;
+                k = fv >> 8;
+                term = A::mul(term, A::pow(mk(xlo[j * stride], xhi[j * stride]), k));
+            }
+        }
+        acc = A::add(acc, term);
+    }
+    return acc;
+}
+
+__device__ __noinline__ ival eval_poly_exact(const STab& t, int p, const double* xlo, const double* xhi,
+                                             int stride) {
+    return eval_poly<Exact>(t, p, xlo, xhi, stride);
+}
+
+// Guard: every nonzero product of a polynomial evaluation over values with
+// exponents in [emin, emax] stays inside the reference's trusted band with a
+// 5-binade margin (so the Dekker error is exact and IEEE RD/RU == reference).
+__device__ __forceinline__ bool poly_guard_ok(int ecmin, int ecmax, int deg, const ExpRange& r) {
+    if (r.emin > r.emax) return true;  // all values zero
+    const int lb = min(ecmin, 0) + deg * min(r.emin, 0);
+    const int ub = max(ecmax + 1, 0) + deg * max(r.emax + 1, 0);
+    return lb >= -965 && ub <= 990;
+}
+
+__device__ __forceinline__ bool prod_guard_ok(const ExpRange& a, const ExpRange& b) {
+    if (a.emin > a.emax || b.emin > b.emax) return true;  // a side is all zero
+    return a.emin + b.emin >= -965 && a.emax + b.emax + 2 <= 990 && a.emax < 990 && b.emax < 990;
+}
+
+__device__ __forceinline__ bool mul_guard_ok(ival x, ival y) {
+    ExpRange a, b;
+    a.init(); b.init();
+    a.add(x.lo); a.add(x.hi);
+    b.add(y.lo); b.add(y.hi);
+    return prod_guard_ok(a, b);
+}
+
+// interval product, guarded per call (rarely taken slow path)
+__device__ __forceinline__ ival gmul(ival x, ival y) {
+    if (mul_guard_ok(x, y)) return Fast::mul(x, y);
+    return Exact::mul(x, y);
+}
+
+enum { DIV_EMPTY = 0, DIV_SINGLE = 1, DIV_SPLIT = 2, DIV_WHOLE = 3 };
+
+// interval.py:394-432 (div_extended), Hanson/Kahan case table.
+__device__ __noinline__ int div_extended(ival x, ival y, ival& p0, ival& p1) {
+    if (!contains_zero(y)) {
+        ival r = mk(div_rd(1.0, y.hi), div_ru(1.0, y.lo));  // recip, interval.py:347-351
+        p0 = gmul(x, r);  // guarded product: Fast when provably trusted
+        return DIV_SINGLE;
+    }
+    if (y.lo == 0.0 && y.hi == 0.0) {
+        if (contains_zero(x)) { p0 = mk(-CUDART_INF, CUDART_INF); return DIV_WHOLE; }
+        return DIV_EMPTY;
+    }
+    if (x.lo < 0.0 && 0.0 < x.hi) { p0 = mk(-CUDART_INF, CUDART_INF); return DIV_WHOLE; }
+    if (x.lo == 0.0 && x.hi == 0.0) { p0 = mk(0.0, 0.0); return DIV_SINGLE; }
+    if (x.hi <= 0.0) {
+        if (y.lo == 0.0) { p0 = mk(-CUDART_INF, div_ru(x.hi, y.hi)); return DIV_SINGLE; }
+        if (y.hi == 0.0) { p0 = mk(div_rd(x.hi, y.lo), CUDART_INF); return DIV_SINGLE; }
+        double a = div_ru(x.hi, y.hi);
+        double b = div_rd(x.hi, y.lo);
+        if (a >= b) { p0 = mk(-CUDART_INF, CUDART_INF); return DIV_WHOLE; }
+        p0 = mk(-CUDART_INF, a);
+        p1 = mk(b, CUDART_INF);
+        return DIV_SPLIT;
+    }
+    if (y.lo == 0.0) { p0 = mk(div_rd(x.lo, y.hi), CUDART_INF); return DIV_SINGLE; }
+    if (y.hi == 0.0) { p0 = mk(-CUDART_INF, div_ru(x.lo, y.lo)); return DIV_SINGLE; }
+    double a = div_ru(x.lo, y.lo);
+    double b = div_rd(x.lo, y.hi);
+    if (a >= b) { p0 = mk(-CUDART_INF, CUDART_INF); return DIV_WHOLE; }
+    p0 = mk(-CUDART_INF, a);
+    p1 = mk(b, CUDART_INF);
+    return DIV_SPLIT;
+}
+
+
+// ------------------------------------------------------------------ frontier views
+
+struct Front {
+    double* lo;
+    double* hi;
+    uint8_t* cert;
+    uint8_t* unsplit;
+    int64_t cap;
+};
+
+struct Counters {
+    unsigned long long n_next;       // rows appended to the next frontier
+    unsigned long long n_carried;    // of which carried (done / degenerate)
+    unsigned long long n_par;        // active parents
+    unsigned long long n_surv;       // filter survivors (may exceed S capacity)
+    unsigned long long child_wmax;   // bits of max child width over survivors
+    unsigned long long wmax;         // bits of max width over the next frontier
+    unsigned long long filter_ops;
+    unsigned long long hs_ops;
+    unsigned long long hs_calls;
+    unsigned long long exact_boxes;
+    unsigned long long dups;
+    unsigned long long hs_on;
+    unsigned long long pad[4];
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ double canon0(double v) { return __dadd_rn(v, 0.0); }  // -0 -> +0
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// warp-aggregated append: returns the slot of this lane (valid if pred)
+__device__ __forceinline__ unsigned long long warp_append(bool pred, unsigned long long* counter,
+                                                          unsigned long long mult = 1) {
+    const unsigned b = __ballot_sync(0xffffffffu, pred);
+    unsigned long long base = 0;
+    const int lane = threadIdx.x & 31;
+    if (b) {
+        const int leader = __ffs(b) - 1;
+        if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(b) * mult);
+        base = __shfl_sync(0xffffffffu, base, leader);
+    }
+    return base + (unsigned long long)__popc(b & lanemask_lt()) * mult;
+}
+
+// ------------------------------------------------------------------ K3 classify
+
+// bnb.py:249-269.  Carried rows (done: width <= target or unsplittable; or
+// degenerate: some midpoint equals an endpoint) are appended to `next` with
+// their flags (degenerate -> cert 0, unsplit 1); the rest become parents.
+// Parent entries carry the filter guard verdict in bit 31 (1 = exact path).
+template <int N>
+__global__ void __launch_bounds__(256) k_classify(TabMeta meta, Front cur, int64_t n_cur, Front next,
+                                                  uint32_t* parents, Counters* ctr, double target) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_cur; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < n_cur;
+        double lo[N], hi[N];
+        double w = 0.0;
+        bool carried = false, deg = false, exact = false;
+        uint8_t cert = 0, uns = 0;
+        if (valid) {
+            ExpRange r;
+            r.init();
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                lo[j] = cur.lo[j * cur.cap + i];
+                hi[j] = cur.hi[j * cur.cap + i];
+                const double d = __dsub_rn(hi[j], lo[j]);
+                w = j == 0 ? d : (d > w ? d : w);
+            }
+            cert = cur.cert[i];
+            uns = cur.unsplit[i];
+            const bool done = (w <= target) || uns;
+            if (!done) {
+#pragma unroll
+                for (int j = 0; j < N; j++) {
+                    const double m = mid_of(lo[j], hi[j]);
+                    deg |= (m == lo[j]) || (m == hi[j]);
+                    r.add(lo[j]);
+                    r.add(hi[j]);
+                    r.add(m);
+                }
+                exact = !poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, r);
+            }
+            carried = done || deg;
+            if (deg && !done) {
+                cert = 0;
+                uns = 1;
+            }
+        }
+        // carried rows -> next frontier
+        const unsigned long long slot = warp_append(valid && carried, &ctr->n_next);
+        if (valid && carried && slot < (unsigned long long)next.cap) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                next.lo[j * next.cap + slot] = lo[j];
+                next.hi[j * next.cap + slot] = hi[j];
+            }
+            next.cert[slot] = cert;
+            next.unsplit[slot] = uns;
+        }
+        const unsigned long long ps = warp_append(valid && !carried, &ctr->n_par);
+        if (valid && !carried) parents[ps] = (uint32_t)i | (exact ? 0x80000000u : 0u);
+        // widths of carried rows feed width_now (bnb.py:329)
+        unsigned long long wb = (valid && carried) ? (unsigned long long)__double_as_longlong(w) : 0ull;
+        wb = warp_max(wb);
+        const unsigned long long nc = __popc(__ballot_sync(0xffffffffu, valid && carried));
+        if ((threadIdx.x & 31) == 0) {
+            if (wb) atomicMax(&ctr->wmax, wb);
+            if (nc) atomicAdd(&ctr->n_carried, nc);
+        }
+    }
+}
+
+// Parents for the rb_filter test hook: every row is a parent (no degeneracy split).
+template <int N>
+__global__ void k_all_parents(TabMeta meta, Front cur, int64_t n_cur, uint32_t* parents, Counters* ctr) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_cur;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        ExpRange r;
+        r.init();
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            const double lo = cur.lo[j * cur.cap + i], hi = cur.hi[j * cur.cap + i];
+            r.add(lo);
+            r.add(hi);
+            r.add(mid_of(lo, hi));
+        }
+        const bool exact = !poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, r);
+        parents[i] = (uint32_t)i | (exact ? 0x80000000u : 0u);
+        if (i == 0) ctr->n_par = (unsigned long long)n_cur;
+    }
+}
+
+// ------------------------------------------------------------------ K1 filter
+
+struct SBuf {  // survivor buffer (HS input), SoA
+    double* lo;
+    double* hi;
+    int64_t cap;
+};
+
+template <int N, class A>
+__device__ __forceinline__ bool feasible(const TabMeta& meta, const STab& t, const double* xlo,
+                                         const double* xhi, int stride, unsigned& ops) {
+#pragma unroll 1
+    for (int e = 0; e < N; e++) {
+        const ival v = A::exact ? eval_poly_exact(t, e, xlo, xhi, stride) : eval_poly<A>(t, e, xlo, xhi, stride);
+        ops += meta.ops_eq[e];
+        if (!(v.lo <= 0.0 && 0.0 <= v.hi)) return false;  // bnb.py:149-154 short-circuit
+    }
+    return true;
+}
+
+// One thread per child.  Child c of parent p takes the low half of component j
+// iff bit (n-1-j) of c is 0 (_batch.py:226-238).  Survivors are compacted by
+// warp ballot + one atomic per warp into S.  `tags` (test hook) receives the
+// child's global index p*2^n + c so the host can restore reference order.
+template <int N>
+__global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
+                                                const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
+                                                int64_t* tags) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const STab tab = load_stab(meta, gtab, smem, true);
+    double* xs = reinterpret_cast<double*>(smem + stab_bytes(meta, true));
+    double* xlo = xs + threadIdx.x;
+    double* xhi = xs + N * blockDim.x + threadIdx.x;
+    const int stride = blockDim.x;
+    __syncthreads();
+    const unsigned long long total = ctr->n_par << N;
+    const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned long long ops_acc = 0, exact_acc = 0;
+    for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < total; base += gstride) {
+        const unsigned long long idx = base + threadIdx.x;
+        const bool valid = idx < total;
+        bool keep = false;
+        double w = 0.0;
+        unsigned ops = 0;
+        if (valid) {
+            const uint32_t pe = parents[idx >> N];
+            const uint32_t p = pe & 0x7fffffffu;
+            const bool exact = pe >> 31;
+            const uint32_t c = (uint32_t)(idx & ((1ull << N) - 1));
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                const double lo = cur.lo[j * cur.cap + p], hi = cur.hi[j * cur.cap + p];
+                const double m = mid_of(lo, hi);
+                const bool up = (c >> (N - 1 - j)) & 1u;
+                const double cl = up ? m : lo, ch = up ? hi : m;
+                xlo[j * stride] = cl;
+                xhi[j * stride] = ch;
+                const double d = __dsub_rn(ch, cl);
+                w = j == 0 ? d : (d > w ? d : w);
+            }
+            if (!exact) keep = feasible<N, Fast>(meta, tab, xlo, xhi, stride, ops);
+            else {
+                keep = feasible<N, Exact>(meta, tab, xlo, xhi, stride, ops);
+                exact_acc++;
+            }
+            ops_acc += ops;
+        }
+        const unsigned long long slot = warp_append(keep, &ctr->n_surv);
+        if (keep && slot < (unsigned long long)S.cap) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                S.lo[j * S.cap + slot] = xlo[j * stride];
+                S.hi[j * S.cap + slot] = xhi[j * stride];
+            }
+            if (tags) tags[slot] = (int64_t)idx;
+        }
+        unsigned long long wb = keep ? (unsigned long long)__double_as_longlong(w) : 0ull;
+        wb = warp_max(wb);
+        if ((threadIdx.x & 31) == 0 && wb) atomicMax(&ctr->child_wmax, wb);
+    }
+    ops_acc = warp_sum(ops_acc);
+    exact_acc = warp_sum(exact_acc);
+    if ((threadIdx.x & 31) == 0) {
+        if (ops_acc) atomicAdd(&ctr->filter_ops, ops_acc);
+        if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
+    }
+}
+
+// ------------------------------------------------------------------ K2 Hansen-Sengupta
+
+struct HsParams {
+    int round_no;
+    int hs_mode;           // 0: decide on device (bnb.py:289-296), 1: force on, 2: force off
+    int hs_enable_round;   // < 0: None
+    int hs_possible;
+    double hs_enable_width;// NaN: None
+    int contract_output;   // SolverConfig.hs_contract
+    int count_from_ctr;    // n_in = ctr->n_surv (clamped to S.cap) instead of n_in arg
+};
+
+template <int N>
+struct HsLayout {
+    static constexpr int G = N <= 2 ? 4 : (N <= 4 ? 8 : (N <= 8 ? 16 : 32));
+    static constexpr int BPW = 32 / G;
+    // per-group scratch (doubles)
+    static constexpr int oX = 0;              // X lo[N], hi[N]
+    static constexpr int oXm = 2 * N;         // midpoints x[N]
+    static constexpr int oFx = 3 * N;         // F(x): lo[N], hi[N]
+    static constexpr int oG = 5 * N;          // g: lo[N], hi[N]
+    static constexpr int oA = 7 * N;          // A[N*N]
+    static constexpr int oJ = 7 * N + N * N;  // J then M: lo[N*N], hi[N*N]
+    static constexpr int doubles = 7 * N + 3 * N * N;
+};
+
+enum { HS_EMPTY = 0, HS_ONE = 1, HS_TWO = 2, HS_SKIP = 3 };
+
+template <int G>
+__device__ __forceinline__ double gshfl(unsigned mask, double v, int src) {
+    return __shfl_sync(mask, v, src, G);
+}
+template <int G>
+__device__ __forceinline__ int gshfl(unsigned mask, int v, int src) {
+    return __shfl_sync(mask, v, src, G);
+}
+
+template <int G>
+__device__ __forceinline__ void group_reduce(unsigned mask, ExpRange& r) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        r.emin = min(r.emin, __shfl_xor_sync(mask, r.emin, o, G));
+        r.emax = max(r.emax, __shfl_xor_sync(mask, r.emax, o, G));
+    }
+}
+
+template <int G>
+__device__ __forceinline__ double group_max(unsigned mask, double v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(mask, v, o, G);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+// M = A * J in place over J, g = A * F(x)  (linalg.py:102-129): acc = [0,0];
+// acc += [a,a] * B[u][j] for u ascending.
+template <int N, int G, class A>
+__device__ __forceinline__ void hs_precond_products(double* s, int l, unsigned gmask) {
+    using L = HsLayout<N>;
+    constexpr int H = (N + 1) / 2;  // rows per half
+    const double* Am = s + L::oA;
+    double* Jl = s + L::oJ;
+    double* Jh = s + L::oJ + N * N;
+    ival res[H];
+    const int col = l % N, half = l / N;
+    const bool act = l < 2 * N;
+    if (act) {
+#pragma unroll
+        for (int r = 0; r < H; r++) {
+            const int i = half * H + r;
+            ival acc = mk(0.0, 0.0);
+            if (i < N) {
+#pragma unroll 4
+                for (int u = 0; u < N; u++) {
+                    const double a = Am[i * N + u];
+                    acc = A::add(acc, A::mul_point(a, mk(Jl[u * N + col], Jh[u * N + col])));
+                }
+            }
+            res[r] = acc;
+        }
+    }
+    __syncwarp(gmask);
+    if (act) {
+#pragma unroll
+        for (int r = 0; r < H; r++) {
+            const int i = half * H + r;
+            if (i < N) {
+                Jl[i * N + col] = res[r].lo;
+                Jh[i * N + col] = res[r].hi;
+            }
+        }
+    }
+    // g_i = sum_u A[i][u] * F_u(x)
+    if (l < N) {
+        ival acc = mk(0.0, 0.0);
+        for (int u = 0; u < N; u++)
+            acc = A::add(acc, A::mul_point(Am[l * N + u], mk(s[L::oFx + u], s[L::oFx + N + u])));
+        s[L::oG + l] = acc.lo;
+        s[L::oG + N + l] = acc.hi;
+    }
+}
+
+// One Hansen-Sengupta contraction of box b by one group of G lanes (hansen.py:77-138).
+// Returns the outcome kind (uniform across the group); lane j < N holds the
+// output component(s) in o0 (and o1 for a fork) and the input component in xin.
+template <int N, int G>
+__device__ int hs_box(const TabMeta& meta, const STab& tab, double* s, unsigned gmask, int l,
+                      const ival& xin, ival& o0, ival& o1, bool& certified, unsigned& exact_flags,
+                      int& rows) {
+    using L = HsLayout<N>;
+    // ---- stage X and the midpoint x (Box.midpoint, poly.py:114-115)
+    double xm = 0.0;
+    ExpRange rx, rm;
+    rx.init();
+    rm.init();
+    if (l < N) {
+        xm = mid_of(xin.lo, xin.hi);
+        s[L::oX + l] = xin.lo;
+        s[L::oX + N + l] = xin.hi;
+        s[L::oXm + l] = xm;
+        rx.add(xin.lo);
+        rx.add(xin.hi);
+        rm.add(xm);
+    }
+    group_reduce<G>(gmask, rx);
+    group_reduce<G>(gmask, rm);
+    const bool fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
+    const bool fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
+    exact_flags = (fastJ ? 0u : 1u) | (fastF ? 0u : 2u);
+    __syncwarp(gmask);
+    // ---- J(X) (hansen.py:61-63) and F(x) (hansen.py:71)
+    double* Jl = s + L::oJ;
+    double* Jh = s + L::oJ + N * N;
+    for (int e = l; e < N * N; e += G) {
+        const ival v = fastJ ? eval_poly<Fast>(tab, N + e, s + L::oX, s + L::oX + N, 1)
+                             : eval_poly_exact(tab, N + e, s + L::oX, s + L::oX + N, 1);
+        Jl[e] = v.lo;
+        Jh[e] = v.hi;
+    }
+    for (int i = l; i < N; i += G) {
+        const ival v = fastF ? eval_poly<Fast>(tab, i, s + L::oXm, s + L::oXm, 1)
+                             : eval_poly_exact(tab, i, s + L::oXm, s + L::oXm, 1);
+        s[L::oFx + i] = v.lo;
+        s[L::oFx + N + i] = v.hi;
+    }
+    __syncwarp(gmask);
+    // ---- Gauss-Jordan inverse of mid(J) (linalg.py:137-172), lane = column of [jc | I]
+    double c[N];
+    double colmax = 0.0;
+    if (l < N) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            c[i] = mid_of(Jl[i * N + l], Jh[i * N + l]);  // mid_matrix, linalg.py:132-134
+            colmax = fmax(colmax, fabs(c[i]));
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; i++) c[i] = (l - N == i) ? 1.0 : 0.0;
+    }
+    const double scale = group_max<G>(gmask, l < N ? colmax : 0.0);
+    bool singular = scale == 0.0;
+    const double threshold = __dmul_rn(1e-12, scale);
+#pragma unroll
+    for (int k = 0; k < N; k++) {
+        if (singular) break;  // group-uniform
+        // first row r >= k with max |c[r][k]| (Python max() keeps the first)
+        int pr = k;
+        double best = fabs(c[k]);
+#pragma unroll
+        for (int r = k + 1; r < N; r++)
+            if (fabs(c[r]) > best) {
+                best = fabs(c[r]);
+                pr = r;
+            }
+        double pv = c[k];
+#pragma unroll
+        for (int r = k + 1; r < N; r++)
+            if (r == pr) pv = c[r];
+        pr = gshfl<G>(gmask, pr, k);
+        const double pivot = gshfl<G>(gmask, pv, k);
+        if (fabs(pivot) < threshold) {
+            singular = true;
+            break;
+        }
+#pragma unroll
+        for (int r = k + 1; r < N; r++)
+            if (r == pr) {
+                const double t = c[k];
+                c[k] = c[r];
+                c[r] = t;
+            }
+        const double inv = __ddiv_rn(1.0, pivot);
+        double f[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) f[i] = gshfl<G>(gmask, c[i], k);
+        if (l >= k && l < 2 * N) {
+            c[k] = __dmul_rn(c[k], inv);
+#pragma unroll
+            for (int i = 0; i < N; i++)
+                if (i != k && f[i] != 0.0) c[i] = __dsub_rn(c[i], __dmul_rn(f[i], c[k]));
+        }
+    }
+    if (singular) return HS_SKIP;  // Singular -> ContractionOutcome "skipped"
+    // A = right half; lane N+u holds column u
+    double* Am = s + L::oA;
+    ExpRange ra;
+    ra.init();
+    if (l >= N && l < 2 * N) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            Am[i * N + (l - N)] = c[i];
+            ra.add(c[i]);
+        }
+    }
+    // exponent ranges of J and F(x) for the product guards
+    ExpRange rj, rf;
+    rj.init();
+    rf.init();
+    for (int e = l; e < N * N; e += G) {
+        rj.add(Jl[e]);
+        rj.add(Jh[e]);
+    }
+    if (l < N) {
+        rf.add(s[L::oFx + l]);
+        rf.add(s[L::oFx + N + l]);
+    }
+    group_reduce<G>(gmask, ra);
+    group_reduce<G>(gmask, rj);
+    group_reduce<G>(gmask, rf);
+    ExpRange rjf = rj;
+    rjf.emin = min(rj.emin, rf.emin);
+    rjf.emax = max(rj.emax, rf.emax);
+    const bool fastM = prod_guard_ok(ra, rjf);
+    if (!fastM) exact_flags |= 4u;
+    __syncwarp(gmask);
+    // ---- M = A J (in place), g = A F(x)  (hansen.py:72-73)
+    if (fastM) hs_precond_products<N, G, Fast>(s, l, gmask);
+    else hs_precond_products<N, G, Exact>(s, l, gmask);
+    __syncwarp(gmask);
+    // ---- Gauss-Seidel sweep (hansen.py:91-127); lane j keeps current[j]
+    ival cur = xin;
+    int fork_i = -1;
+    ival fp0 = mk(0.0, 0.0), fp1 = mk(0.0, 0.0);
+    const double xj = (l < N) ? xm : 0.0;
+    rows = 0;
+#pragma unroll 1
+    for (int i = 0; i < N; i++) {
+        rows = i + 1;
+        // lane j: t_j = M_ij * (current_j - [x_j, x_j])
+        ival t = mk(0.0, 0.0);
+        int nz = 0;
+        if (l < N && l != i) {
+            const ival mij = mk(Jl[i * N + l], Jh[i * N + l]);
+            nz = !(mij.lo == 0.0 && mij.hi == 0.0);
+            if (nz) t = gmul(mij, Fast::sub(cur, mk(xj, xj)));
+        }
+        // p = -g_i - sum_{j != i, M_ij != 0} t_j, left to right
+        ival p = mk(-s[L::oG + N + i], -s[L::oG + i]);
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            const double tl = gshfl<G>(gmask, t.lo, j);
+            const double th = gshfl<G>(gmask, t.hi, j);
+            const int z = gshfl<G>(gmask, nz, j);
+            if (j != i && z) p = Fast::sub(p, mk(tl, th));
+        }
+        const ival cur_i = mk(gshfl<G>(gmask, cur.lo, i), gshfl<G>(gmask, cur.hi, i));
+        const double xi = s[L::oXm + i];
+        const ival mii = mk(Jl[i * N + i], Jh[i * N + i]);
+        ival q0, q1;
+        const int kind = div_extended(p, mii, q0, q1);
+        if (kind == DIV_EMPTY) return HS_EMPTY;
+        if (kind == DIV_WHOLE) continue;
+        const int np = kind == DIV_SPLIT ? 2 : 1;
+        ival pieces[2];
+        int npieces = 0;
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            if (q < np) {
+                const ival qq = q == 0 ? q0 : q1;
+                const ival y = Fast::add(mk(xi, xi), qq);
+                const double lo = py_max(y.lo, cur_i.lo);  // Interval.intersect, interval.py:358-363
+                const double hi = py_min(y.hi, cur_i.hi);
+                if (!(lo > hi)) pieces[npieces++] = mk(lo, hi);
+            }
+        }
+        if (npieces == 0) return HS_EMPTY;
+        ival newc;
+        if (npieces == 1) {
+            newc = pieces[0];
+        } else {
+            newc = mk(py_min(pieces[0].lo, pieces[1].lo), py_max(pieces[0].hi, pieces[1].hi));  // hull
+            if (fork_i < 0) {
+                fork_i = i;
+                fp0 = pieces[0];
+                fp1 = pieces[1];
+            }
+        }
+        if (l == i) cur = newc;
+    }
+    if (fork_i < 0) {
+        // certified iff the output lies strictly inside the input (hansen.py:129-132)
+        int inside = 1;
+        if (l < N) inside = (xin.lo < cur.lo) && (cur.hi < xin.hi);
+        certified = __all_sync(gmask, inside) != 0;
+        o0 = cur;
+        return HS_ONE;
+    }
+    certified = false;
+    o0 = cur;
+    o1 = cur;
+    if (l == fork_i) {
+        o0 = fp0;
+        o1 = fp1;
+    }
+    return HS_TWO;
+}
+
+// G lanes per box; boxes assigned warp-uniformly so warp collectives stay converged.
+// Outputs are appended to `out` after the carried rows (ctr->n_next).  `tags`
+// (test hook) receives 2*row + piece to restore reference order.
+template <int N>
+__global__ void __launch_bounds__(128) k_hs(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
+                                            int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
+                                            int64_t* tags) {
+    using L = HsLayout<N>;
+    constexpr int G = L::G;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const STab tab = load_stab(meta, gtab, smem, false);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gi = lane / G;
+    const int l = lane % G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
+    double* s = reinterpret_cast<double*>(smem + stab_bytes(meta, false)) +
+                (size_t)(warp * L::BPW + gi) * L::doubles;
+    __syncthreads();
+
+    int64_t n_in = n_in_arg;
+    if (prm.count_from_ctr) {
+        const unsigned long long ns = ctr->n_surv;
+        n_in = (int64_t)(ns < (unsigned long long)S.cap ? ns : (unsigned long long)S.cap);
+    }
+    // HS trigger (bnb.py:289-296) on the max child width of the filter survivors
+    bool hs_on;
+    if (prm.hs_mode == 1) hs_on = true;
+    else if (prm.hs_mode == 2) hs_on = false;
+    else {
+        const double cw = __longlong_as_double((long long)ctr->child_wmax);
+        hs_on = false;
+        if (n_in > 0 && prm.hs_possible) {
+            if (prm.hs_enable_round >= 0 && prm.round_no >= prm.hs_enable_round) hs_on = true;
+            if (!isnan(prm.hs_enable_width) && cw <= prm.hs_enable_width) hs_on = true;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
+
+    if (!hs_on) {
+        // pass-through: survivors join the frontier uncertified (bnb.py:580-581)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x < n_in;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const bool valid = i < n_in;
+            double w = 0.0;
+            const unsigned long long slot = warp_append(valid, &ctr->n_next);
+            if (valid) {
+#pragma unroll
+                for (int j = 0; j < N; j++) {
+                    const double lo = S.lo[j * S.cap + i], hi = S.hi[j * S.cap + i];
+                    const double d = __dsub_rn(hi, lo);
+                    w = j == 0 ? d : (d > w ? d : w);
+                    if (slot < (unsigned long long)out.cap) {
+                        out.lo[j * out.cap + slot] = lo;
+                        out.hi[j * out.cap + slot] = hi;
+                    }
+                }
+                if (slot < (unsigned long long)out.cap) {
+                    out.cert[slot] = 0;
+                    out.unsplit[slot] = 0;
+                }
+                if (tags && slot < (unsigned long long)out.cap) tags[slot] = 2 * i;
+            }
+            unsigned long long wb = valid ? (unsigned long long)__double_as_longlong(w) : 0ull;
+            wb = warp_max(wb);
+            if (lane == 0 && wb) atomicMax(&ctr->wmax, wb);
+        }
+        return;
+    }
+
+    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t wglob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    unsigned long long ops_acc = 0, calls_acc = 0, exact_acc = 0;
+    for (int64_t wb0 = wglob * L::BPW; wb0 < n_in; wb0 += warps_total * L::BPW) {
+        const int64_t b = wb0 + gi;
+        const bool valid = b < n_in;
+        int kind = HS_EMPTY;
+        bool cert = false;
+        ival xin = mk(0.0, 0.0), o0 = mk(0.0, 0.0), o1 = mk(0.0, 0.0);
+        unsigned exf = 0;
+        int rows = 0;
+        if (valid) {
+            if (l < N) xin = mk(S.lo[l * S.cap + b], S.hi[l * S.cap + b]);
+            kind = hs_box<N, G>(meta, tab, s, gmask, l, xin, o0, o1, cert, exf, rows);
+            if (l == 0) {
+                calls_acc++;
+                ops_acc += meta.ops_hs_pre + (unsigned long long)meta.ops_hs_row * rows;
+                exact_acc += exf ? 1 : 0;
+            }
+        }
+        __syncwarp();
+        // outputs (bnb.py:197-210)
+        int cnt = 0;
+        bool use_input = false;
+        if (valid) {
+            if (kind == HS_SKIP) {
+                cnt = 1;
+                use_input = true;
+                cert = false;
+            } else if (kind == HS_EMPTY) {
+                cnt = 0;
+            } else if (!prm.contract_output) {
+                cnt = 1;
+                use_input = true;
+            } else {
+                cnt = kind == HS_TWO ? 2 : 1;
+            }
+        }
+        // warp prefix over groups
+        int off = 0, total = 0;
+#pragma unroll
+        for (int g = 0; g < L::BPW; g++) {
+            const int cg = __shfl_sync(0xffffffffu, cnt, g * G);
+            if (g < gi) off += cg;
+            total += cg;
+        }
+        unsigned long long base = 0;
+        if (lane == 0 && total) base = atomicAdd(&ctr->n_next, (unsigned long long)total);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        double wmax = 0.0;
+        for (int q = 0; q < cnt; q++) {
+            const unsigned long long slot = base + off + q;
+            const ival v = use_input ? xin : (q == 0 ? o0 : o1);
+            double w = 0.0;
+            if (l < N) {
+                if (slot < (unsigned long long)out.cap) {
+                    out.lo[l * out.cap + slot] = canon0(v.lo);
+                    out.hi[l * out.cap + slot] = canon0(v.hi);
+                }
+                w = __dsub_rn(v.hi, v.lo);
+            }
+            w = group_max<G>(gmask, w);
+            wmax = fmax(wmax, w);
+            if (l == 0 && slot < (unsigned long long)out.cap) {
+                out.cert[slot] = cert ? 1 : 0;
+                out.unsplit[slot] = 0;
+                if (tags) tags[slot] = 2 * b + q;
+            }
+        }
+        unsigned long long wbits = (unsigned long long)__double_as_longlong(wmax);
+        wbits = warp_max(wbits);
+        if (lane == 0 && wbits) atomicMax(&ctr->wmax, wbits);
+    }
+    ops_acc = warp_sum(ops_acc);
+    calls_acc = warp_sum(calls_acc);
+    exact_acc = warp_sum(exact_acc);
+    if (lane == 0) {
+        if (ops_acc) atomicAdd(&ctr->hs_ops, ops_acc);
+        if (calls_acc) atomicAdd(&ctr->hs_calls, calls_acc);
+        if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
+    }
+}
+
+// ------------------------------------------------------------------ dedup
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+template <int N>
+__device__ __forceinline__ unsigned long long row_hash(const Front& f, int64_t i) {
+    unsigned long long h = 0x9e3779b97f4a7c15ull;
+#pragma unroll
+    for (int j = 0; j < N; j++) {
+        h = mix64(h ^ (unsigned long long)__double_as_longlong(canon0(f.lo[j * f.cap + i])));
+        h = mix64(h ^ (unsigned long long)__double_as_longlong(canon0(f.hi[j * f.cap + i])));
+    }
+    return h;
+}
+
+template <int N>
+__device__ __forceinline__ bool rows_equal(const Front& f, int64_t a, int64_t b) {
+#pragma unroll
+    for (int j = 0; j < N; j++)
+        if (!(f.lo[j * f.cap + a] == f.lo[j * f.cap + b]) || !(f.hi[j * f.cap + a] == f.hi[j * f.cap + b]))
+            return false;
+    return true;
+}
+
+__device__ __forceinline__ void atomic_or_u8(uint8_t* p, uint8_t v) {
+    if (!v) return;
+    const size_t a = reinterpret_cast<size_t>(p);
+    unsigned* w = reinterpret_cast<unsigned*>(a & ~size_t(3));
+    atomicOr(w, (unsigned)v << (8 * (a & 3)));
+}
+
+// Open-addressing insert of every row; a row equal to an already inserted one
+// is marked dead and ORs its flags into the keeper (dedup_sorted, _batch.py:253-266).
+template <int N>
+__global__ void k_dedup_insert(Front f, int64_t n, unsigned* table, unsigned long long mask, uint8_t* dead,
+                               Counters* ctr) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long slot = row_hash<N>(f, i) & mask;
+        bool dup = false;
+        while (true) {
+            const unsigned prev = atomicCAS(&table[slot], 0u, (unsigned)(i + 1));
+            if (prev == 0u) break;
+            const int64_t k = (int64_t)prev - 1;
+            if (rows_equal<N>(f, k, i)) {
+                dup = true;
+                atomic_or_u8(&f.cert[k], f.cert[i]);
+                atomic_or_u8(&f.unsplit[k], f.unsplit[i]);
+                break;
+            }
+            slot = (slot + 1) & mask;
+        }
+        dead[i] = dup ? 1 : 0;
+        if (dup) atomicAdd(&ctr->dups, 1ull);
+    }
+}
+
+template <int N>
+__global__ void k_compact(Front src, int64_t n, const uint8_t* dead, Front dst, unsigned long long* counter) {
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool live = i < n && !dead[i];
+        const unsigned long long slot = warp_append(live, counter);
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                dst.lo[j * dst.cap + slot] = src.lo[j * src.cap + i];
+                dst.hi[j * dst.cap + slot] = src.hi[j * src.cap + i];
+            }
+            dst.cert[slot] = src.cert[i];
+            dst.unsplit[slot] = src.unsplit[i];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ canonical order
+
+__device__ __forceinline__ unsigned long long order_key(double v) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(canon0(v));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// key k of row perm[i]: k < n -> lo_k, else hi_{k-n}  (np.lexsort key order, _batch.py:247-249)
+__global__ void k_sort_keys(Front f, int n, int64_t N, int k, const unsigned* perm, unsigned long long* keys) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = perm ? perm[i] : i;
+        const double v = k < n ? f.lo[k * f.cap + r] : f.hi[(k - n) * f.cap + r];
+        keys[i] = order_key(v);
+    }
+}
+
+__global__ void k_iota(unsigned* p, int64_t N) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (unsigned)i;
+}
+
+// gather rows in perm order into row-major outputs
+__global__ void k_gather_rows(Front f, int n, int64_t N, const unsigned* perm, double* olo, double* ohi,
+                              uint8_t* ocert, uint8_t* ouns) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = perm ? perm[i] : i;
+        for (int j = 0; j < n; j++) {
+            olo[i * n + j] = canon0(f.lo[j * f.cap + r]);
+            ohi[i * n + j] = canon0(f.hi[j * f.cap + r]);
+        }
+        ocert[i] = f.cert[r];
+        ouns[i] = f.unsplit[r];
+    }
+}
+
+// row-major (host layout) -> SoA frontier rows [off, off+N)
+__global__ void k_rows_to_soa(const double* rlo, const double* rhi, const uint8_t* rc, const uint8_t* ru, int n,
+                              int64_t N, Front f, int64_t off) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        for (int j = 0; j < n; j++) {
+            f.lo[j * f.cap + off + i] = rlo[i * n + j];
+            f.hi[j * f.cap + off + i] = rhi[i * n + j];
+        }
+        if (f.cert) f.cert[off + i] = rc ? rc[i] : 0;
+        if (f.unsplit) f.unsplit[off + i] = ru ? ru[i] : 0;
+    }
+}
+
+}  // namespace rb
