@@ -113,6 +113,7 @@ struct rb_handle {
     int filter_blocks_per_sm = 1;
     int hs_blocks_per_sm = 1;
     size_t filter_smem = 0, hs_smem = 0;
+    int smem_optin = 48 * 1024;
 };
 
 // ---------------------------------------------------------------- dispatch on n
@@ -144,8 +145,12 @@ struct SetupK {
                            (size_t)(h->hs_threads / 32) * HsLayout<N>::BPW * HsLayout<N>::doubles * sizeof(double);
         h->filter_smem = fs;
         h->hs_smem = hsm;
-        ck(cudaFuncSetAttribute(k_filter<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs), "attr filter");
-        ck(cudaFuncSetAttribute(k_hs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm), "attr hs");
+        // the attribute is per kernel (shared by every handle of this n): set it to the opt-in maximum
+        if ((int)fs > h->smem_optin || (int)hsm > h->smem_optin)
+            throw ArgError{RB_ERR_LIMIT, "system tables exceed the shared-memory budget"};
+        ck(cudaFuncSetAttribute(k_filter<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin),
+           "attr filter");
+        ck(cudaFuncSetAttribute(k_hs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr hs");
         int nb = 0;
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter<N>, h->filter_threads, fs), "occ filter");
         h->filter_blocks_per_sm = std::max(1, nb);
@@ -756,6 +761,7 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         ck(cudaGetDeviceProperties(&prop, device), "props");
         if (prop.major < 10) throw ArgError{RB_ERR_CUDA, "device is not sm_100 class (B200 required)"};
         h->sms = prop.multiProcessorCount;
+        h->smem_optin = (int)prop.sharedMemPerBlockOptin;
         ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "stream");
         for (auto& e : h->ev) ck(cudaEventCreate(&e), "event");
         build_tables(h, sys);
