@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark: boxes/s and time-to-all-solutions of the interval B&B + HS solve on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+A step is one complete solve (rootbox.bnb.solve semantics, bnb.py:224-354) of
+the configured system to its target width.  Default workload: BASELINE.json
+configs[1], Broyden tridiagonal n=6 on [-2,2]^6, eps=1e-8.
+
+boxes = children evaluated by the filter (active parents x 2^n, every round)
+      + boxes contracted by Hansen-Sengupta.
+value = boxes of all ranks / max over ranks of the device time of the K steps
+        (CUDA events on the engine's stream, first to last op of each solve).
+e2e   = the same metric through the public API ``paper_1802_00330_b200.solve``
+        from host buffers: engine creation (table upload H2D), solve, result
+        fetch (D2H) and Python SolveResult construction, timed on the host.
+
+Multi-GPU (torchrun, one rank per GPU): every rank solves its own copy of the
+workload (weak scaling; replicas -- see DESIGN.md §Multi-GPU).
+
+--impl reference times the reference algorithm's CPU implementation (the C
+restatement in oracle/, all host threads) on the same workload and metric;
+rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (system, SolverConfig kwargs, description)
+    "circle_line": ("circle_line", dict(target_width=1e-6), "circle-line x^2+y^2-1, x-y on [-2,2]^2, eps=1e-6"),
+    "broyden_tri6": ("broyden_tri6", dict(target_width=1e-8), "Broyden tridiagonal n=6 on [-2,2]^6, eps=1e-8"),
+    "katsura6": ("katsura6", dict(), "Katsura-6 (7 vars) on [-1,1]^7, default eps 2^-9, HS width 1.0"),
+    "eco8": ("eco8", dict(), "eco8 on [-8,8]^8, default eps 2^-6, HS width 1.0"),
+    "brown8": ("brown8", dict(target_width=1e-8), "Brown almost-linear n=8 on [-2,2]^8, eps=1e-8"),
+    "broyden_banded12": ("broyden_banded12", dict(target_width=1e-8),
+                         "Broyden banded n=12 on [-1,1]^12, eps=1e-8"),
+}
+
+
+def load_spec(name):
+    from paper_1802_00330_b200 import SystemSpec
+    with open(os.path.join(ROOT, "tests", "golden", "systems.json")) as f:
+        d = json.load(f)["systems"][name]
+    return SystemSpec.from_json(d, name=name)
+
+
+def boxes_of(stats):
+    return int(sum(s["children"] + s["hs_calls"] for s in stats))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def l2_flush(buf):
+    if buf is not None:
+        buf.add_(1.0)  # 512 MiB read+write > 126 MB L2
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(world, v, local):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(world, v, local):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def cpu_baseline(spec, kw, budget_s=10.0, threads=None):
+    """The oracle (C restatement of the reference algorithm) on the host cores:
+    repeated full solves of the same workload for ~budget_s seconds."""
+    from oracle import oracle as O
+    threads = threads or os.cpu_count() or 1
+    osys = O.OSystem(spec.n, spec.eqs, spec.jac)
+    reps, boxes, t_total = 0, 0, 0.0
+    status = None
+    while t_total < budget_s and reps < 1000:
+        t0 = time.perf_counter()
+        r = osys.solve(spec.init_lo, spec.init_hi, threads=threads, **kw)
+        t_total += time.perf_counter() - t0
+        boxes += int(r["stats"][:, 6].sum() + r["stats"][:, 7].sum())
+        status = r["status"]
+        reps += 1
+    return {"value": boxes / t_total, "unit": "boxes/s", "cores": threads, "kind": "port",
+            "sample": f"{reps} complete solve(s) of the same workload ({status}), "
+                      f"{t_total:.2f} s of CPU wall time, oracle/rootbox_oracle.c with {threads} threads",
+            "time_to_solution_s": t_total / reps}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    sysname, kw, desc = CONFIGS[args.config]
+    spec = load_spec(sysname)
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    osys = O.OSystem(spec.n, spec.eqs, spec.jac)
+    for _ in range(args.warmup):
+        osys.solve(spec.init_lo, spec.init_hi, threads=threads, **kw)
+    times, boxes = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = osys.solve(spec.init_lo, spec.init_hi, threads=threads, **kw)
+        times.append(time.perf_counter() - t0)
+        boxes += int(r["stats"][:, 6].sum() + r["stats"][:, 7].sum())
+    total = sum(times)
+    value = boxes / total
+    line = {
+        "impl": "reference", "metric": "boxes/s (children evaluated + HS boxes contracted) per complete solve",
+        "value": value, "unit": "boxes/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic benchmark system)",
+        "config": {"workload": desc, "system": sysname, "time_to_solution_s": total / args.steps},
+        "cpu_baseline": {"value": value, "unit": "boxes/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} complete solves, oracle/rootbox_oracle.c with {threads} threads"},
+        "e2e": {"value": value, "unit": "boxes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_1802_00330_b200 import SolverConfig, _native, bnb
+    sysname, kw, desc = CONFIGS[args.config]
+    spec = load_spec(sysname)
+    cfg = SolverConfig(**kw)
+    torch.cuda.set_device(local)
+    flush = torch.zeros(128 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 512 MiB
+    eng = bnb.engine_for(spec, local)
+    ncfg = bnb.native_config(cfg)
+    for _ in range(max(3, args.warmup)):
+        out = eng.solve(ncfg)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    sampler.start()
+    dev_ms, boxes, launches = [], 0, 0
+    filt_ms = hs_ms = cls_ms = 0.0
+    filt_ops = hs_ops = cls_bytes = 0
+    t_wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        l2_flush(flush)
+        torch.cuda.synchronize()
+        out = eng.solve(ncfg)
+        dev_ms.append(out["device_ms"])
+        boxes += boxes_of(out["stats"])
+        launches += out["kernel_launches"]
+        for s in out["stats"]:
+            filt_ms += s["filter_ms"]; hs_ms += s["hs_ms"]; cls_ms += s["classify_ms"]
+            filt_ops += s["filter_ops"]; hs_ops += s["hs_ops"]; cls_bytes += s["classify_bytes"]
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall0
+    barrier(world)
+    clocks = sampler.stop()
+    t_dev = sum(dev_ms) * 1e-3
+    t_max = allreduce_max(world, t_dev, local)
+    boxes_all = allreduce_sum(world, boxes, local)
+    value = boxes_all / t_max
+    status = out["status"]
+    nrounds = len(out["stats"])
+    nfinal = out["lo"].shape[0]
+
+    # ---- e2e through the public API from host buffers (cold engine each step)
+    from paper_1802_00330_b200 import solve as public_solve
+    from paper_1802_00330_b200.system import compile_tables
+    e2e_steps = max(3, min(args.steps, 20))
+    bnb._ENGINES.clear()
+    tabs = compile_tables(spec)
+    h2d = sum(a.nbytes for a in (tabs.poly_off, tabs.coeff, tabs.fac_off, tabs.fac_var, tabs.fac_exp,
+                                 tabs.init_lo, tabs.init_hi))
+    e2e_t, e2e_boxes, d2h = [], 0, 0
+    for _ in range(e2e_steps):
+        bnb._ENGINES.clear()
+        t0 = time.perf_counter()
+        res = public_solve(spec, cfg)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_boxes = boxes_of(out["stats"]) * e2e_steps
+    d2h = nfinal * spec.n * 16 + 2 * nfinal + nrounds * 152
+    e2e_value = allreduce_sum(world, e2e_boxes, local) / allreduce_max(world, sum(e2e_t), local)
+    assert len(res.boxes) == nfinal and res.status == status
+    # warm-engine e2e (system compiled once, solved repeatedly: the serving case)
+    warm_t = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        public_solve(spec, cfg)
+        warm_t.append(time.perf_counter() - t0)
+
+    # ---- roofline of the dominant kernel (FP64 directed-op pipe)
+    peak = _native.fp64_peak(local)
+    if hs_ms >= filt_ms:
+        dom, ops, ms = "k_hs (Hansen-Sengupta)", hs_ops, hs_ms
+    else:
+        dom, ops, ms = "k_filter (bisect+inclusion filter+compaction)", filt_ops, filt_ms
+    achieved = ops / (ms * 1e-3) if ms > 0 else 0.0
+    roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved / 1e12, "peak": peak / 1e12,
+                "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
+                "note": "1 directed FP64 op (DMUL/DADD.RM/RP) = 1 FLOP; peak = measured directed-op throughput "
+                        "of this B200 (rb_fp64_peak microbenchmark); algorithmic ops per SURVEY §8(d)",
+                "share_of_step": {"filter_ms": filt_ms / args.steps, "hs_ms": hs_ms / args.steps,
+                                  "classify_ms": cls_ms / args.steps,
+                                  "device_ms": sum(dev_ms) / args.steps},
+                "classify_hbm_gbs": (cls_bytes / (cls_ms * 1e-3) / 1e9) if cls_ms > 0 else None}
+
+    line = {
+        "metric": "boxes/s (children evaluated + HS boxes contracted) per complete solve",
+        "value": value, "unit": "boxes/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sum(dev_ms) / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic benchmark system)",
+        "config": {"workload": desc, "system": sysname, "status": status, "rounds": nrounds,
+                   "final_boxes": nfinal, "boxes_per_step": boxes // args.steps,
+                   "time_to_solution_ms": sum(dev_ms) / args.steps,
+                   "l2": "flushed between steps (512 MiB write)", "parallelism": f"replicas x{world}",
+                   "host_wall_ms_per_step": 1e3 * wall / args.steps},
+        "e2e": {"value": e2e_value, "unit": "boxes/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "time_to_solution_ms": 1e3 * statistics.mean(e2e_t),
+                "path": "paper_1802_00330_b200.solve(spec, cfg) -> SolveResult, cold engine (rb_create) each step",
+                "warm_engine_ms": 1e3 * statistics.mean(warm_t)},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(spec, kw, budget_s=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="broyden_tri6")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank)
+        else:
+            run_ours(args, world, rank, local)
+    finally:
+        if world > 1 and args.impl == "ours":
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -95,6 +95,7 @@ typedef struct rb_round_stats {
     double hs_ms;              /* device time of the HS kernel(s)               */
     double classify_ms;        /* device time of the classify/compaction kernel */
     int64_t classify_bytes;    /* algorithmic HBM bytes of the classify kernel  */
+    int64_t attempts;          /* 1 + redos after a buffer had to grow          */
 } rb_round_stats;
 
 typedef struct rb_result_info {
@@ -102,6 +103,8 @@ typedef struct rb_result_info {
     int32_t nrounds;
     int64_t nboxes;
     double solve_seconds;      /* host wall time inside rb_solve */
+    double device_ms;          /* CUDA-event time on the engine stream, first to last op */
+    int64_t kernel_launches;   /* engine kernels launched by this solve (CUB sort passes excluded) */
 } rb_result_info;
 
 typedef struct rb_handle rb_handle;
@@ -177,6 +180,12 @@ int rb_shard_import(rb_handle* h, int64_t keep, const double* lo, const double* 
 
 /* Current frontier size of the shard. */
 int64_t rb_shard_size(rb_handle* h);
+
+/* ---- measurement utility ----------------------------------------------------
+ * Measured throughput of the FP64 pipe on `device` for the directed-rounding
+ * instructions the engine issues (DMUL.RM/RP, DADD.RM/RP; one op each), in
+ * ops/s: the roofline denominator for the filter and HS kernels. */
+int rb_fp64_peak(int device, double* ops_per_second);
 
 #ifdef __cplusplus
 }

@@ -44,13 +44,13 @@ class RbRoundStats(C.Structure):
         ("children", C.c_int64), ("hs_calls", C.c_int64), ("filter_ops", C.c_int64), ("hs_ops", C.c_int64),
         ("dups", C.c_int64), ("exact_boxes", C.c_int64),
         ("filter_ms", C.c_double), ("hs_ms", C.c_double), ("classify_ms", C.c_double),
-        ("classify_bytes", C.c_int64),
+        ("classify_bytes", C.c_int64), ("attempts", C.c_int64),
     ]
 
 
 class RbResultInfo(C.Structure):
     _fields_ = [("status", C.c_int32), ("nrounds", C.c_int32), ("nboxes", C.c_int64),
-                ("solve_seconds", C.c_double)]
+                ("solve_seconds", C.c_double), ("device_ms", C.c_double), ("kernel_launches", C.c_int64)]
 
 
 STATS_FIELDS = [f for f, _ in RbRoundStats._fields_]
@@ -101,13 +101,15 @@ def lib():
     L.rb_shard_import.restype = i32
     L.rb_shard_size.argtypes = [P]
     L.rb_shard_size.restype = i64
+    L.rb_fp64_peak.argtypes = [i32, C.POINTER(C.c_double)]
+    L.rb_fp64_peak.restype = i32
     _lib = L
     return L
 
 
 EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch", "rb_filter", "rb_hs",
             "rb_last_error", "rb_destroy", "rb_shard_load", "rb_round_filter", "rb_round_hs",
-            "rb_shard_export", "rb_shard_import", "rb_shard_size"]
+            "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak"]
 
 
 def _p(a):
@@ -168,7 +170,8 @@ class Engine:
                "rb_fetch")
         st = [{f: getattr(stats[i], f) for f in STATS_FIELDS} for i in range(info.nrounds)]
         return {"status": STATUS_NAMES[info.status], "lo": lo, "hi": hi, "cert": cert.astype(bool),
-                "unsplit": uns.astype(bool), "stats": st, "solve_seconds": info.solve_seconds}
+                "unsplit": uns.astype(bool), "stats": st, "solve_seconds": info.solve_seconds,
+                "device_ms": info.device_ms, "kernel_launches": int(info.kernel_launches)}
 
     def filter(self, plo, phi):
         plo = np.ascontiguousarray(plo, np.float64); phi = np.ascontiguousarray(phi, np.float64)
@@ -198,6 +201,13 @@ class Engine:
 
 def device_count() -> int:
     return int(lib().rb_device_count())
+
+
+def fp64_peak(device: int = 0) -> float:
+    """Measured directed-rounding FP64 op throughput (ops/s) of the device."""
+    v = C.c_double()
+    _check(lib().rb_fp64_peak(int(device), C.byref(v)), None, "rb_fp64_peak")
+    return v.value
 
 
 def version() -> str:

@@ -68,7 +68,8 @@ struct rb_handle {
     int n = 0;
     int sms = 148;
     cudaStream_t st = nullptr;
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev[8] = {};
+    int64_t launches = 0;
     TabMeta meta{};
     uint8_t* d_tab = nullptr;
     std::vector<double> init_lo, init_hi;
@@ -83,11 +84,14 @@ struct rb_handle {
     Counters* h_ctr = nullptr;  // pinned
     int64_t* d_tags = nullptr;
     int64_t cap_tags = 0;
-    // dedup scratch
+    // dedup scratch (table kept all-zero between rounds)
     unsigned* d_table = nullptr;
     size_t table_slots = 0;
+    unsigned* d_slot = nullptr;
     uint8_t* d_dead = nullptr;
     int64_t cap_dead = 0;
+    // capacity prediction from the previous round
+    size_t mem_budget = 0;     // bytes the engine may hold
     // sort scratch
     void* d_cub = nullptr;
     size_t cub_bytes = 0;
@@ -106,6 +110,7 @@ struct rb_handle {
     double shard_target = 0.0;
     int64_t shard_carried = 0;
     int shard_round = 0;
+    int64_t shard_need_f = 0;
     std::string err;
     // launch shapes
     int filter_threads = 256;
@@ -164,6 +169,7 @@ struct ClassifyK {
     static void run(rb_handle* h, double target) {
         Front cur = h->F[h->cur].f, next = h->F[h->cur ^ 1].f;
         const int blocks = grid_for(h->n_cur, 256, h->sms * 8);
+        h->launches++;
         k_classify<N><<<blocks, 256, 0, h->st>>>(h->meta, cur, h->n_cur, next, h->parents, h->d_ctr, target);
         ck(cudaGetLastError(), "classify launch");
     }
@@ -173,6 +179,7 @@ template <int N>
 struct AllParentsK {
     static void run(rb_handle* h) {
         const int blocks = grid_for(h->n_cur, 256, h->sms * 8);
+        h->launches++;
         k_all_parents<N><<<blocks, 256, 0, h->st>>>(h->meta, h->F[h->cur].f, h->n_cur, h->parents, h->d_ctr);
         ck(cudaGetLastError(), "parents launch");
     }
@@ -183,6 +190,7 @@ struct FilterK {
     static void run(rb_handle* h, int64_t max_parents, int64_t* tags) {
         const int64_t work = max_parents << N;
         const int blocks = grid_for(work, h->filter_threads, h->sms * h->filter_blocks_per_sm);
+        h->launches++;
         k_filter<N><<<blocks, h->filter_threads, h->filter_smem, h->st>>>(h->meta, h->d_tab, h->F[h->cur].f,
                                                                          h->parents, h->d_ctr, h->S, tags);
         ck(cudaGetLastError(), "filter launch");
@@ -194,6 +202,7 @@ struct HsK {
     static void run(rb_handle* h, int64_t max_in, int64_t n_in, HsParams prm, int64_t* tags) {
         const int per_block_boxes = (h->hs_threads / 32) * HsLayout<N>::BPW;
         const int blocks = grid_for(max_in * 1, per_block_boxes, h->sms * h->hs_blocks_per_sm);
+        h->launches++;
         k_hs<N><<<std::max(blocks, 1), h->hs_threads, h->hs_smem, h->st>>>(
             h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
         ck(cudaGetLastError(), "hs launch");
@@ -202,20 +211,15 @@ struct HsK {
 
 template <int N>
 struct DedupK {
-    static void run(rb_handle* h, Front f, int64_t n, size_t slots) {
-        const int blocks = grid_for(n, 256, h->sms * 8);
-        k_dedup_insert<N><<<blocks, 256, 0, h->st>>>(f, n, h->d_table, (unsigned long long)(slots - 1),
-                                                     h->d_dead, h->d_ctr);
+    static void run(rb_handle* h, Front next, Front other) {
+        // persistent grids: the row count is read on the device
+        const int blocks = grid_for(next.cap, 256, h->sms * 8);
+        h->launches += 2;
+        k_dedup_insert<N><<<blocks, 256, 0, h->st>>>(next, h->d_table, (unsigned long long)(h->table_slots - 1),
+                                                     h->d_slot, h->d_dead, h->d_ctr, h->S.cap);
+        k_dedup_finish<N><<<blocks, 256, 0, h->st>>>(next, other, h->d_table, h->d_slot, h->d_dead, h->d_ctr,
+                                                     h->S.cap);
         ck(cudaGetLastError(), "dedup launch");
-    }
-};
-
-template <int N>
-struct CompactK {
-    static void run(rb_handle* h, Front src, int64_t n, Front dst, unsigned long long* counter) {
-        const int blocks = grid_for(n, 256, h->sms * 8);
-        k_compact<N><<<blocks, 256, 0, h->st>>>(src, n, h->d_dead, dst, counter);
-        ck(cudaGetLastError(), "compact launch");
     }
 };
 
@@ -408,6 +412,7 @@ static void load_rows(rb_handle* h, DevFront& F, int64_t off, const double* lo, 
         dalloc(&du, (size_t)N);
         ck(cudaMemcpyAsync(du, uns, N, cudaMemcpyHostToDevice, h->st), "rows h2d");
     }
+    h->launches++;
     k_rows_to_soa<<<grid_for(N, 256, h->sms * 8), 256, 0, h->st>>>(dlo, dhi, dc, du, n, N, F.f, off);
     ck(cudaGetLastError(), "rows_to_soa");
     ck(cudaStreamSynchronize(h->st), "rows sync");
@@ -423,121 +428,119 @@ struct RoundOut {
     bool hs_on;
     unsigned long long filter_ops, hs_ops;
     double classify_ms, filter_ms, hs_ms;
+    int attempts;
 };
 
-// classify + filter, with overflow retry of the survivor buffer
-static void round_filter(rb_handle* h, double target, RoundOut& ro) {
-    const int n = h->n;
-    DevFront& next = h->F[h->cur ^ 1];
-    // the carried rows can never exceed the current frontier
-    front_reserve(h, next, std::max<int64_t>(h->n_cur, 1), 0);
-    parents_reserve(h, std::max<int64_t>(h->n_cur, 1));
-    surv_reserve(h, std::max<int64_t>(h->S.cap, 4096));
-    ck(cudaMemsetAsync(h->d_ctr, 0, sizeof(Counters), h->st), "ctr memset");
-    ck(cudaEventRecord(h->ev[0], h->st), "ev");
-    if (h->n_cur > 0) dispatch_n<ClassifyK>(n, h, target);
-    ck(cudaEventRecord(h->ev[1], h->st), "ev");
-    if (h->n_cur > 0) dispatch_n<FilterK>(n, h, h->n_cur, (int64_t*)nullptr);
-    ck(cudaEventRecord(h->ev[2], h->st), "ev");
-    sync_counters(h);
-    if (h->h_ctr->n_surv > (unsigned long long)h->S.cap) {
-        // retry the filter into a buffer of the exact size
-        surv_reserve(h, (int64_t)h->h_ctr->n_surv);
-        Counters c = *h->h_ctr;
-        c.n_surv = 0;
-        c.child_wmax = 0;
-        c.filter_ops = 0;
-        c.exact_boxes = 0;
-        ck(cudaMemcpyAsync(h->d_ctr, &c, sizeof(Counters), cudaMemcpyHostToDevice, h->st), "ctr h2d");
-        ck(cudaEventRecord(h->ev[1], h->st), "ev");
-        dispatch_n<FilterK>(n, h, h->n_cur, (int64_t*)nullptr);
-        ck(cudaEventRecord(h->ev[2], h->st), "ev");
-        sync_counters(h);
+// both frontier buffers share one capacity (the dedup compaction may target
+// either); the current one keeps its rows when grown
+static void fronts_reserve(rb_handle* h, int64_t need) {
+    front_reserve(h, h->F[h->cur], need, h->n_cur);
+    front_reserve(h, h->F[h->cur ^ 1], h->F[h->cur].f.cap, 0);
+    if (h->F[h->cur ^ 1].f.cap != h->F[h->cur].f.cap) front_reserve(h, h->F[h->cur], h->F[h->cur ^ 1].f.cap, h->n_cur);
+    const int64_t cap = h->F[h->cur].f.cap;
+    if (h->cap_dead < cap || !h->d_dead) {
+        dalloc(&h->d_dead, (size_t)cap);
+        dalloc(&h->d_slot, (size_t)cap);
+        h->cap_dead = cap;
     }
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
-    ro.classify_ms = ms;
-    cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]);
-    ro.filter_ms = ms;
-    ro.boxes_in = h->n_cur;
-    ro.carried = (int64_t)h->h_ctr->n_carried;
-    ro.survivors = (int64_t)h->h_ctr->n_surv;
-    ro.children = (int64_t)(h->h_ctr->n_par << n);
-    ro.child_width = bits_to_double(h->h_ctr->child_wmax);
-    ro.filter_ops = h->h_ctr->filter_ops;
-    ro.exact = (int64_t)h->h_ctr->exact_boxes;
+    size_t slots = 1;
+    while (slots < (size_t)(2 * cap)) slots <<= 1;
+    if (slots > h->table_slots || !h->d_table) {
+        dalloc(&h->d_table, slots);
+        ck(cudaMemsetAsync(h->d_table, 0, slots * sizeof(unsigned), h->st), "table memset");
+        h->table_slots = slots;
+    }
 }
 
-// HS (or pass-through) into F_next after the carried rows, with overflow retry; then dedup
-static void round_hs(rb_handle* h, const HsParams& prm0, bool dedup, RoundOut& ro) {
+static void record(rb_handle* h, int i) { ck(cudaEventRecord(h->ev[i], h->st), "event"); }
+
+static float elapsed(rb_handle* h, int a, int b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]);
+    return ms;
+}
+
+// K3 classify + K1 filter (no sync)
+static void launch_filter_phase(rb_handle* h, double target) {
     const int n = h->n;
-    DevFront& next = h->F[h->cur ^ 1];
-    const int64_t carried = ro.carried;
-    const int64_t surv = ro.survivors;
+    ck(cudaMemsetAsync(h->d_ctr, 0, sizeof(Counters), h->st), "ctr memset");
+    record(h, 0);
+    if (h->n_cur > 0) dispatch_n<ClassifyK>(n, h, target);
+    record(h, 1);
+    if (h->n_cur > 0) dispatch_n<FilterK>(n, h, h->n_cur, (int64_t*)nullptr);
+    record(h, 2);
+}
+
+// K2 HS (or pass-through) + exact dedup (no sync)
+static void launch_hs_phase(rb_handle* h, const HsParams& prm0, bool dedup) {
     HsParams prm = prm0;
     prm.count_from_ctr = 1;
-    // F_next must hold carried + up to 2 outputs per survivor; try the current
-    // capacity first (forks are rare), grow exactly on overflow
-    front_reserve(h, next, carried + surv + 1, carried);
-    ck(cudaEventRecord(h->ev[3], h->st), "ev");
-    if (surv > 0) dispatch_n<HsK>(n, h, surv, (int64_t)0, prm, (int64_t*)nullptr);
-    ck(cudaEventRecord(h->ev[4], h->st), "ev");
-    sync_counters(h);
-    if (h->h_ctr->n_next > (unsigned long long)next.f.cap) {
-        front_reserve(h, next, (int64_t)h->h_ctr->n_next, carried);
-        Counters c = *h->h_ctr;
-        c.n_next = carried;  // keep wmax: a max over the same rows the retry rewrites
-        c.hs_ops = 0;
-        c.hs_calls = 0;
-        c.exact_boxes = 0;
-        ck(cudaMemcpyAsync(h->d_ctr, &c, sizeof(Counters), cudaMemcpyHostToDevice, h->st), "ctr h2d");
-        ck(cudaEventRecord(h->ev[3], h->st), "ev");
-        dispatch_n<HsK>(n, h, surv, (int64_t)0, prm, (int64_t*)nullptr);
-        ck(cudaEventRecord(h->ev[4], h->st), "ev");
+    if (h->n_cur > 0) dispatch_n<HsK>(h->n, h, std::min<int64_t>(h->S.cap, h->n_cur << h->n), (int64_t)0, prm,
+                                      (int64_t*)nullptr);
+    record(h, 3);
+    if (dedup) dispatch_n<DedupK>(h->n, h, h->F[h->cur ^ 1].f, h->F[h->cur].f);
+}
+
+// Capacities for the coming round.  S keeps the largest size a round has
+// needed (it grows, with a redo, when a round overflows it); F is sized so that
+// it can never overflow: carried rows <= n_cur and HS emits <= 2 rows per survivor.
+static void plan_capacity(rb_handle* h, int64_t& need_s, int64_t& need_f) {
+    need_s = std::max<int64_t>(h->S.cap, 4096);
+    need_f = h->n_cur + 2 * need_s + 1;
+}
+static void fill_round_out(rb_handle* h, RoundOut& ro) {
+    const Counters& c = *h->h_ctr;
+    ro.boxes_in = h->n_cur;
+    ro.carried = (int64_t)c.n_carried;
+    ro.survivors = (int64_t)c.n_surv;
+    ro.children = (int64_t)(c.n_par << h->n);
+    ro.child_width = bits_to_double(c.child_wmax);
+    ro.filter_ops = c.filter_ops;
+    ro.exact = (int64_t)c.exact_boxes;
+    ro.hs_on = c.hs_on != 0;
+    ro.hs_calls = (int64_t)c.hs_calls;
+    ro.hs_ops = c.hs_ops;
+    ro.width = bits_to_double(c.wmax);
+    ro.dups = (int64_t)c.dups;
+    ro.after_hs = (int64_t)c.n_next - ro.dups;
+}
+
+// After a completed round: make F[cur] the new frontier.
+static void commit_round(rb_handle* h, RoundOut& ro) {
+    if (ro.dups == 0) h->cur ^= 1;  // else k_dedup_finish compacted into F[cur]
+    h->n_cur = ro.after_hs;
+}
+
+// One round of bnb.solve (bnb.py:248-337) with a single host sync; buffers that
+// turn out too small are grown and the round is redone (the input is untouched).
+static void run_round(rb_handle* h, double target, const HsParams& prm, bool dedup, RoundOut& ro) {
+    int64_t need_s, need_f;
+    plan_capacity(h, need_s, need_f);
+    for (int attempt = 1;; attempt++) {
+        fronts_reserve(h, need_f);
+        surv_reserve(h, need_s);
+        parents_reserve(h, std::max<int64_t>(h->n_cur, 1));
+        launch_filter_phase(h, target);
+        launch_hs_phase(h, prm, dedup);
+        record(h, 4);
         sync_counters(h);
+        const Counters& c = *h->h_ctr;
+        if (c.n_surv > (unsigned long long)h->S.cap) {
+            need_s = (int64_t)(c.n_surv + c.n_surv / 4);
+            need_f = h->n_cur + 2 * need_s + 1;
+            continue;
+        }
+        if (c.n_next > (unsigned long long)h->F[h->cur ^ 1].f.cap) {  // cannot happen (see plan_capacity)
+            need_f = (int64_t)(c.n_next + c.n_next / 4);
+            continue;
+        }
+        fill_round_out(h, ro);
+        ro.attempts = attempt;
+        ro.classify_ms = elapsed(h, 0, 1);
+        ro.filter_ms = elapsed(h, 1, 2);
+        ro.hs_ms = elapsed(h, 2, 3);
+        return;
     }
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
-    ro.hs_ms = ms;
-    ro.hs_on = h->h_ctr->hs_on != 0;
-    ro.hs_calls = (int64_t)h->h_ctr->hs_calls;
-    ro.hs_ops = h->h_ctr->hs_ops;
-    ro.exact = (int64_t)h->h_ctr->exact_boxes;
-    int64_t n_next = (int64_t)h->h_ctr->n_next;
-    ro.width = bits_to_double(h->h_ctr->wmax);
-    ro.dups = 0;
-    if (dedup && n_next >= 2) {
-        // open-addressing table of >= 2 n slots (power of two)
-        size_t slots = 1;
-        while (slots < (size_t)(2 * n_next)) slots <<= 1;
-        if (slots > h->table_slots || !h->d_table) {
-            dalloc(&h->d_table, slots);
-            h->table_slots = slots;
-        }
-        if (h->cap_dead < n_next || !h->d_dead) {
-            dalloc(&h->d_dead, (size_t)grow_cap(n_next));
-            h->cap_dead = grow_cap(n_next);
-        }
-        // use exactly `slots` entries (mask = slots - 1)
-        ck(cudaMemsetAsync(h->d_table, 0, slots * sizeof(unsigned), h->st), "table memset");
-        dispatch_n<DedupK>(n, h, next.f, n_next, slots);
-        sync_counters(h);
-        const int64_t dups = (int64_t)h->h_ctr->dups;
-        if (dups > 0) {
-            DevFront& other = h->F[h->cur];  // consumed input frontier, free now
-            front_reserve(h, other, n_next - dups, 0);
-            unsigned long long* cnt = &h->d_ctr->pad[0];
-            ck(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), h->st), "cnt memset");
-            dispatch_n<CompactK>(n, h, next.f, n_next, other.f, cnt);
-            ck(cudaStreamSynchronize(h->st), "compact sync");
-            // the compacted frontier now lives in F[cur]; swap roles so that
-            // F[cur ^ 1] is the next frontier
-            std::swap(h->F[0], h->F[1]);
-            n_next -= dups;
-        }
-        ro.dups = dups;
-    }
-    ro.after_hs = n_next;
 }
 
 static void release_all(rb_handle* h) {
@@ -553,6 +556,7 @@ static void release_all(rb_handle* h) {
     fr(h->d_tags);
     fr(h->d_table);
     fr(h->d_dead);
+    fr(h->d_slot);
     fr(h->d_cub);
     fr(h->d_keys[0]);
     fr(h->d_keys[1]);
@@ -596,11 +600,13 @@ static void finalize_sorted(rb_handle* h) {
             h->cub_bytes = bytes;
         }
         const int blocks = grid_for(N, 256, h->sms * 8);
+        h->launches++;
         k_iota<<<blocks, 256, 0, h->st>>>(h->d_perm[0], N);
         // LSD over the 2n keys of np.lexsort order: least significant first (hi_{n-1}), most
         // significant last (lo_0); each pass is a stable radix sort.
         int cur = 0;
         for (int k = 2 * n - 1; k >= 0; k--) {
+            h->launches++;
             k_sort_keys<<<blocks, 256, 0, h->st>>>(f, n, N, k, h->d_perm[cur], h->d_keys[0]);
             size_t bytes = h->cub_bytes;
             ck(cub::DeviceRadixSort::SortPairs(h->d_cub, bytes, h->d_keys[0], h->d_keys[1], h->d_perm[cur],
@@ -610,6 +616,7 @@ static void finalize_sorted(rb_handle* h) {
         }
         perm = h->d_perm[cur];
     }
+    h->launches++;
     k_gather_rows<<<grid_for(N, 256, h->sms * 8), 256, 0, h->st>>>(f, n, N, perm, h->r_lo, h->r_hi, h->r_cert,
                                                                     h->r_uns);
     ck(cudaGetLastError(), "gather");
@@ -624,17 +631,24 @@ static double now_s() {
 static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info) {
     const int n = h->n;
     const double t_start = now_s();
+    h->launches = 0;
+    ck(cudaEventRecord(h->ev[5], h->st), "ev start");
     h->stats.clear();
     h->have_result = false;
     if (cfg->max_rounds < 1) throw ArgError{RB_ERR_ARG, "max_rounds must be at least 1"};
     if (cfg->max_boxes < 1) throw ArgError{RB_ERR_ARG, "max_boxes must be at least 1"};
-    // initial frontier = the initial box (bnb.py:229-232)
-    front_reserve(h, h->F[0], 4096, 0);
-    front_reserve(h, h->F[1], 4096, 0);
+    // initial frontier = the initial box (bnb.py:229-232): strided H2D into column 0
     h->cur = 0;
+    h->n_cur = 0;
+    fronts_reserve(h, 4096);
     {
-        uint8_t z = 0;
-        load_rows(h, h->F[0], 0, h->init_lo.data(), h->init_hi.data(), &z, &z, 1);
+        Front f = h->F[0].f;
+        ck(cudaMemcpy2DAsync(f.lo, f.cap * sizeof(double), h->init_lo.data(), sizeof(double), sizeof(double), n,
+                             cudaMemcpyHostToDevice, h->st), "init lo");
+        ck(cudaMemcpy2DAsync(f.hi, f.cap * sizeof(double), h->init_hi.data(), sizeof(double), sizeof(double), n,
+                             cudaMemcpyHostToDevice, h->st), "init hi");
+        ck(cudaMemsetAsync(f.cert, 0, 1, h->st), "init cert");
+        ck(cudaMemsetAsync(f.unsplit, 0, 1, h->st), "init uns");
     }
     h->n_cur = 1;
     double init_width = 0.0;
@@ -653,7 +667,6 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
         for (int round_no = 1; round_no <= cfg->max_rounds; round_no++) {
             const double t0 = now_s();
             RoundOut ro{};
-            round_filter(h, target, ro);
             HsParams prm{};
             prm.round_no = round_no;
             prm.hs_mode = 0;
@@ -661,9 +674,8 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
             prm.hs_possible = hs_possible ? 1 : 0;
             prm.hs_enable_width = cfg->hs_enable_width;
             prm.contract_output = cfg->hs_contract ? 1 : 0;
-            round_hs(h, prm, cfg->exact_round_dedup != 0, ro);
-            h->cur ^= 1;
-            h->n_cur = ro.after_hs;
+            run_round(h, target, prm, cfg->exact_round_dedup != 0, ro);
+            commit_round(h, ro);
             rb_round_stats st{};
             st.round = round_no;
             st.hs_on = ro.hs_on;
@@ -680,7 +692,8 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
             st.filter_ms = ro.filter_ms;
             st.hs_ms = ro.hs_ms;
             st.classify_ms = ro.classify_ms;
-            // classify reads every row (16n + 2 B) and writes carried rows + 4 B per parent
+            st.attempts = ro.attempts;
+            // classify reads every row (16n + 2 B) and writes carried rows (16n + 2 B) + 4 B per parent
             st.classify_bytes = ro.boxes_in * (16 * n + 2) + ro.carried * (16 * n + 2) +
                                 (ro.boxes_in - ro.carried) * 4;
             st.elapsed_seconds = now_s() - t0;
@@ -705,8 +718,14 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
         }
     }
     finalize_sorted(h);
+    ck(cudaEventRecord(h->ev[6], h->st), "ev end");
+    ck(cudaEventSynchronize(h->ev[6]), "ev sync");
+    float dev_ms = 0.f;
+    cudaEventElapsedTime(&dev_ms, h->ev[5], h->ev[6]);
     h->have_result = true;
     if (info) {
+        info->device_ms = dev_ms;
+        info->kernel_launches = h->launches;
         info->status = status;
         info->nrounds = (int32_t)h->stats.size();
         info->nboxes = h->r_n;
@@ -765,6 +784,9 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "stream");
         for (auto& e : h->ev) ck(cudaEventCreate(&e), "event");
         build_tables(h, sys);
+        size_t free_b = 0, total_b = 0;
+        ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
+        h->mem_budget = (size_t)(0.80 * (double)free_b);
         dalloc(&h->d_ctr, 1);
         ck(cudaMallocHost((void**)&h->h_ctr, sizeof(Counters)), "pinned ctr");
         dispatch_n<SetupK>(h->n, h);
@@ -943,10 +965,11 @@ int rb_shard_load(rb_handle* h, const double* lo, const double* hi, const uint8_
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
         h->cur = 0;
-        front_reserve(h, h->F[0], std::max<int64_t>(N, 1), 0);
-        front_reserve(h, h->F[1], std::max<int64_t>(N, 1), 0);
+        h->n_cur = 0;
+        fronts_reserve(h, std::max<int64_t>(N, 1));
         load_rows(h, h->F[0], 0, lo, hi, cert, unsplit, N);
         h->n_cur = N;
+
         h->shard_target = target_width;
         h->have_result = false;
     })
@@ -958,14 +981,28 @@ int rb_round_filter(rb_handle* h, int32_t round_no, int64_t* carried, int64_t* s
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
-        RoundOut ro{};
-        round_filter(h, h->shard_target, ro);
-        h->shard_carried = ro.carried;
+        int64_t need_s, need_f;
+        plan_capacity(h, need_s, need_f);
+        for (;;) {
+            fronts_reserve(h, need_f);
+            surv_reserve(h, need_s);
+            parents_reserve(h, std::max<int64_t>(h->n_cur, 1));
+            launch_filter_phase(h, h->shard_target);
+            sync_counters(h);
+            if (h->h_ctr->n_surv > (unsigned long long)h->S.cap) {
+                need_s = (int64_t)(h->h_ctr->n_surv + h->h_ctr->n_surv / 4);
+                need_f = h->n_cur + 2 * need_s + 1;
+                continue;
+            }
+            break;
+        }
         h->shard_round = round_no;
-        if (carried) *carried = ro.carried;
-        if (survivors) *survivors = ro.survivors;
-        if (child_width) *child_width = ro.child_width;
-        if (children) *children = ro.children;
+        h->shard_need_f = need_f;
+        const Counters& c = *h->h_ctr;
+        if (carried) *carried = (int64_t)c.n_carried;
+        if (survivors) *survivors = (int64_t)c.n_surv;
+        if (child_width) *child_width = bits_to_double(c.child_wmax);
+        if (children) *children = (int64_t)(c.n_par << h->n);
     })
 }
 
@@ -974,16 +1011,24 @@ int rb_round_hs(rb_handle* h, int32_t hs_on, int32_t hs_contract, int64_t* n_out
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
-        RoundOut ro{};
-        ro.carried = h->shard_carried;
-        ro.survivors = (int64_t)h->h_ctr->n_surv;
         HsParams prm{};
         prm.round_no = h->shard_round;
         prm.hs_mode = hs_on ? 1 : 2;
         prm.contract_output = hs_contract ? 1 : 0;
-        round_hs(h, prm, true, ro);
-        h->cur ^= 1;
-        h->n_cur = ro.after_hs;
+        for (;;) {
+            launch_hs_phase(h, prm, true);
+            sync_counters(h);
+            if (h->h_ctr->n_next > (unsigned long long)h->F[h->cur ^ 1].f.cap) {
+                // redo the round with a larger frontier (the input rows are preserved)
+                fronts_reserve(h, (int64_t)(h->h_ctr->n_next + h->h_ctr->n_next / 4));
+                launch_filter_phase(h, h->shard_target);
+                continue;
+            }
+            break;
+        }
+        RoundOut ro{};
+        fill_round_out(h, ro);
+        commit_round(h, ro);
         if (n_out) *n_out = ro.after_hs;
         if (width) *width = ro.after_hs ? ro.width : 0.0;
         if (hs_calls) *hs_calls = ro.hs_calls;
@@ -1038,13 +1083,62 @@ int rb_shard_import(rb_handle* h, int64_t keep, const double* lo, const double* 
     }
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
-        DevFront& F = h->F[h->cur];
-        front_reserve(h, F, keep + count, keep);
-        load_rows(h, F, keep, lo, hi, cert, unsplit, count);
+        h->n_cur = keep;
+        fronts_reserve(h, keep + count);
+        load_rows(h, h->F[h->cur], keep, lo, hi, cert, unsplit, count);
         h->n_cur = keep + count;
     })
 }
 
 int64_t rb_shard_size(rb_handle* h) { return h ? h->n_cur : -1; }
+
+// Independent chains of directed DMUL/DADD per thread; values stay in [1, 2).
+__global__ void k_fp64_peak(double* sink, int iters) {
+    double a0 = 1.0 + threadIdx.x * 1e-9, a1 = a0 + 1e-10, a2 = a0 + 2e-10, a3 = a0 + 3e-10;
+    double a4 = a0 + 4e-10, a5 = a0 + 5e-10, a6 = a0 + 6e-10, a7 = a0 + 7e-10;
+    const double m = 1.0000000001, d = -1e-12;
+    for (int i = 0; i < iters; i++) {
+        a0 = __dmul_rd(a0, m); a1 = __dmul_ru(a1, m); a2 = __dadd_rd(a2, d); a3 = __dadd_ru(a3, d);
+        a4 = __dmul_rd(a4, m); a5 = __dmul_ru(a5, m); a6 = __dadd_rd(a6, d); a7 = __dadd_ru(a7, d);
+    }
+    const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (r == 12345.0) sink[0] = r;  // never true; keeps the chains alive
+}
+
+int rb_fp64_peak(int device, double* ops_per_second) {
+    if (!ops_per_second) return RB_ERR_ARG;
+    try {
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, device), "props");
+        double* sink = nullptr;
+        ck(cudaMalloc(&sink, 8), "malloc");
+        cudaEvent_t a, b;
+        ck(cudaEventCreate(&a), "ev");
+        ck(cudaEventCreate(&b), "ev");
+        const int threads = 256, blocks = prop.multiProcessorCount * 8, iters = 1 << 14;
+        k_fp64_peak<<<blocks, threads>>>(sink, 256);  // warm-up
+        double best = 0.0;
+        for (int rep = 0; rep < 5; rep++) {
+            ck(cudaEventRecord(a), "ev");
+            k_fp64_peak<<<blocks, threads>>>(sink, iters);
+            ck(cudaEventRecord(b), "ev");
+            ck(cudaEventSynchronize(b), "ev sync");
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, a, b);
+            const double ops = 8.0 * iters * (double)threads * blocks;
+            best = std::max(best, ops / (ms * 1e-3));
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaFree(sink);
+        *ops_per_second = best;
+        return RB_OK;
+    } catch (const CudaError& ce) {
+        g_create_error = std::string(ce.what) + ": " + cudaGetErrorString(ce.e);
+        cudaGetLastError();
+        return RB_ERR_CUDA;
+    }
+}
 
 }  // extern "C"

@@ -202,7 +202,8 @@ struct Counters {
     unsigned long long exact_boxes;
     unsigned long long dups;
     unsigned long long hs_on;
-    unsigned long long pad[4];
+    unsigned long long n_compact;
+    unsigned long long pad[3];
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -446,7 +447,11 @@ struct HsLayout {
     static constexpr int oG = 5 * N;          // g: lo[N], hi[N]
     static constexpr int oA = 7 * N;          // A[N*N]
     static constexpr int oJ = 7 * N + N * N;  // J then M: lo[N*N], hi[N*N]
-    static constexpr int doubles = 7 * N + 3 * N * N;
+    static constexpr int oCol = 7 * N + 3 * N * N;  // GJ pivot column[N] + pivot row
+    static constexpr int oT = oCol + N + 1;   // sweep products t_j: lo[N], hi[N]
+    static constexpr int oNz = oT + 2 * N;    // M_ij != [0,0] flags (as 0.0 / 1.0)
+    static constexpr int oCur = oNz + N;      // current box: lo[N], hi[N]
+    static constexpr int doubles = oCur + 2 * N;
 };
 
 enum { HS_EMPTY = 0, HS_ONE = 1, HS_TWO = 2, HS_SKIP = 3 };
@@ -527,6 +532,16 @@ __device__ __forceinline__ void hs_precond_products(double* s, int l, unsigned g
     }
 }
 
+template <int N, int G>
+__device__ __noinline__ void hs_precond_products_exact(double* s, int l, unsigned gmask) {
+    hs_precond_products<N, G, Exact>(s, l, gmask);
+}
+
+__device__ __noinline__ ival eval_poly_fast_call(const STab& t, int p, const double* xlo, const double* xhi,
+                                                 int stride) {
+    return eval_poly<Fast>(t, p, xlo, xhi, stride);
+}
+
 // One Hansen-Sengupta contraction of box b by one group of G lanes (hansen.py:77-138).
 // Returns the outcome kind (uniform across the group); lane j < N holds the
 // output component(s) in o0 (and o1 for a fork) and the input component in xin.
@@ -559,13 +574,13 @@ __device__ int hs_box(const TabMeta& meta, const STab& tab, double* s, unsigned 
     double* Jl = s + L::oJ;
     double* Jh = s + L::oJ + N * N;
     for (int e = l; e < N * N; e += G) {
-        const ival v = fastJ ? eval_poly<Fast>(tab, N + e, s + L::oX, s + L::oX + N, 1)
+        const ival v = fastJ ? eval_poly_fast_call(tab, N + e, s + L::oX, s + L::oX + N, 1)
                              : eval_poly_exact(tab, N + e, s + L::oX, s + L::oX + N, 1);
         Jl[e] = v.lo;
         Jh[e] = v.hi;
     }
     for (int i = l; i < N; i += G) {
-        const ival v = fastF ? eval_poly<Fast>(tab, i, s + L::oXm, s + L::oXm, 1)
+        const ival v = fastF ? eval_poly_fast_call(tab, i, s + L::oXm, s + L::oXm, 1)
                              : eval_poly_exact(tab, i, s + L::oXm, s + L::oXm, 1);
         s[L::oFx + i] = v.lo;
         s[L::oFx + N + i] = v.hi;
@@ -587,24 +602,28 @@ __device__ int hs_box(const TabMeta& meta, const STab& tab, double* s, unsigned 
     const double scale = group_max<G>(gmask, l < N ? colmax : 0.0);
     bool singular = scale == 0.0;
     const double threshold = __dmul_rn(1e-12, scale);
+    double* sCol = s + L::oCol;
 #pragma unroll
     for (int k = 0; k < N; k++) {
         if (singular) break;  // group-uniform
-        // first row r >= k with max |c[r][k]| (Python max() keeps the first)
-        int pr = k;
-        double best = fabs(c[k]);
+        // lane k: first row r >= k with max |c[r][k]| (Python max() keeps the first);
+        // it publishes its column and the pivot row through shared memory
+        if (l == k) {
+            int pr = k;
+            double best = fabs(c[k]);
 #pragma unroll
-        for (int r = k + 1; r < N; r++)
-            if (fabs(c[r]) > best) {
-                best = fabs(c[r]);
-                pr = r;
-            }
-        double pv = c[k];
+            for (int r = k + 1; r < N; r++)
+                if (fabs(c[r]) > best) {
+                    best = fabs(c[r]);
+                    pr = r;
+                }
 #pragma unroll
-        for (int r = k + 1; r < N; r++)
-            if (r == pr) pv = c[r];
-        pr = gshfl<G>(gmask, pr, k);
-        const double pivot = gshfl<G>(gmask, pv, k);
+            for (int i = 0; i < N; i++) sCol[i] = c[i];
+            sCol[N] = (double)pr;
+        }
+        __syncwarp(gmask);
+        const int pr = (int)sCol[N];
+        const double pivot = sCol[pr];
         if (fabs(pivot) < threshold) {
             singular = true;
             break;
@@ -617,15 +636,17 @@ __device__ int hs_box(const TabMeta& meta, const STab& tab, double* s, unsigned 
                 c[r] = t;
             }
         const double inv = __ddiv_rn(1.0, pivot);
-        double f[N];
-#pragma unroll
-        for (int i = 0; i < N; i++) f[i] = gshfl<G>(gmask, c[i], k);
         if (l >= k && l < 2 * N) {
             c[k] = __dmul_rn(c[k], inv);
 #pragma unroll
-            for (int i = 0; i < N; i++)
-                if (i != k && f[i] != 0.0) c[i] = __dsub_rn(c[i], __dmul_rn(f[i], c[k]));
+            for (int i = 0; i < N; i++) {
+                if (i == k) continue;
+                // column k after the row swap: rows k and pr exchanged
+                const double f = sCol[i == pr ? k : i];
+                if (f != 0.0) c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
+            }
         }
+        __syncwarp(gmask);
     }
     if (singular) return HS_SKIP;  // Singular -> ContractionOutcome "skipped"
     // A = right half; lane N+u holds column u
@@ -662,68 +683,95 @@ __device__ int hs_box(const TabMeta& meta, const STab& tab, double* s, unsigned 
     __syncwarp(gmask);
     // ---- M = A J (in place), g = A F(x)  (hansen.py:72-73)
     if (fastM) hs_precond_products<N, G, Fast>(s, l, gmask);
-    else hs_precond_products<N, G, Exact>(s, l, gmask);
+    else hs_precond_products_exact<N, G>(s, l, gmask);
     __syncwarp(gmask);
-    // ---- Gauss-Seidel sweep (hansen.py:91-127); lane j keeps current[j]
-    ival cur = xin;
+    // ---- Gauss-Seidel sweep (hansen.py:91-127); current[] lives in shared memory
+    double* sT = s + L::oT;
+    double* sNz = s + L::oNz;
+    double* sCur = s + L::oCur;
+    if (l < N) {
+        sCur[l] = xin.lo;
+        sCur[N + l] = xin.hi;
+    }
+    __syncwarp(gmask);
     int fork_i = -1;
     ival fp0 = mk(0.0, 0.0), fp1 = mk(0.0, 0.0);
-    const double xj = (l < N) ? xm : 0.0;
+    int outcome = HS_ONE;
     rows = 0;
 #pragma unroll 1
     for (int i = 0; i < N; i++) {
         rows = i + 1;
         // lane j: t_j = M_ij * (current_j - [x_j, x_j])
-        ival t = mk(0.0, 0.0);
-        int nz = 0;
-        if (l < N && l != i) {
-            const ival mij = mk(Jl[i * N + l], Jh[i * N + l]);
-            nz = !(mij.lo == 0.0 && mij.hi == 0.0);
-            if (nz) t = gmul(mij, Fast::sub(cur, mk(xj, xj)));
+        if (l < N) {
+            double nz = 0.0;
+            ival t = mk(0.0, 0.0);
+            if (l != i) {
+                const ival mij = mk(Jl[i * N + l], Jh[i * N + l]);
+                if (!(mij.lo == 0.0 && mij.hi == 0.0)) {
+                    nz = 1.0;
+                    t = gmul(mij, Fast::sub(mk(sCur[l], sCur[N + l]), mk(xm, xm)));
+                }
+            }
+            sT[l] = t.lo;
+            sT[N + l] = t.hi;
+            sNz[l] = nz;
         }
-        // p = -g_i - sum_{j != i, M_ij != 0} t_j, left to right
+        __syncwarp(gmask);
+        // p = -g_i - sum_{j != i, M_ij != 0} t_j, left to right (redundantly on every lane)
         ival p = mk(-s[L::oG + N + i], -s[L::oG + i]);
-#pragma unroll
-        for (int j = 0; j < N; j++) {
-            const double tl = gshfl<G>(gmask, t.lo, j);
-            const double th = gshfl<G>(gmask, t.hi, j);
-            const int z = gshfl<G>(gmask, nz, j);
-            if (j != i && z) p = Fast::sub(p, mk(tl, th));
-        }
-        const ival cur_i = mk(gshfl<G>(gmask, cur.lo, i), gshfl<G>(gmask, cur.hi, i));
+#pragma unroll 1
+        for (int j = 0; j < N; j++)
+            if (j != i && sNz[j] != 0.0) p = Fast::sub(p, mk(sT[j], sT[N + j]));
+        const ival cur_i = mk(sCur[i], sCur[N + i]);
         const double xi = s[L::oXm + i];
         const ival mii = mk(Jl[i * N + i], Jh[i * N + i]);
-        ival q0, q1;
+        ival q0 = mk(0.0, 0.0), q1 = mk(0.0, 0.0);
         const int kind = div_extended(p, mii, q0, q1);
-        if (kind == DIV_EMPTY) return HS_EMPTY;
-        if (kind == DIV_WHOLE) continue;
-        const int np = kind == DIV_SPLIT ? 2 : 1;
-        ival pieces[2];
-        int npieces = 0;
+        bool stop = false, update = false;
+        ival newc = cur_i;
+        if (kind == DIV_EMPTY) {
+            outcome = HS_EMPTY;
+            stop = true;
+        } else if (kind != DIV_WHOLE) {
+            const int np = kind == DIV_SPLIT ? 2 : 1;
+            ival pieces[2];
+            int npieces = 0;
 #pragma unroll
-        for (int q = 0; q < 2; q++) {
-            if (q < np) {
-                const ival qq = q == 0 ? q0 : q1;
-                const ival y = Fast::add(mk(xi, xi), qq);
-                const double lo = py_max(y.lo, cur_i.lo);  // Interval.intersect, interval.py:358-363
-                const double hi = py_min(y.hi, cur_i.hi);
-                if (!(lo > hi)) pieces[npieces++] = mk(lo, hi);
+            for (int q = 0; q < 2; q++) {
+                if (q < np) {
+                    const ival y = Fast::add(mk(xi, xi), q == 0 ? q0 : q1);
+                    const double lo = py_max(y.lo, cur_i.lo);  // Interval.intersect, interval.py:358-363
+                    const double hi = py_min(y.hi, cur_i.hi);
+                    if (!(lo > hi)) pieces[npieces++] = mk(lo, hi);
+                }
+            }
+            if (npieces == 0) {
+                outcome = HS_EMPTY;
+                stop = true;
+            } else if (npieces == 1) {
+                newc = pieces[0];
+                update = true;
+            } else {
+                newc = mk(py_min(pieces[0].lo, pieces[1].lo), py_max(pieces[0].hi, pieces[1].hi));  // hull
+                update = true;
+                if (fork_i < 0) {
+                    fork_i = i;
+                    fp0 = pieces[0];
+                    fp1 = pieces[1];
+                }
             }
         }
-        if (npieces == 0) return HS_EMPTY;
-        ival newc;
-        if (npieces == 1) {
-            newc = pieces[0];
-        } else {
-            newc = mk(py_min(pieces[0].lo, pieces[1].lo), py_max(pieces[0].hi, pieces[1].hi));  // hull
-            if (fork_i < 0) {
-                fork_i = i;
-                fp0 = pieces[0];
-                fp1 = pieces[1];
-            }
+        __syncwarp(gmask);  // every lane has read sT / sCur of this row
+        if (update && l == 0) {
+            sCur[i] = newc.lo;
+            sCur[N + i] = newc.hi;
         }
-        if (l == i) cur = newc;
+        __syncwarp(gmask);
+        if (stop) break;
     }
+    if (outcome == HS_EMPTY) return HS_EMPTY;
+    ival cur = mk(0.0, 0.0);
+    if (l < N) cur = mk(sCur[l], sCur[N + l]);
     if (fork_i < 0) {
         // certified iff the output lies strictly inside the input (hansen.py:129-132)
         int inside = 1;
@@ -765,7 +813,8 @@ __global__ void __launch_bounds__(128) k_hs(TabMeta meta, const uint8_t* __restr
     int64_t n_in = n_in_arg;
     if (prm.count_from_ctr) {
         const unsigned long long ns = ctr->n_surv;
-        n_in = (int64_t)(ns < (unsigned long long)S.cap ? ns : (unsigned long long)S.cap);
+        if (ns > (unsigned long long)S.cap) return;  // overflowed: the host grows S and redoes the round
+        n_in = (int64_t)ns;
     }
     // HS trigger (bnb.py:289-296) on the max child width of the filter survivors
     bool hs_on;
@@ -933,11 +982,21 @@ __device__ __forceinline__ void atomic_or_u8(uint8_t* p, uint8_t v) {
     atomicOr(w, (unsigned)v << (8 * (a & 3)));
 }
 
+// The round's dedup runs without host knowledge of the frontier size: both
+// kernels read n_next from the counters and do nothing when the round
+// overflowed a buffer (the host then grows the buffers and redoes the round).
+__device__ __forceinline__ bool round_ok(const Counters* c, int64_t s_cap, int64_t f_cap) {
+    return c->n_surv <= (unsigned long long)s_cap && c->n_next <= (unsigned long long)f_cap;
+}
+
 // Open-addressing insert of every row; a row equal to an already inserted one
 // is marked dead and ORs its flags into the keeper (dedup_sorted, _batch.py:253-266).
+// slot_of[i] records the occupied slot so k_dedup_finish can leave the table clean.
 template <int N>
-__global__ void k_dedup_insert(Front f, int64_t n, unsigned* table, unsigned long long mask, uint8_t* dead,
-                               Counters* ctr) {
+__global__ void k_dedup_insert(Front f, unsigned* table, unsigned long long mask, unsigned* slot_of, uint8_t* dead,
+                               Counters* ctr, int64_t s_cap) {
+    if (!round_ok(ctr, s_cap, f.cap)) return;
+    const int64_t n = (int64_t)ctr->n_next;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         unsigned long long slot = row_hash<N>(f, i) & mask;
         bool dup = false;
@@ -954,16 +1013,25 @@ __global__ void k_dedup_insert(Front f, int64_t n, unsigned* table, unsigned lon
             slot = (slot + 1) & mask;
         }
         dead[i] = dup ? 1 : 0;
+        slot_of[i] = dup ? 0xffffffffu : (unsigned)slot;
         if (dup) atomicAdd(&ctr->dups, 1ull);
     }
 }
 
+// Clear the used table slots; when duplicates were found, compact the live rows
+// into dst (counter ctr->n_compact).
 template <int N>
-__global__ void k_compact(Front src, int64_t n, const uint8_t* dead, Front dst, unsigned long long* counter) {
+__global__ void k_dedup_finish(Front src, Front dst, unsigned* table, const unsigned* slot_of, const uint8_t* dead,
+                               Counters* ctr, int64_t s_cap) {
+    if (!round_ok(ctr, s_cap, src.cap)) return;
+    const int64_t n = (int64_t)ctr->n_next;
+    const bool compact = ctr->dups != 0;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = base + threadIdx.x;
+        if (i < n && slot_of[i] != 0xffffffffu) table[slot_of[i]] = 0u;
+        if (!compact) continue;
         const bool live = i < n && !dead[i];
-        const unsigned long long slot = warp_append(live, counter);
+        const unsigned long long slot = warp_append(live, &ctr->n_compact);
         if (live) {
 #pragma unroll
             for (int j = 0; j < N; j++) {
