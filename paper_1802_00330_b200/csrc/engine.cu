@@ -34,14 +34,26 @@ namespace {
 
 std::string g_create_error;
 
+// Stream-ordered allocations from the handle's memory pool (memory is retained
+// across rounds and solves, so growth never stalls the device); set per API call.
+thread_local cudaMemPool_t t_pool = nullptr;
+thread_local cudaStream_t t_stream = nullptr;
+
+inline void dfree(void* p) {
+    if (!p) return;
+    if (t_pool) cudaFreeAsync(p, t_stream);
+    else cudaFree(p);
+}
+
+
 struct DevFront {
     Front f{};
     int n = 0;
     void release() {
-        if (f.lo) cudaFree(f.lo);
-        if (f.hi) cudaFree(f.hi);
-        if (f.cert) cudaFree(f.cert);
-        if (f.unsplit) cudaFree(f.unsplit);
+        dfree(f.lo);
+        dfree(f.hi);
+        dfree(f.cert);
+        dfree(f.unsplit);
         f = Front{};
     }
 };
@@ -68,6 +80,7 @@ struct rb_handle {
     int n = 0;
     int sms = 148;
     cudaStream_t st = nullptr;
+    cudaMemPool_t pool = nullptr;
     cudaEvent_t ev[8] = {};
     int64_t launches = 0;
     TabMeta meta{};
@@ -116,9 +129,21 @@ struct rb_handle {
     int filter_threads = 256;
     int hs_threads = 128;
     int filter_blocks_per_sm = 1;
-    int hs_blocks_per_sm = 1;
-    size_t filter_smem = 0, hs_smem = 0;
+    int eval_blocks_per_sm = 1, lin_blocks_per_sm = 1, sweep_blocks_per_sm = 1;
+    size_t filter_smem = 0, eval_smem = 0, lin_smem = 0, sweep_smem = 0;
+    HsScratch W{};
     int smem_optin = 48 * 1024;
+};
+
+struct PoolScope {
+    explicit PoolScope(rb_handle* h) {
+        t_pool = h->pool;
+        t_stream = h->st;
+    }
+    ~PoolScope() {
+        t_pool = nullptr;
+        t_stream = nullptr;
+    }
 };
 
 // ---------------------------------------------------------------- dispatch on n
@@ -145,22 +170,27 @@ static int grid_for(int64_t work, int threads, int max_blocks) {
 template <int N>
 struct SetupK {
     static void run(rb_handle* h) {
-        const size_t fs = stab_bytes(h->meta, true) + (size_t)2 * N * h->filter_threads * sizeof(double);
-        const size_t hsm = stab_bytes(h->meta, false) +
-                           (size_t)(h->hs_threads / 32) * HsLayout<N>::BPW * HsLayout<N>::doubles * sizeof(double);
-        h->filter_smem = fs;
-        h->hs_smem = hsm;
+        const int T = h->hs_threads;
+        h->filter_smem = stab_bytes(h->meta, true) + (size_t)2 * N * h->filter_threads * sizeof(double);
+        h->eval_smem = stab_bytes(h->meta, false) + (size_t)3 * N * T * sizeof(double);
+        h->lin_smem = (size_t)(T / 32) * LinLayout<N>::BPW * LinLayout<N>::doubles * sizeof(double);
+        h->sweep_smem = (size_t)2 * N * T * sizeof(double);
         // the attribute is per kernel (shared by every handle of this n): set it to the opt-in maximum
-        if ((int)fs > h->smem_optin || (int)hsm > h->smem_optin)
-            throw ArgError{RB_ERR_LIMIT, "system tables exceed the shared-memory budget"};
-        ck(cudaFuncSetAttribute(k_filter<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin),
-           "attr filter");
-        ck(cudaFuncSetAttribute(k_hs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr hs");
+        const size_t mx = std::max({h->filter_smem, h->eval_smem, h->lin_smem, h->sweep_smem});
+        if ((int)mx > h->smem_optin) throw ArgError{RB_ERR_LIMIT, "system tables exceed the shared-memory budget"};
+        ck(cudaFuncSetAttribute(k_filter<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr");
+        ck(cudaFuncSetAttribute(k_hs_eval<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr");
+        ck(cudaFuncSetAttribute(k_hs_lin<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr");
+        ck(cudaFuncSetAttribute(k_hs_sweep<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr");
         int nb = 0;
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter<N>, h->filter_threads, fs), "occ filter");
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter<N>, h->filter_threads, h->filter_smem), "occ");
         h->filter_blocks_per_sm = std::max(1, nb);
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs<N>, h->hs_threads, hsm), "occ hs");
-        h->hs_blocks_per_sm = std::max(1, nb);
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_eval<N>, T, h->eval_smem), "occ");
+        h->eval_blocks_per_sm = std::max(1, nb);
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_lin<N>, T, h->lin_smem), "occ");
+        h->lin_blocks_per_sm = std::max(1, nb);
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_sweep<N>, T, h->sweep_smem), "occ");
+        h->sweep_blocks_per_sm = std::max(1, nb);
     }
 };
 
@@ -197,14 +227,20 @@ struct FilterK {
     }
 };
 
+// K2a + K2b + K2c over rows [b0, b0 + W.B) of S (n_in read on the device when prm.count_from_ctr)
 template <int N>
 struct HsK {
-    static void run(rb_handle* h, int64_t max_in, int64_t n_in, HsParams prm, int64_t* tags) {
-        const int per_block_boxes = (h->hs_threads / 32) * HsLayout<N>::BPW;
-        const int blocks = grid_for(max_in * 1, per_block_boxes, h->sms * h->hs_blocks_per_sm);
-        h->launches++;
-        k_hs<N><<<std::max(blocks, 1), h->hs_threads, h->hs_smem, h->st>>>(
-            h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
+    static void run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* tags) {
+        const int T = h->hs_threads;
+        const int64_t B = h->W.B;
+        Front out = h->F[h->cur ^ 1].f;
+        h->launches += 3;
+        k_hs_eval<N><<<grid_for(B, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem, h->st>>>(
+            h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
+        k_hs_lin<N><<<grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem,
+                      h->st>>>(h->S, n_in, b0, prm, h->W, h->d_ctr);
+        k_hs_sweep<N><<<grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem, h->st>>>(
+            h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
         ck(cudaGetLastError(), "hs launch");
     }
 };
@@ -227,10 +263,11 @@ struct DedupK {
 
 template <typename T>
 static void dalloc(T** p, size_t count) {
-    if (*p) cudaFree(*p);
+    if (*p) dfree(*p);
     *p = nullptr;
     if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+    cudaError_t e = t_pool ? cudaMallocFromPoolAsync((void**)p, count * sizeof(T), t_pool, t_stream)
+                           : cudaMalloc((void**)p, count * sizeof(T));
     if (e != cudaSuccess) {
         cudaGetLastError();
         *p = nullptr;
@@ -264,7 +301,6 @@ static void front_reserve(rb_handle* h, DevFront& F, int64_t need, int64_t keep)
                              cudaMemcpyDeviceToDevice, h->st), "grow copy hi");
         ck(cudaMemcpyAsync(G.f.cert, F.f.cert, keep, cudaMemcpyDeviceToDevice, h->st), "grow copy cert");
         ck(cudaMemcpyAsync(G.f.unsplit, F.f.unsplit, keep, cudaMemcpyDeviceToDevice, h->st), "grow copy uns");
-        ck(cudaStreamSynchronize(h->st), "grow sync");
     }
     F.release();
     F = G;
@@ -273,12 +309,39 @@ static void front_reserve(rb_handle* h, DevFront& F, int64_t need, int64_t keep)
 static void surv_reserve(rb_handle* h, int64_t need) {
     if (h->S.cap >= need && h->S.lo) return;
     const int64_t cap = grow_cap(need);
-    if (h->S.lo) cudaFree(h->S.lo);
-    if (h->S.hi) cudaFree(h->S.hi);
+    dfree(h->S.lo);
+    dfree(h->S.hi);
     h->S.lo = h->S.hi = nullptr;
     dalloc(&h->S.lo, (size_t)cap * h->n);
     dalloc(&h->S.hi, (size_t)cap * h->n);
     h->S.cap = cap;
+}
+
+// HS scratch: batch capacity B <= S.cap, bounded so the scratch stays small
+static void scratch_reserve(rb_handle* h, int64_t want) {
+    const int n = h->n;
+    const size_t per_box = (size_t)(2 * n * n + 3 * n) * sizeof(double) + 1;
+    const size_t cap_bytes = std::min<size_t>((size_t)4 << 30, h->mem_budget / 5);
+    int64_t B = std::min<int64_t>(want, std::max<int64_t>(65536, (int64_t)(cap_bytes / per_box)));
+    B = std::max<int64_t>(B, 1024);
+    if (h->W.B >= B && h->W.x) return;
+    auto fr = [](void* p) { dfree(p); };
+    fr(h->W.x); fr(h->W.jl); fr(h->W.jh); fr(h->W.fl); fr(h->W.fh); fr(h->W.flags);
+    h->W = HsScratch{};
+    dalloc(&h->W.x, (size_t)B * n);
+    dalloc(&h->W.jl, (size_t)B * n * n);
+    dalloc(&h->W.jh, (size_t)B * n * n);
+    dalloc(&h->W.fl, (size_t)B * n);
+    dalloc(&h->W.fh, (size_t)B * n);
+    dalloc(&h->W.flags, (size_t)B);
+    h->W.B = B;
+}
+
+// all batches of the HS pipeline over at most `bound` survivors
+static void launch_hs_batches(rb_handle* h, int64_t bound, int64_t n_in, const HsParams& prm, int64_t* tags) {
+    scratch_reserve(h, std::max<int64_t>(bound, 1));
+    const int64_t B = h->W.B;
+    for (int64_t b0 = 0; b0 == 0 || b0 < bound; b0 += B) dispatch_n<HsK>(h->n, h, b0, n_in, prm, tags);
 }
 
 static void parents_reserve(rb_handle* h, int64_t need) {
@@ -416,10 +479,10 @@ static void load_rows(rb_handle* h, DevFront& F, int64_t off, const double* lo, 
     k_rows_to_soa<<<grid_for(N, 256, h->sms * 8), 256, 0, h->st>>>(dlo, dhi, dc, du, n, N, F.f, off);
     ck(cudaGetLastError(), "rows_to_soa");
     ck(cudaStreamSynchronize(h->st), "rows sync");
-    cudaFree(dlo);
-    cudaFree(dhi);
-    if (dc) cudaFree(dc);
-    if (du) cudaFree(du);
+    dfree(dlo);
+    dfree(dhi);
+    dfree(dc);
+    dfree(du);
 }
 
 struct RoundOut {
@@ -475,8 +538,7 @@ static void launch_filter_phase(rb_handle* h, double target) {
 static void launch_hs_phase(rb_handle* h, const HsParams& prm0, bool dedup) {
     HsParams prm = prm0;
     prm.count_from_ctr = 1;
-    if (h->n_cur > 0) dispatch_n<HsK>(h->n, h, std::min<int64_t>(h->S.cap, h->n_cur << h->n), (int64_t)0, prm,
-                                      (int64_t*)nullptr);
+    if (h->n_cur > 0) launch_hs_batches(h, std::min<int64_t>(h->S.cap, h->n_cur << h->n), 0, prm, nullptr);
     record(h, 3);
     if (dedup) dispatch_n<DedupK>(h->n, h, h->F[h->cur ^ 1].f, h->F[h->cur].f);
 }
@@ -520,6 +582,7 @@ static void run_round(rb_handle* h, double target, const HsParams& prm, bool ded
         fronts_reserve(h, need_f);
         surv_reserve(h, need_s);
         parents_reserve(h, std::max<int64_t>(h->n_cur, 1));
+        scratch_reserve(h, std::max<int64_t>(1, std::min<int64_t>(h->S.cap, h->n_cur << h->n)));
         launch_filter_phase(h, target);
         launch_hs_phase(h, prm, dedup);
         record(h, 4);
@@ -546,9 +609,7 @@ static void run_round(rb_handle* h, double target, const HsParams& prm, bool ded
 static void release_all(rb_handle* h) {
     h->F[0].release();
     h->F[1].release();
-    auto fr = [](void* p) {
-        if (p) cudaFree(p);
-    };
+    auto fr = [](void* p) { dfree(p); };
     fr(h->parents);
     fr(h->S.lo);
     fr(h->S.hi);
@@ -567,6 +628,15 @@ static void release_all(rb_handle* h) {
     fr(h->r_cert);
     fr(h->r_uns);
     fr(h->d_tab);
+    fr(h->W.x);
+    fr(h->W.jl);
+    fr(h->W.jh);
+    fr(h->W.fl);
+    fr(h->W.fh);
+    fr(h->W.flags);
+    if (h->st) cudaStreamSynchronize(h->st);
+    if (h->pool) cudaMemPoolDestroy(h->pool);
+    h->pool = nullptr;
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
@@ -782,6 +852,16 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         h->sms = prop.multiProcessorCount;
         h->smem_optin = (int)prop.sharedMemPerBlockOptin;
         ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "stream");
+        {
+            cudaMemPoolProps pp{};
+            pp.allocType = cudaMemAllocationTypePinned;
+            pp.location.type = cudaMemLocationTypeDevice;
+            pp.location.id = device;
+            ck(cudaMemPoolCreate(&h->pool, &pp), "mempool");
+            uint64_t thr = UINT64_MAX;
+            ck(cudaMemPoolSetAttribute(h->pool, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
+        }
+        PoolScope ps(h);
         for (auto& e : h->ev) ck(cudaEventCreate(&e), "event");
         build_tables(h, sys);
         size_t free_b = 0, total_b = 0;
@@ -797,11 +877,17 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         cudaGetLastError();
     } catch (const ArgError& ae) {
         g_create_error = ae.msg;
-        release_all(h);
+        {
+            PoolScope ps(h);
+            release_all(h);
+        }
         delete h;
         return ae.code;
     }
-    release_all(h);
+    {
+        PoolScope ps(h);
+        release_all(h);
+    }
     delete h;
     return RB_ERR_CUDA;
 }
@@ -811,6 +897,7 @@ int rb_solve(rb_handle* h, const rb_config* cfg, rb_result_info* info) {
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
         solve_impl(h, cfg, info);
     })
 }
@@ -824,6 +911,7 @@ int rb_fetch(rb_handle* h, double* lo, double* hi, uint8_t* cert, uint8_t* unspl
     }
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
         const int64_t N = h->r_n;
         if (N > 0) {
             if (lo) ck(cudaMemcpyAsync(lo, h->r_lo, sizeof(double) * N * h->n, cudaMemcpyDeviceToHost, h->st), "d2h");
@@ -843,6 +931,7 @@ int rb_filter(rb_handle* h, const double* plo, const double* phi, int64_t P, dou
     h->have_result = false;
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
         const int n = h->n;
         *M = 0;
         if (P == 0) return RB_OK;
@@ -893,6 +982,7 @@ int rb_hs(rb_handle* h, const double* lo, const double* hi, int64_t M, int contr
     h->have_result = false;
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
         const int n = h->n;
         *M2 = 0;
         if (M == 0) return RB_OK;
@@ -911,7 +1001,7 @@ int rb_hs(rb_handle* h, const double* lo, const double* hi, int64_t M, int contr
         prm.contract_output = contract_output ? 1 : 0;
         prm.count_from_ctr = 0;
         ck(cudaMemsetAsync(h->d_ctr, 0, sizeof(Counters), h->st), "ctr memset");
-        dispatch_n<HsK>(n, h, M, M, prm, h->d_tags);
+        launch_hs_batches(h, M, M, prm, h->d_tags);
         sync_counters(h);
         const int64_t m = (int64_t)h->h_ctr->n_next;
         *M2 = m;
@@ -951,6 +1041,7 @@ void rb_destroy(rb_handle* h) {
     {
         std::lock_guard<std::mutex> lk(h->mu);
         cudaSetDevice(h->dev);
+        PoolScope ps(h);
         release_all(h);
     }
     delete h;
@@ -964,6 +1055,7 @@ int rb_shard_load(rb_handle* h, const double* lo, const double* hi, const uint8_
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
         h->cur = 0;
         h->n_cur = 0;
         fronts_reserve(h, std::max<int64_t>(N, 1));
@@ -981,6 +1073,7 @@ int rb_round_filter(rb_handle* h, int32_t round_no, int64_t* carried, int64_t* s
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
         int64_t need_s, need_f;
         plan_capacity(h, need_s, need_f);
         for (;;) {
@@ -1011,6 +1104,7 @@ int rb_round_hs(rb_handle* h, int32_t hs_on, int32_t hs_contract, int64_t* n_out
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
         HsParams prm{};
         prm.round_no = h->shard_round;
         prm.hs_mode = hs_on ? 1 : 2;
@@ -1045,6 +1139,7 @@ int rb_shard_export(rb_handle* h, int64_t start, int64_t count, double* lo, doub
     }
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
         const int n = h->n;
         if (count == 0) return RB_OK;
         Front f = h->F[h->cur].f;
@@ -1066,10 +1161,10 @@ int rb_shard_export(rb_handle* h, int64_t start, int64_t count, double* lo, doub
         if (cert) ck(cudaMemcpyAsync(cert, dc, count, cudaMemcpyDeviceToHost, h->st), "d2h");
         if (unsplit) ck(cudaMemcpyAsync(unsplit, du, count, cudaMemcpyDeviceToHost, h->st), "d2h");
         ck(cudaStreamSynchronize(h->st), "export sync");
-        cudaFree(dlo);
-        cudaFree(dhi);
-        cudaFree(dc);
-        cudaFree(du);
+        dfree(dlo);
+        dfree(dhi);
+        dfree(dc);
+        dfree(du);
     })
 }
 
@@ -1083,6 +1178,7 @@ int rb_shard_import(rb_handle* h, int64_t keep, const double* lo, const double* 
     }
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
         h->n_cur = keep;
         fronts_reserve(h, keep + count);
         load_rows(h, h->F[h->cur], keep, lo, hi, cert, unsplit, count);

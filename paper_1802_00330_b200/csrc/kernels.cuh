@@ -425,6 +425,19 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
 }
 
 // ------------------------------------------------------------------ K2 Hansen-Sengupta
+//
+// hansen.contract (hansen.py:56-138) over a batch of boxes as a three-kernel
+// pipeline with an HBM scratch of J/M, F(x)/g and x per box (SoA, stride B):
+//
+//   K2a k_hs_eval   thread per box: x = mid(X), J(X) (n^2 interval polynomials),
+//                   F(x) (n point polynomials) -- the same uniform interpreter as K1
+//   K2b k_hs_lin    G lanes per box: mid(J), Gauss-Jordan inverse A (lane = column,
+//                   registers), M = A J and g = A F(x), written back over J / F(x)
+//   K2c k_hs_sweep  thread per box: Gauss-Seidel sweep with extended division,
+//                   fork / certification, compaction of 0-2 outputs into F_next
+//
+// The scratch costs (2n^2 + 3n) x 8 B of HBM traffic per box and pass, small
+// against the O(n^3) FP64 work; every phase gets the parallel shape that suits it.
 
 struct HsParams {
     int round_no;
@@ -433,28 +446,143 @@ struct HsParams {
     int hs_possible;
     double hs_enable_width;// NaN: None
     int contract_output;   // SolverConfig.hs_contract
-    int count_from_ctr;    // n_in = ctr->n_surv (clamped to S.cap) instead of n_in arg
+    int count_from_ctr;    // n_in = ctr->n_surv instead of n_in arg
 };
 
-template <int N>
-struct HsLayout {
-    static constexpr int G = N <= 2 ? 4 : (N <= 4 ? 8 : (N <= 8 ? 16 : 32));
-    static constexpr int BPW = 32 / G;
-    // per-group scratch (doubles)
-    static constexpr int oX = 0;              // X lo[N], hi[N]
-    static constexpr int oXm = 2 * N;         // midpoints x[N]
-    static constexpr int oFx = 3 * N;         // F(x): lo[N], hi[N]
-    static constexpr int oG = 5 * N;          // g: lo[N], hi[N]
-    static constexpr int oA = 7 * N;          // A[N*N]
-    static constexpr int oJ = 7 * N + N * N;  // J then M: lo[N*N], hi[N*N]
-    static constexpr int oCol = 7 * N + 3 * N * N;  // GJ pivot column[N] + pivot row
-    static constexpr int oT = oCol + N + 1;   // sweep products t_j: lo[N], hi[N]
-    static constexpr int oNz = oT + 2 * N;    // M_ij != [0,0] flags (as 0.0 / 1.0)
-    static constexpr int oCur = oNz + N;      // current box: lo[N], hi[N]
-    static constexpr int doubles = oCur + 2 * N;
+struct HsScratch {         // SoA with stride B (batch capacity)
+    double* x;             // [n][B] midpoints
+    double* jl;            // [n*n][B] J(X), then M = A J
+    double* jh;
+    double* fl;            // [n][B] F(x), then g = A F(x)
+    double* fh;
+    uint8_t* flags;        // [B] bit0: exact J/F, bit1: exact M/g, bit2: singular
+    int64_t B;
 };
 
 enum { HS_EMPTY = 0, HS_ONE = 1, HS_TWO = 2, HS_SKIP = 3 };
+enum { HSF_EXACT_EVAL = 1, HSF_EXACT_LIN = 2, HSF_SINGULAR = 4 };
+
+// number of HS boxes this launch may process; also decides the HS trigger
+__device__ __forceinline__ int64_t hs_count(const HsParams& prm, const Counters* ctr, int64_t n_in_arg,
+                                            int64_t s_cap, bool& hs_on) {
+    int64_t n_in = n_in_arg;
+    if (prm.count_from_ctr) {
+        const unsigned long long ns = ctr->n_surv;
+        if (ns > (unsigned long long)s_cap) {  // overflowed: the host grows S and redoes the round
+            hs_on = false;
+            return -1;
+        }
+        n_in = (int64_t)ns;
+    }
+    if (prm.hs_mode == 1) hs_on = true;
+    else if (prm.hs_mode == 2) hs_on = false;
+    else {  // bnb.py:289-296 on the max width of the filter survivors
+        const double cw = __longlong_as_double((long long)ctr->child_wmax);
+        hs_on = false;
+        if (n_in > 0 && prm.hs_possible) {
+            if (prm.hs_enable_round >= 0 && prm.round_no >= prm.hs_enable_round) hs_on = true;
+            if (!isnan(prm.hs_enable_width) && cw <= prm.hs_enable_width) hs_on = true;
+        }
+    }
+    return n_in;
+}
+
+// K2a: thread per box.  Rows [b0, b0 + B) of S.  When HS is off for this round the
+// first batch launch copies S into F_next instead (bnb.py:580-581).
+template <int N>
+__global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
+                                                 int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
+                                                 Front out, Counters* ctr, int64_t* tags) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    bool hs_on;
+    const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
+    if (n_in < 0) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && b0 == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
+    const int lane = threadIdx.x & 31;
+    if (!hs_on) {
+        if (b0 != 0) return;
+        // pass-through: survivors join the frontier uncertified
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x < n_in;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const bool valid = i < n_in;
+            double w = 0.0;
+            const unsigned long long slot = warp_append(valid, &ctr->n_next);
+            if (valid) {
+#pragma unroll
+                for (int j = 0; j < N; j++) {
+                    const double lo = S.lo[j * S.cap + i], hi = S.hi[j * S.cap + i];
+                    const double d = __dsub_rn(hi, lo);
+                    w = j == 0 ? d : (d > w ? d : w);
+                    if (slot < (unsigned long long)out.cap) {
+                        out.lo[j * out.cap + slot] = lo;
+                        out.hi[j * out.cap + slot] = hi;
+                    }
+                }
+                if (slot < (unsigned long long)out.cap) {
+                    out.cert[slot] = 0;
+                    out.unsplit[slot] = 0;
+                    if (tags) tags[slot] = 2 * i;
+                }
+            }
+            unsigned long long wb = valid ? (unsigned long long)__double_as_longlong(w) : 0ull;
+            wb = warp_max(wb);
+            if (lane == 0 && wb) atomicMax(&ctr->wmax, wb);
+        }
+        return;
+    }
+    const int64_t b_end = min(n_in, b0 + W.B);
+    if (b0 >= b_end) return;
+    const STab tab = load_stab(meta, gtab, smem, false);
+    double* xs = reinterpret_cast<double*>(smem + stab_bytes(meta, false));
+    const int stride = blockDim.x;
+    double* xlo = xs + threadIdx.x;
+    double* xhi = xs + N * stride + threadIdx.x;
+    double* xmid = xs + 2 * N * stride + threadIdx.x;
+    __syncthreads();
+    unsigned long long exact_acc = 0;
+    for (int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < b_end;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = b - b0;
+        ExpRange rx, rm;
+        rx.init();
+        rm.init();
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            const double lo = S.lo[j * S.cap + b], hi = S.hi[j * S.cap + b];
+            const double m = mid_of(lo, hi);  // Box.midpoint, poly.py:114-115
+            xlo[j * stride] = lo;
+            xhi[j * stride] = hi;
+            xmid[j * stride] = m;
+            W.x[j * W.B + t] = m;
+            rx.add(lo);
+            rx.add(hi);
+            rm.add(m);
+        }
+        const bool fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
+        const bool fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
+        // J(X) (hansen.py:61-63); zero polynomials evaluate to [0,0]
+#pragma unroll 1
+        for (int e = 0; e < N * N; e++) {
+            const ival v = fastJ ? eval_poly<Fast>(tab, N + e, xlo, xhi, stride)
+                                 : eval_poly_exact(tab, N + e, xlo, xhi, stride);
+            W.jl[e * W.B + t] = v.lo;
+            W.jh[e * W.B + t] = v.hi;
+        }
+        // F(x) = eval_point (poly.py:205-207): interval arithmetic on the point box
+#pragma unroll 1
+        for (int i = 0; i < N; i++) {
+            const ival v = fastF ? eval_poly<Fast>(tab, i, xmid, xmid, stride)
+                                 : eval_poly_exact(tab, i, xmid, xmid, stride);
+            W.fl[i * W.B + t] = v.lo;
+            W.fh[i * W.B + t] = v.hi;
+        }
+        const bool ex = !(fastJ && fastF);
+        W.flags[t] = ex ? HSF_EXACT_EVAL : 0;
+        exact_acc += ex;
+    }
+    exact_acc = warp_sum(exact_acc);
+    if (lane == 0 && exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
+}
 
 template <int G>
 __device__ __forceinline__ double gshfl(unsigned mask, double v, int src) {
@@ -484,404 +612,298 @@ __device__ __forceinline__ double group_max(unsigned mask, double v) {
     return v;
 }
 
-// M = A * J in place over J, g = A * F(x)  (linalg.py:102-129): acc = [0,0];
-// acc += [a,a] * B[u][j] for u ascending.
-template <int N, int G, class A>
-__device__ __forceinline__ void hs_precond_products(double* s, int l, unsigned gmask) {
-    using L = HsLayout<N>;
-    constexpr int H = (N + 1) / 2;  // rows per half
-    const double* Am = s + L::oA;
-    double* Jl = s + L::oJ;
-    double* Jh = s + L::oJ + N * N;
-    ival res[H];
-    const int col = l % N, half = l / N;
-    const bool act = l < 2 * N;
-    if (act) {
-#pragma unroll
-        for (int r = 0; r < H; r++) {
-            const int i = half * H + r;
-            ival acc = mk(0.0, 0.0);
-            if (i < N) {
-#pragma unroll 4
-                for (int u = 0; u < N; u++) {
-                    const double a = Am[i * N + u];
-                    acc = A::add(acc, A::mul_point(a, mk(Jl[u * N + col], Jh[u * N + col])));
-                }
-            }
-            res[r] = acc;
-        }
-    }
-    __syncwarp(gmask);
-    if (act) {
-#pragma unroll
-        for (int r = 0; r < H; r++) {
-            const int i = half * H + r;
-            if (i < N) {
-                Jl[i * N + col] = res[r].lo;
-                Jh[i * N + col] = res[r].hi;
-            }
-        }
-    }
-    // g_i = sum_u A[i][u] * F_u(x)
-    if (l < N) {
-        ival acc = mk(0.0, 0.0);
-        for (int u = 0; u < N; u++)
-            acc = A::add(acc, A::mul_point(Am[l * N + u], mk(s[L::oFx + u], s[L::oFx + N + u])));
-        s[L::oG + l] = acc.lo;
-        s[L::oG + N + l] = acc.hi;
-    }
-}
-
-template <int N, int G>
-__device__ __noinline__ void hs_precond_products_exact(double* s, int l, unsigned gmask) {
-    hs_precond_products<N, G, Exact>(s, l, gmask);
-}
-
-__device__ __noinline__ ival eval_poly_fast_call(const STab& t, int p, const double* xlo, const double* xhi,
-                                                 int stride) {
-    return eval_poly<Fast>(t, p, xlo, xhi, stride);
-}
-
-// One Hansen-Sengupta contraction of box b by one group of G lanes (hansen.py:77-138).
-// Returns the outcome kind (uniform across the group); lane j < N holds the
-// output component(s) in o0 (and o1 for a fork) and the input component in xin.
-template <int N, int G>
-__device__ int hs_box(const TabMeta& meta, const STab& tab, double* s, unsigned gmask, int l,
-                      const ival& xin, ival& o0, ival& o1, bool& certified, unsigned& exact_flags,
-                      int& rows) {
-    using L = HsLayout<N>;
-    // ---- stage X and the midpoint x (Box.midpoint, poly.py:114-115)
-    double xm = 0.0;
-    ExpRange rx, rm;
-    rx.init();
-    rm.init();
-    if (l < N) {
-        xm = mid_of(xin.lo, xin.hi);
-        s[L::oX + l] = xin.lo;
-        s[L::oX + N + l] = xin.hi;
-        s[L::oXm + l] = xm;
-        rx.add(xin.lo);
-        rx.add(xin.hi);
-        rm.add(xm);
-    }
-    group_reduce<G>(gmask, rx);
-    group_reduce<G>(gmask, rm);
-    const bool fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
-    const bool fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
-    exact_flags = (fastJ ? 0u : 1u) | (fastF ? 0u : 2u);
-    __syncwarp(gmask);
-    // ---- J(X) (hansen.py:61-63) and F(x) (hansen.py:71)
-    double* Jl = s + L::oJ;
-    double* Jh = s + L::oJ + N * N;
-    for (int e = l; e < N * N; e += G) {
-        const ival v = fastJ ? eval_poly_fast_call(tab, N + e, s + L::oX, s + L::oX + N, 1)
-                             : eval_poly_exact(tab, N + e, s + L::oX, s + L::oX + N, 1);
-        Jl[e] = v.lo;
-        Jh[e] = v.hi;
-    }
-    for (int i = l; i < N; i += G) {
-        const ival v = fastF ? eval_poly_fast_call(tab, i, s + L::oXm, s + L::oXm, 1)
-                             : eval_poly_exact(tab, i, s + L::oXm, s + L::oXm, 1);
-        s[L::oFx + i] = v.lo;
-        s[L::oFx + N + i] = v.hi;
-    }
-    __syncwarp(gmask);
-    // ---- Gauss-Jordan inverse of mid(J) (linalg.py:137-172), lane = column of [jc | I]
-    double c[N];
-    double colmax = 0.0;
-    if (l < N) {
-#pragma unroll
-        for (int i = 0; i < N; i++) {
-            c[i] = mid_of(Jl[i * N + l], Jh[i * N + l]);  // mid_matrix, linalg.py:132-134
-            colmax = fmax(colmax, fabs(c[i]));
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < N; i++) c[i] = (l - N == i) ? 1.0 : 0.0;
-    }
-    const double scale = group_max<G>(gmask, l < N ? colmax : 0.0);
-    bool singular = scale == 0.0;
-    const double threshold = __dmul_rn(1e-12, scale);
-    double* sCol = s + L::oCol;
-#pragma unroll
-    for (int k = 0; k < N; k++) {
-        if (singular) break;  // group-uniform
-        // lane k: first row r >= k with max |c[r][k]| (Python max() keeps the first);
-        // it publishes its column and the pivot row through shared memory
-        if (l == k) {
-            int pr = k;
-            double best = fabs(c[k]);
-#pragma unroll
-            for (int r = k + 1; r < N; r++)
-                if (fabs(c[r]) > best) {
-                    best = fabs(c[r]);
-                    pr = r;
-                }
-#pragma unroll
-            for (int i = 0; i < N; i++) sCol[i] = c[i];
-            sCol[N] = (double)pr;
-        }
-        __syncwarp(gmask);
-        const int pr = (int)sCol[N];
-        const double pivot = sCol[pr];
-        if (fabs(pivot) < threshold) {
-            singular = true;
-            break;
-        }
-#pragma unroll
-        for (int r = k + 1; r < N; r++)
-            if (r == pr) {
-                const double t = c[k];
-                c[k] = c[r];
-                c[r] = t;
-            }
-        const double inv = __ddiv_rn(1.0, pivot);
-        if (l >= k && l < 2 * N) {
-            c[k] = __dmul_rn(c[k], inv);
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                if (i == k) continue;
-                // column k after the row swap: rows k and pr exchanged
-                const double f = sCol[i == pr ? k : i];
-                if (f != 0.0) c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
-            }
-        }
-        __syncwarp(gmask);
-    }
-    if (singular) return HS_SKIP;  // Singular -> ContractionOutcome "skipped"
-    // A = right half; lane N+u holds column u
-    double* Am = s + L::oA;
-    ExpRange ra;
-    ra.init();
-    if (l >= N && l < 2 * N) {
-#pragma unroll
-        for (int i = 0; i < N; i++) {
-            Am[i * N + (l - N)] = c[i];
-            ra.add(c[i]);
-        }
-    }
-    // exponent ranges of J and F(x) for the product guards
-    ExpRange rj, rf;
-    rj.init();
-    rf.init();
-    for (int e = l; e < N * N; e += G) {
-        rj.add(Jl[e]);
-        rj.add(Jh[e]);
-    }
-    if (l < N) {
-        rf.add(s[L::oFx + l]);
-        rf.add(s[L::oFx + N + l]);
-    }
-    group_reduce<G>(gmask, ra);
-    group_reduce<G>(gmask, rj);
-    group_reduce<G>(gmask, rf);
-    ExpRange rjf = rj;
-    rjf.emin = min(rj.emin, rf.emin);
-    rjf.emax = max(rj.emax, rf.emax);
-    const bool fastM = prod_guard_ok(ra, rjf);
-    if (!fastM) exact_flags |= 4u;
-    __syncwarp(gmask);
-    // ---- M = A J (in place), g = A F(x)  (hansen.py:72-73)
-    if (fastM) hs_precond_products<N, G, Fast>(s, l, gmask);
-    else hs_precond_products_exact<N, G>(s, l, gmask);
-    __syncwarp(gmask);
-    // ---- Gauss-Seidel sweep (hansen.py:91-127); current[] lives in shared memory
-    double* sT = s + L::oT;
-    double* sNz = s + L::oNz;
-    double* sCur = s + L::oCur;
-    if (l < N) {
-        sCur[l] = xin.lo;
-        sCur[N + l] = xin.hi;
-    }
-    __syncwarp(gmask);
-    int fork_i = -1;
-    ival fp0 = mk(0.0, 0.0), fp1 = mk(0.0, 0.0);
-    int outcome = HS_ONE;
-    rows = 0;
-#pragma unroll 1
-    for (int i = 0; i < N; i++) {
-        rows = i + 1;
-        // lane j: t_j = M_ij * (current_j - [x_j, x_j])
-        if (l < N) {
-            double nz = 0.0;
-            ival t = mk(0.0, 0.0);
-            if (l != i) {
-                const ival mij = mk(Jl[i * N + l], Jh[i * N + l]);
-                if (!(mij.lo == 0.0 && mij.hi == 0.0)) {
-                    nz = 1.0;
-                    t = gmul(mij, Fast::sub(mk(sCur[l], sCur[N + l]), mk(xm, xm)));
-                }
-            }
-            sT[l] = t.lo;
-            sT[N + l] = t.hi;
-            sNz[l] = nz;
-        }
-        __syncwarp(gmask);
-        // p = -g_i - sum_{j != i, M_ij != 0} t_j, left to right (redundantly on every lane)
-        ival p = mk(-s[L::oG + N + i], -s[L::oG + i]);
-#pragma unroll 1
-        for (int j = 0; j < N; j++)
-            if (j != i && sNz[j] != 0.0) p = Fast::sub(p, mk(sT[j], sT[N + j]));
-        const ival cur_i = mk(sCur[i], sCur[N + i]);
-        const double xi = s[L::oXm + i];
-        const ival mii = mk(Jl[i * N + i], Jh[i * N + i]);
-        ival q0 = mk(0.0, 0.0), q1 = mk(0.0, 0.0);
-        const int kind = div_extended(p, mii, q0, q1);
-        bool stop = false, update = false;
-        ival newc = cur_i;
-        if (kind == DIV_EMPTY) {
-            outcome = HS_EMPTY;
-            stop = true;
-        } else if (kind != DIV_WHOLE) {
-            const int np = kind == DIV_SPLIT ? 2 : 1;
-            ival pieces[2];
-            int npieces = 0;
-#pragma unroll
-            for (int q = 0; q < 2; q++) {
-                if (q < np) {
-                    const ival y = Fast::add(mk(xi, xi), q == 0 ? q0 : q1);
-                    const double lo = py_max(y.lo, cur_i.lo);  // Interval.intersect, interval.py:358-363
-                    const double hi = py_min(y.hi, cur_i.hi);
-                    if (!(lo > hi)) pieces[npieces++] = mk(lo, hi);
-                }
-            }
-            if (npieces == 0) {
-                outcome = HS_EMPTY;
-                stop = true;
-            } else if (npieces == 1) {
-                newc = pieces[0];
-                update = true;
-            } else {
-                newc = mk(py_min(pieces[0].lo, pieces[1].lo), py_max(pieces[0].hi, pieces[1].hi));  // hull
-                update = true;
-                if (fork_i < 0) {
-                    fork_i = i;
-                    fp0 = pieces[0];
-                    fp1 = pieces[1];
-                }
-            }
-        }
-        __syncwarp(gmask);  // every lane has read sT / sCur of this row
-        if (update && l == 0) {
-            sCur[i] = newc.lo;
-            sCur[N + i] = newc.hi;
-        }
-        __syncwarp(gmask);
-        if (stop) break;
-    }
-    if (outcome == HS_EMPTY) return HS_EMPTY;
-    ival cur = mk(0.0, 0.0);
-    if (l < N) cur = mk(sCur[l], sCur[N + l]);
-    if (fork_i < 0) {
-        // certified iff the output lies strictly inside the input (hansen.py:129-132)
-        int inside = 1;
-        if (l < N) inside = (xin.lo < cur.lo) && (cur.hi < xin.hi);
-        certified = __all_sync(gmask, inside) != 0;
-        o0 = cur;
-        return HS_ONE;
-    }
-    certified = false;
-    o0 = cur;
-    o1 = cur;
-    if (l == fork_i) {
-        o0 = fp0;
-        o1 = fp1;
-    }
-    return HS_TWO;
-}
-
-// G lanes per box; boxes assigned warp-uniformly so warp collectives stay converged.
-// Outputs are appended to `out` after the carried rows (ctr->n_next).  `tags`
-// (test hook) receives 2*row + piece to restore reference order.
 template <int N>
-__global__ void __launch_bounds__(128) k_hs(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
-                                            int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
-                                            int64_t* tags) {
-    using L = HsLayout<N>;
+struct LinLayout {
+    static constexpr int G = N <= 2 ? 4 : (N <= 4 ? 8 : (N <= 8 ? 16 : 32));
+    static constexpr int BPW = 32 / G;
+    static constexpr int oA = 0;           // A[N*N]
+    static constexpr int oCol = N * N;     // pivot column[N] + pivot row
+    static constexpr int doubles = N * N + N + 1;
+};
+
+// M = A J and g = A F(x) (linalg.py:102-129): acc = [0,0]; acc += [a,a] * B[u][j], u ascending.
+// Lane (col, half) holds J[:, col] in registers and produces rows of its half.
+template <int N, class A>
+__device__ __forceinline__ void lin_products(const double* Am, const ival* jcol, int l, int64_t t,
+                                             const HsScratch& W, unsigned gmask) {
+    constexpr int H = (N + 1) / 2;
+    if (l < 2 * N) {
+        const int col = l % N, half = l / N;
+#pragma unroll
+        for (int r = 0; r < H; r++) {
+            const int i = half * H + r;
+            if (i < N) {
+                ival acc = mk(0.0, 0.0);
+#pragma unroll
+                for (int u = 0; u < N; u++) acc = A::add(acc, A::mul_point(Am[i * N + u], jcol[u]));
+                W.jl[(i * N + col) * W.B + t] = acc.lo;
+                W.jh[(i * N + col) * W.B + t] = acc.hi;
+            }
+        }
+    }
+    ival acc = mk(0.0, 0.0);
+    if (l < N) {
+#pragma unroll
+        for (int u = 0; u < N; u++)
+            acc = A::add(acc, A::mul_point(Am[l * N + u], mk(W.fl[u * W.B + t], W.fh[u * W.B + t])));
+    }
+    __syncwarp(gmask);  // every lane has read F(x) before g overwrites it
+    if (l < N) {
+        W.fl[l * W.B + t] = acc.lo;
+        W.fh[l * W.B + t] = acc.hi;
+    }
+}
+
+template <int N>
+__device__ __noinline__ void lin_products_exact(const double* Am, const ival* jcol, int l, int64_t t,
+                                                const HsScratch& W, unsigned gmask) {
+    lin_products<N, Exact>(Am, jcol, l, t, W, gmask);
+}
+
+// K2b: G lanes per box; boxes assigned warp-uniformly.
+template <int N>
+__global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
+                                                Counters* ctr) {
+    using L = LinLayout<N>;
     constexpr int G = L::G;
     extern __shared__ __align__(16) uint8_t smem[];
-    const STab tab = load_stab(meta, gtab, smem, false);
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int gi = lane / G;
-    const int l = lane % G;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
-    double* s = reinterpret_cast<double*>(smem + stab_bytes(meta, false)) +
-                (size_t)(warp * L::BPW + gi) * L::doubles;
-    __syncthreads();
-
-    int64_t n_in = n_in_arg;
-    if (prm.count_from_ctr) {
-        const unsigned long long ns = ctr->n_surv;
-        if (ns > (unsigned long long)S.cap) return;  // overflowed: the host grows S and redoes the round
-        n_in = (int64_t)ns;
-    }
-    // HS trigger (bnb.py:289-296) on the max child width of the filter survivors
     bool hs_on;
-    if (prm.hs_mode == 1) hs_on = true;
-    else if (prm.hs_mode == 2) hs_on = false;
-    else {
-        const double cw = __longlong_as_double((long long)ctr->child_wmax);
-        hs_on = false;
-        if (n_in > 0 && prm.hs_possible) {
-            if (prm.hs_enable_round >= 0 && prm.round_no >= prm.hs_enable_round) hs_on = true;
-            if (!isnan(prm.hs_enable_width) && cw <= prm.hs_enable_width) hs_on = true;
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
-
-    if (!hs_on) {
-        // pass-through: survivors join the frontier uncertified (bnb.py:580-581)
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x < n_in;
-             i += (int64_t)gridDim.x * blockDim.x) {
-            const bool valid = i < n_in;
-            double w = 0.0;
-            const unsigned long long slot = warp_append(valid, &ctr->n_next);
-            if (valid) {
-#pragma unroll
-                for (int j = 0; j < N; j++) {
-                    const double lo = S.lo[j * S.cap + i], hi = S.hi[j * S.cap + i];
-                    const double d = __dsub_rn(hi, lo);
-                    w = j == 0 ? d : (d > w ? d : w);
-                    if (slot < (unsigned long long)out.cap) {
-                        out.lo[j * out.cap + slot] = lo;
-                        out.hi[j * out.cap + slot] = hi;
-                    }
-                }
-                if (slot < (unsigned long long)out.cap) {
-                    out.cert[slot] = 0;
-                    out.unsplit[slot] = 0;
-                }
-                if (tags && slot < (unsigned long long)out.cap) tags[slot] = 2 * i;
-            }
-            unsigned long long wb = valid ? (unsigned long long)__double_as_longlong(w) : 0ull;
-            wb = warp_max(wb);
-            if (lane == 0 && wb) atomicMax(&ctr->wmax, wb);
-        }
-        return;
-    }
-
+    const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
+    if (n_in < 0 || !hs_on) return;
+    const int64_t b_end = min(n_in, b0 + W.B);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gi = lane / G, l = lane % G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
+    double* s = reinterpret_cast<double*>(smem) + (size_t)(warp * L::BPW + gi) * L::doubles;
+    double* Am = s + L::oA;
+    double* sCol = s + L::oCol;
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t wglob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    unsigned long long ops_acc = 0, calls_acc = 0, exact_acc = 0;
-    for (int64_t wb0 = wglob * L::BPW; wb0 < n_in; wb0 += warps_total * L::BPW) {
+    unsigned long long exact_acc = 0;
+    for (int64_t wb0 = b0 + wglob * L::BPW; wb0 < b_end; wb0 += warps_total * L::BPW) {
         const int64_t b = wb0 + gi;
-        const bool valid = b < n_in;
-        int kind = HS_EMPTY;
-        bool cert = false;
-        ival xin = mk(0.0, 0.0), o0 = mk(0.0, 0.0), o1 = mk(0.0, 0.0);
-        unsigned exf = 0;
-        int rows = 0;
-        if (valid) {
-            if (l < N) xin = mk(S.lo[l * S.cap + b], S.hi[l * S.cap + b]);
-            kind = hs_box<N, G>(meta, tab, s, gmask, l, xin, o0, o1, cert, exf, rows);
-            if (l == 0) {
-                calls_acc++;
-                ops_acc += meta.ops_hs_pre + (unsigned long long)meta.ops_hs_row * rows;
-                exact_acc += exf ? 1 : 0;
+        if (b < b_end) {
+            const int64_t t = b - b0;
+            // J column (l % N), kept in registers for M
+            ival jcol[N];
+            double c[N];
+            double colmax = 0.0;
+            ExpRange rj;
+            rj.init();
+            if (l < 2 * N) {
+                const int col = l % N;
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    jcol[i] = mk(W.jl[(i * N + col) * W.B + t], W.jh[(i * N + col) * W.B + t]);
+                    rj.add(jcol[i].lo);
+                    rj.add(jcol[i].hi);
+                }
             }
+            if (l < N) {
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    c[i] = mid_of(jcol[i].lo, jcol[i].hi);  // mid_matrix, linalg.py:132-134
+                    colmax = fmax(colmax, fabs(c[i]));
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < N; i++) c[i] = (l - N == i) ? 1.0 : 0.0;
+            }
+            // Gauss-Jordan inverse (linalg.py:137-172), lane = column of [jc | I]
+            const double scale = group_max<G>(gmask, l < N ? colmax : 0.0);
+            bool singular = scale == 0.0;
+            const double threshold = __dmul_rn(1e-12, scale);
+#pragma unroll
+            for (int k = 0; k < N; k++) {
+                if (singular) break;  // group-uniform
+                if (l == k) {
+                    int pr = k;  // first row r >= k with max |c[r][k]|
+                    double best = fabs(c[k]);
+#pragma unroll
+                    for (int r = k + 1; r < N; r++)
+                        if (fabs(c[r]) > best) {
+                            best = fabs(c[r]);
+                            pr = r;
+                        }
+#pragma unroll
+                    for (int i = 0; i < N; i++) sCol[i] = c[i];
+                    sCol[N] = (double)pr;
+                }
+                __syncwarp(gmask);
+                const int pr = (int)sCol[N];
+                const double pivot = sCol[pr];
+                if (fabs(pivot) < threshold) {
+                    singular = true;
+                } else {
+#pragma unroll
+                    for (int r = k + 1; r < N; r++)
+                        if (r == pr) {
+                            const double tmp = c[k];
+                            c[k] = c[r];
+                            c[r] = tmp;
+                        }
+                    const double inv = __ddiv_rn(1.0, pivot);
+                    if (l >= k && l < 2 * N) {
+                        c[k] = __dmul_rn(c[k], inv);
+#pragma unroll
+                        for (int i = 0; i < N; i++) {
+                            if (i == k) continue;
+                            const double f = sCol[i == pr ? k : i];  // column k after the row swap
+                            if (f != 0.0) c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
+                        }
+                    }
+                }
+                __syncwarp(gmask);
+            }
+            if (singular) {
+                if (l == 0) W.flags[t] |= HSF_SINGULAR;
+            } else {
+                ExpRange ra, rf;
+                ra.init();
+                rf.init();
+                if (l >= N && l < 2 * N) {
+#pragma unroll
+                    for (int i = 0; i < N; i++) {
+                        Am[i * N + (l - N)] = c[i];
+                        ra.add(c[i]);
+                    }
+                }
+                if (l < N) {
+                    rf.add(W.fl[l * W.B + t]);
+                    rf.add(W.fh[l * W.B + t]);
+                }
+                group_reduce<G>(gmask, ra);
+                group_reduce<G>(gmask, rj);
+                group_reduce<G>(gmask, rf);
+                rj.emin = min(rj.emin, rf.emin);
+                rj.emax = max(rj.emax, rf.emax);
+                const bool fastM = prod_guard_ok(ra, rj);
+                __syncwarp(gmask);
+                if (fastM) lin_products<N, Fast>(Am, jcol, l, t, W, gmask);
+                else {
+                    lin_products_exact<N>(Am, jcol, l, t, W, gmask);
+                    if (l == 0) W.flags[t] |= HSF_EXACT_LIN;
+                }
+                exact_acc += (!fastM && l == 0) ? 1 : 0;
+            }
+            __syncwarp(gmask);
         }
         __syncwarp();
+    }
+    (void)exact_acc;
+}
+
+// fast reciprocal-based single case of div_extended; exact emulation elsewhere
+__device__ __forceinline__ int div_extended_fast(ival p, ival y, ival& q0, ival& q1) {
+    if (!contains_zero(y)) {
+        const double al = fabs(y.lo), ah = fabs(y.hi);
+        if (al > 0x1p-990 && ah < 0x1p990) {
+            // _div_rd/_div_ru (interval.py:157-190) == IEEE directed division inside the trusted band
+            const ival r = mk(__ddiv_rd(1.0, y.hi), __ddiv_ru(1.0, y.lo));
+            q0 = gmul(p, r);
+            return DIV_SINGLE;
+        }
+    }
+    return div_extended(p, y, q0, q1);
+}
+
+// K2c: thread per box: the Gauss-Seidel sweep (hansen.py:91-138) and the
+// _hs_pass output rules (bnb.py:197-210), compacted into `out` after the carried rows.
+template <int N>
+__global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm,
+                                                  HsScratch W, Front out, Counters* ctr, int64_t* tags) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    bool hs_on;
+    const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
+    if (n_in < 0 || !hs_on) return;
+    const int64_t b_end = min(n_in, b0 + W.B);
+    const int lane = threadIdx.x & 31;
+    const int stride = blockDim.x;
+    double* cl = reinterpret_cast<double*>(smem) + threadIdx.x;  // current[j].lo at cl[j*stride]
+    double* ch = cl + N * stride;
+    unsigned long long ops_acc = 0, calls_acc = 0;
+    for (int64_t base = b0 + (int64_t)blockIdx.x * blockDim.x; base < b_end; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = base + threadIdx.x;
+        const bool valid = b < b_end;
+        const int64_t t = b - b0;
+        int kind = HS_EMPTY;
+        bool cert = false;
+        int fork_i = -1;
+        ival fp0 = mk(0.0, 0.0), fp1 = mk(0.0, 0.0);
+        int rows = 0;
+        if (valid) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                cl[j * stride] = S.lo[j * S.cap + b];
+                ch[j * stride] = S.hi[j * S.cap + b];
+            }
+            if (W.flags[t] & HSF_SINGULAR) {
+                kind = HS_SKIP;
+            } else {
+                kind = HS_ONE;
+#pragma unroll 1
+                for (int i = 0; i < N; i++) {
+                    rows = i + 1;
+                    // p = -g_i - sum_{j != i, M_ij != [0,0]} M_ij (current_j - [x_j, x_j])
+                    ival p = mk(-W.fh[i * W.B + t], -W.fl[i * W.B + t]);
+#pragma unroll 1
+                    for (int j = 0; j < N; j++) {
+                        if (j == i) continue;
+                        const ival mij = mk(W.jl[(i * N + j) * W.B + t], W.jh[(i * N + j) * W.B + t]);
+                        if (mij.lo == 0.0 && mij.hi == 0.0) continue;
+                        const double xj = W.x[j * W.B + t];
+                        const ival d = Fast::sub(mk(cl[j * stride], ch[j * stride]), mk(xj, xj));
+                        p = Fast::sub(p, gmul(mij, d));
+                    }
+                    const ival mii = mk(W.jl[(i * N + i) * W.B + t], W.jh[(i * N + i) * W.B + t]);
+                    ival q0 = mk(0.0, 0.0), q1 = mk(0.0, 0.0);
+                    const int dk = div_extended_fast(p, mii, q0, q1);
+                    if (dk == DIV_EMPTY) {
+                        kind = HS_EMPTY;
+                        break;
+                    }
+                    if (dk == DIV_WHOLE) continue;
+                    const double xi = W.x[i * W.B + t];
+                    const ival cur_i = mk(cl[i * stride], ch[i * stride]);
+                    ival pieces[2];
+                    int npieces = 0;
+                    const int np = dk == DIV_SPLIT ? 2 : 1;
+#pragma unroll
+                    for (int q = 0; q < 2; q++) {
+                        if (q < np) {
+                            const ival y = Fast::add(mk(xi, xi), q == 0 ? q0 : q1);
+                            const double lo = py_max(y.lo, cur_i.lo);  // Interval.intersect
+                            const double hi = py_min(y.hi, cur_i.hi);
+                            if (!(lo > hi)) pieces[npieces++] = mk(lo, hi);
+                        }
+                    }
+                    if (npieces == 0) {
+                        kind = HS_EMPTY;
+                        break;
+                    }
+                    ival nc = pieces[0];
+                    if (npieces == 2) {
+                        nc = mk(py_min(pieces[0].lo, pieces[1].lo), py_max(pieces[0].hi, pieces[1].hi));  // hull
+                        if (fork_i < 0) {
+                            fork_i = i;
+                            fp0 = pieces[0];
+                            fp1 = pieces[1];
+                        }
+                    }
+                    cl[i * stride] = nc.lo;
+                    ch[i * stride] = nc.hi;
+                }
+                if (kind == HS_ONE && fork_i >= 0) kind = HS_TWO;
+                if (kind == HS_ONE) {  // certified iff strictly inside the input (hansen.py:129-132)
+                    cert = true;
+#pragma unroll
+                    for (int j = 0; j < N; j++)
+                        cert = cert && (S.lo[j * S.cap + b] < cl[j * stride]) && (ch[j * stride] < S.hi[j * S.cap + b]);
+                }
+            }
+            calls_acc++;
+            ops_acc += meta.ops_hs_pre + (unsigned long long)meta.ops_hs_row * rows;
+        }
         // outputs (bnb.py:197-210)
         int cnt = 0;
         bool use_input = false;
@@ -899,32 +921,40 @@ __global__ void __launch_bounds__(128) k_hs(TabMeta meta, const uint8_t* __restr
                 cnt = kind == HS_TWO ? 2 : 1;
             }
         }
-        // warp prefix over groups
-        int off = 0, total = 0;
-#pragma unroll
-        for (int g = 0; g < L::BPW; g++) {
-            const int cg = __shfl_sync(0xffffffffu, cnt, g * G);
-            if (g < gi) off += cg;
-            total += cg;
-        }
-        unsigned long long base = 0;
-        if (lane == 0 && total) base = atomicAdd(&ctr->n_next, (unsigned long long)total);
-        base = __shfl_sync(0xffffffffu, base, 0);
+        const unsigned b1 = __ballot_sync(0xffffffffu, cnt == 1);
+        const unsigned b2 = __ballot_sync(0xffffffffu, cnt == 2);
+        const unsigned lt = lanemask_lt();
+        const unsigned off = __popc(b1 & lt) + 2 * __popc(b2 & lt);
+        const unsigned total = __popc(b1) + 2 * __popc(b2);
+        unsigned long long wbase = 0;
+        if (lane == 0 && total) wbase = atomicAdd(&ctr->n_next, (unsigned long long)total);
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
         double wmax = 0.0;
         for (int q = 0; q < cnt; q++) {
-            const unsigned long long slot = base + off + q;
-            const ival v = use_input ? xin : (q == 0 ? o0 : o1);
+            const unsigned long long slot = wbase + off + q;
             double w = 0.0;
-            if (l < N) {
-                if (slot < (unsigned long long)out.cap) {
-                    out.lo[l * out.cap + slot] = canon0(v.lo);
-                    out.hi[l * out.cap + slot] = canon0(v.hi);
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                double lo, hi;
+                if (use_input) {
+                    lo = S.lo[j * S.cap + b];
+                    hi = S.hi[j * S.cap + b];
+                } else if (j == fork_i) {
+                    lo = q == 0 ? fp0.lo : fp1.lo;
+                    hi = q == 0 ? fp0.hi : fp1.hi;
+                } else {
+                    lo = cl[j * stride];
+                    hi = ch[j * stride];
                 }
-                w = __dsub_rn(v.hi, v.lo);
+                const double d = __dsub_rn(hi, lo);
+                w = j == 0 ? d : (d > w ? d : w);
+                if (slot < (unsigned long long)out.cap) {
+                    out.lo[j * out.cap + slot] = canon0(lo);
+                    out.hi[j * out.cap + slot] = canon0(hi);
+                }
             }
-            w = group_max<G>(gmask, w);
             wmax = fmax(wmax, w);
-            if (l == 0 && slot < (unsigned long long)out.cap) {
+            if (slot < (unsigned long long)out.cap) {
                 out.cert[slot] = cert ? 1 : 0;
                 out.unsplit[slot] = 0;
                 if (tags) tags[slot] = 2 * b + q;
@@ -936,13 +966,12 @@ __global__ void __launch_bounds__(128) k_hs(TabMeta meta, const uint8_t* __restr
     }
     ops_acc = warp_sum(ops_acc);
     calls_acc = warp_sum(calls_acc);
-    exact_acc = warp_sum(exact_acc);
     if (lane == 0) {
         if (ops_acc) atomicAdd(&ctr->hs_ops, ops_acc);
         if (calls_acc) atomicAdd(&ctr->hs_calls, calls_acc);
-        if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
     }
 }
+
 
 // ------------------------------------------------------------------ dedup
 
