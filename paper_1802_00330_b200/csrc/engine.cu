@@ -117,6 +117,9 @@ struct rb_handle {
     uint8_t* r_cert = nullptr;
     uint8_t* r_uns = nullptr;
     int64_t r_n = 0;
+    bool r_on_host = false;  // small results are ordered on the host
+    std::vector<double> hr_lo, hr_hi;
+    std::vector<uint8_t> hr_cert, hr_uns;
     bool have_result = false;
     std::vector<rb_round_stats> stats;
     // sharded protocol state
@@ -134,6 +137,26 @@ struct rb_handle {
     HsScratch W{};
     int smem_optin = 48 * 1024;
 };
+
+// One stream-ordered memory pool per device for the whole process, retaining
+// its memory (release threshold = max): a new handle for the next system reuses
+// the frontier buffers of the last one instead of mapping fresh memory.
+static cudaMemPool_t device_pool(int device) {
+    static std::mutex mu;
+    static std::vector<cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)pools.size() <= device) pools.resize(device + 1, nullptr);
+    if (!pools[device]) {
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = device;
+        ck(cudaMemPoolCreate(&pools[device], &pp), "mempool");
+        uint64_t thr = UINT64_MAX;
+        ck(cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
+    }
+    return pools[device];
+}
 
 struct PoolScope {
     explicit PoolScope(rb_handle* h) {
@@ -230,13 +253,17 @@ struct FilterK {
 // K2a + K2b + K2c over rows [b0, b0 + W.B) of S (n_in read on the device when prm.count_from_ctr)
 template <int N>
 struct HsK {
-    static void run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* tags) {
+    static void run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* tags, int64_t batch_bound) {
         const int T = h->hs_threads;
         const int64_t B = h->W.B;
         Front out = h->F[h->cur ^ 1].f;
         h->launches += 3;
-        k_hs_eval<N><<<grid_for(B, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem, h->st>>>(
-            h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
+        // split each box's n^2 + n polynomials over R threads when the batch is small
+        const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(B, batch_bound));
+        const int64_t target = (int64_t)h->sms * 1024;
+        const int R = (int)std::max<int64_t>(1, std::min<int64_t>(N * N + N, (target + bound - 1) / bound));
+        k_hs_eval<N><<<grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem, h->st>>>(
+            h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags, R);
         k_hs_lin<N><<<grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem,
                       h->st>>>(h->S, n_in, b0, prm, h->W, h->d_ctr);
         k_hs_sweep<N><<<grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem, h->st>>>(
@@ -341,7 +368,8 @@ static void scratch_reserve(rb_handle* h, int64_t want) {
 static void launch_hs_batches(rb_handle* h, int64_t bound, int64_t n_in, const HsParams& prm, int64_t* tags) {
     scratch_reserve(h, std::max<int64_t>(bound, 1));
     const int64_t B = h->W.B;
-    for (int64_t b0 = 0; b0 == 0 || b0 < bound; b0 += B) dispatch_n<HsK>(h->n, h, b0, n_in, prm, tags);
+    for (int64_t b0 = 0; b0 == 0 || b0 < bound; b0 += B)
+        dispatch_n<HsK>(h->n, h, b0, n_in, prm, tags, std::min<int64_t>(B, bound - b0));
 }
 
 static void parents_reserve(rb_handle* h, int64_t need) {
@@ -634,8 +662,7 @@ static void release_all(rb_handle* h) {
     fr(h->W.fl);
     fr(h->W.fh);
     fr(h->W.flags);
-    if (h->st) cudaStreamSynchronize(h->st);
-    if (h->pool) cudaMemPoolDestroy(h->pool);
+    if (h->st) cudaStreamSynchronize(h->st);  // frees are stream-ordered; the pool is shared
     h->pool = nullptr;
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     for (auto& e : h->ev)
@@ -644,6 +671,8 @@ static void release_all(rb_handle* h) {
 }
 
 // canonical order of F[cur] rows [0, N) -> result buffers (row-major)
+constexpr int64_t kHostSortRows = 16384;
+
 static void finalize_sorted(rb_handle* h) {
     const int n = h->n;
     const int64_t N = h->n_cur;
@@ -653,7 +682,51 @@ static void finalize_sorted(rb_handle* h) {
     dalloc(&h->r_cert, (size_t)std::max<int64_t>(N, 1));
     dalloc(&h->r_uns, (size_t)std::max<int64_t>(N, 1));
     h->r_n = N;
+    h->r_on_host = false;
     if (N == 0) return;
+    if (N <= kHostSortRows) {
+        // small final sets: one gather + D2H, then canonical order on the host
+        // (cheaper than 2n radix passes of launch latency)
+        h->launches++;
+        k_gather_rows<<<grid_for(N, 256, h->sms * 8), 256, 0, h->st>>>(f, n, N, nullptr, h->r_lo, h->r_hi,
+                                                                        h->r_cert, h->r_uns);
+        ck(cudaGetLastError(), "gather");
+        std::vector<double> lo((size_t)N * n), hi((size_t)N * n);
+        std::vector<uint8_t> c(N), u(N);
+        ck(cudaMemcpyAsync(lo.data(), h->r_lo, sizeof(double) * N * n, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaMemcpyAsync(hi.data(), h->r_hi, sizeof(double) * N * n, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaMemcpyAsync(c.data(), h->r_cert, N, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaMemcpyAsync(u.data(), h->r_uns, N, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaStreamSynchronize(h->st), "finalize sync");
+        std::vector<int64_t> ord(N);
+        std::iota(ord.begin(), ord.end(), 0);
+        // np.lexsort keys: lo_0..lo_{n-1}, then hi_0..hi_{n-1} (_batch.py:244-250); stable
+        std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+            for (int j = 0; j < n; j++) {
+                const double x = lo[a * n + j], y = lo[b * n + j];
+                if (x < y) return true;
+                if (y < x) return false;
+            }
+            for (int j = 0; j < n; j++) {
+                const double x = hi[a * n + j], y = hi[b * n + j];
+                if (x < y) return true;
+                if (y < x) return false;
+            }
+            return false;
+        });
+        h->hr_lo.resize((size_t)N * n);
+        h->hr_hi.resize((size_t)N * n);
+        h->hr_cert.resize(N);
+        h->hr_uns.resize(N);
+        for (int64_t r = 0; r < N; r++) {
+            std::memcpy(&h->hr_lo[r * n], &lo[ord[r] * n], sizeof(double) * n);
+            std::memcpy(&h->hr_hi[r * n], &hi[ord[r] * n], sizeof(double) * n);
+            h->hr_cert[r] = c[ord[r]];
+            h->hr_uns[r] = u[ord[r]];
+        }
+        h->r_on_host = true;
+        return;
+    }
     const unsigned* perm = nullptr;
     if (N > 1) {
         if (h->cap_sort < N) {
@@ -852,15 +925,7 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         h->sms = prop.multiProcessorCount;
         h->smem_optin = (int)prop.sharedMemPerBlockOptin;
         ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "stream");
-        {
-            cudaMemPoolProps pp{};
-            pp.allocType = cudaMemAllocationTypePinned;
-            pp.location.type = cudaMemLocationTypeDevice;
-            pp.location.id = device;
-            ck(cudaMemPoolCreate(&h->pool, &pp), "mempool");
-            uint64_t thr = UINT64_MAX;
-            ck(cudaMemPoolSetAttribute(h->pool, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
-        }
+        h->pool = device_pool(device);  // process-wide per device: memory outlives handles
         PoolScope ps(h);
         for (auto& e : h->ev) ck(cudaEventCreate(&e), "event");
         build_tables(h, sys);
@@ -913,7 +978,12 @@ int rb_fetch(rb_handle* h, double* lo, double* hi, uint8_t* cert, uint8_t* unspl
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
         PoolScope ps(h);
         const int64_t N = h->r_n;
-        if (N > 0) {
+        if (N > 0 && h->r_on_host) {
+            if (lo) std::memcpy(lo, h->hr_lo.data(), sizeof(double) * N * h->n);
+            if (hi) std::memcpy(hi, h->hr_hi.data(), sizeof(double) * N * h->n);
+            if (cert) std::memcpy(cert, h->hr_cert.data(), N);
+            if (unsplit) std::memcpy(unsplit, h->hr_uns.data(), N);
+        } else if (N > 0) {
             if (lo) ck(cudaMemcpyAsync(lo, h->r_lo, sizeof(double) * N * h->n, cudaMemcpyDeviceToHost, h->st), "d2h");
             if (hi) ck(cudaMemcpyAsync(hi, h->r_hi, sizeof(double) * N * h->n, cudaMemcpyDeviceToHost, h->st), "d2h");
             if (cert) ck(cudaMemcpyAsync(cert, h->r_cert, N, cudaMemcpyDeviceToHost, h->st), "d2h");

@@ -492,7 +492,7 @@ __device__ __forceinline__ int64_t hs_count(const HsParams& prm, const Counters*
 template <int N>
 __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
                                                  int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
-                                                 Front out, Counters* ctr, int64_t* tags) {
+                                                 Front out, Counters* ctr, int64_t* tags, int R) {
     extern __shared__ __align__(16) uint8_t smem[];
     bool hs_on;
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
@@ -539,10 +539,16 @@ __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __
     double* xhi = xs + N * stride + threadIdx.x;
     double* xmid = xs + 2 * N * stride + threadIdx.x;
     __syncthreads();
+    // work item = (poly group r, box t): the n^2 + n polynomials of a box are split
+    // into R groups so small batches still fill the GPU (R = 1 for large batches)
+    constexpr int P = N * N + N;
+    const int64_t nb = b_end - b0;
+    const int64_t items = nb * R;
     unsigned long long exact_acc = 0;
-    for (int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < b_end;
-         b += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = b - b0;
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = it % nb;
+        const int r = (int)(it / nb);
+        const int64_t b = b0 + t;
         ExpRange rx, rm;
         rx.init();
         rm.init();
@@ -553,32 +559,36 @@ __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __
             xlo[j * stride] = lo;
             xhi[j * stride] = hi;
             xmid[j * stride] = m;
-            W.x[j * W.B + t] = m;
+            if (r == 0) W.x[j * W.B + t] = m;
             rx.add(lo);
             rx.add(hi);
             rm.add(m);
         }
         const bool fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
         const bool fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
-        // J(X) (hansen.py:61-63); zero polynomials evaluate to [0,0]
+        const int p0 = (int)((int64_t)r * P / R), p1 = (int)((int64_t)(r + 1) * P / R);
 #pragma unroll 1
-        for (int e = 0; e < N * N; e++) {
-            const ival v = fastJ ? eval_poly<Fast>(tab, N + e, xlo, xhi, stride)
-                                 : eval_poly_exact(tab, N + e, xlo, xhi, stride);
-            W.jl[e * W.B + t] = v.lo;
-            W.jh[e * W.B + t] = v.hi;
+        for (int q = p0; q < p1; q++) {
+            if (q < N * N) {
+                // J(X) (hansen.py:61-63); zero polynomials evaluate to [0,0]
+                const ival v = fastJ ? eval_poly<Fast>(tab, N + q, xlo, xhi, stride)
+                                     : eval_poly_exact(tab, N + q, xlo, xhi, stride);
+                W.jl[q * W.B + t] = v.lo;
+                W.jh[q * W.B + t] = v.hi;
+            } else {
+                // F(x) = eval_point (poly.py:205-207): interval arithmetic on the point box
+                const int i = q - N * N;
+                const ival v = fastF ? eval_poly<Fast>(tab, i, xmid, xmid, stride)
+                                     : eval_poly_exact(tab, i, xmid, xmid, stride);
+                W.fl[i * W.B + t] = v.lo;
+                W.fh[i * W.B + t] = v.hi;
+            }
         }
-        // F(x) = eval_point (poly.py:205-207): interval arithmetic on the point box
-#pragma unroll 1
-        for (int i = 0; i < N; i++) {
-            const ival v = fastF ? eval_poly<Fast>(tab, i, xmid, xmid, stride)
-                                 : eval_poly_exact(tab, i, xmid, xmid, stride);
-            W.fl[i * W.B + t] = v.lo;
-            W.fh[i * W.B + t] = v.hi;
+        if (r == 0) {
+            const bool ex = !(fastJ && fastF);
+            W.flags[t] = ex ? HSF_EXACT_EVAL : 0;
+            exact_acc += ex;
         }
-        const bool ex = !(fastJ && fastF);
-        W.flags[t] = ex ? HSF_EXACT_EVAL : 0;
-        exact_acc += ex;
     }
     exact_acc = warp_sum(exact_acc);
     if (lane == 0 && exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
@@ -841,21 +851,34 @@ __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t 
                 kind = HS_SKIP;
             } else {
                 kind = HS_ONE;
+                double xv[N];
+#pragma unroll
+                for (int j = 0; j < N; j++) xv[j] = W.x[j * W.B + t];
 #pragma unroll 1
                 for (int i = 0; i < N; i++) {
                     rows = i + 1;
-                    // p = -g_i - sum_{j != i, M_ij != [0,0]} M_ij (current_j - [x_j, x_j])
+                    // row i of M, loaded together (independent loads, one latency)
+                    ival mrow[N];
+#pragma unroll
+                    for (int j = 0; j < N; j++)
+                        mrow[j] = mk(W.jl[(i * N + j) * W.B + t], W.jh[(i * N + j) * W.B + t]);
+                    // p = -g_i - sum_{j != i, M_ij != [0,0]} M_ij (current_j - [x_j, x_j]), left to right
                     ival p = mk(-W.fh[i * W.B + t], -W.fl[i * W.B + t]);
-#pragma unroll 1
+#pragma unroll
                     for (int j = 0; j < N; j++) {
                         if (j == i) continue;
-                        const ival mij = mk(W.jl[(i * N + j) * W.B + t], W.jh[(i * N + j) * W.B + t]);
-                        if (mij.lo == 0.0 && mij.hi == 0.0) continue;
-                        const double xj = W.x[j * W.B + t];
-                        const ival d = Fast::sub(mk(cl[j * stride], ch[j * stride]), mk(xj, xj));
-                        p = Fast::sub(p, gmul(mij, d));
+                        if (mrow[j].lo == 0.0 && mrow[j].hi == 0.0) continue;
+                        const ival d = Fast::sub(mk(cl[j * stride], ch[j * stride]), mk(xv[j], xv[j]));
+                        p = Fast::sub(p, gmul(mrow[j], d));
                     }
-                    const ival mii = mk(W.jl[(i * N + i) * W.B + t], W.jh[(i * N + i) * W.B + t]);
+                    ival mii = mrow[0];
+                    double xi = xv[0];
+#pragma unroll
+                    for (int j = 1; j < N; j++)
+                        if (j == i) {
+                            mii = mrow[j];
+                            xi = xv[j];
+                        }
                     ival q0 = mk(0.0, 0.0), q1 = mk(0.0, 0.0);
                     const int dk = div_extended_fast(p, mii, q0, q1);
                     if (dk == DIV_EMPTY) {
@@ -863,7 +886,6 @@ __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t 
                         break;
                     }
                     if (dk == DIV_WHOLE) continue;
-                    const double xi = W.x[i * W.B + t];
                     const ival cur_i = mk(cl[i * stride], ch[i * stride]);
                     ival pieces[2];
                     int npieces = 0;

@@ -221,6 +221,7 @@ def test_init_width_below_target(native):
 
 @pytest.mark.parametrize("name,kw,rounds", [
     ("katsura6", dict(), 3),
+    ("katsura6", dict(), 4),  # 117k-row frontier: exercises the device radix sort path
     ("eco8", dict(), 2),
     ("brown8", dict(target_width=1e-8), 2),
     ("broyden_banded12", dict(target_width=1e-8), 1),
