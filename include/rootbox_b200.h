@@ -181,6 +181,11 @@ int rb_shard_import(rb_handle* h, int64_t keep, const double* lo, const double* 
 /* Current frontier size of the shard. */
 int64_t rb_shard_size(rb_handle* h);
 
+/* Engine tuning knobs (results never depend on them):
+ *   "filter_tab"  1 (default): tabulated per-parent term filter when the tables fit;
+ *                 0: direct per-child evaluation (k_filter). */
+int rb_set_option(rb_handle* h, const char* key, int64_t value);
+
 /* ---- measurement utility ----------------------------------------------------
  * Measured throughput of the FP64 pipe on `device` for the directed-rounding
  * instructions the engine issues (DMUL.RM/RP, DADD.RM/RP; one op each), in

@@ -101,6 +101,8 @@ def lib():
     L.rb_shard_import.restype = i32
     L.rb_shard_size.argtypes = [P]
     L.rb_shard_size.restype = i64
+    L.rb_set_option.argtypes = [P, C.c_char_p, i64]
+    L.rb_set_option.restype = i32
     L.rb_fp64_peak.argtypes = [i32, C.POINTER(C.c_double)]
     L.rb_fp64_peak.restype = i32
     _lib = L
@@ -109,7 +111,7 @@ def lib():
 
 EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch", "rb_filter", "rb_hs",
             "rb_last_error", "rb_destroy", "rb_shard_load", "rb_round_filter", "rb_round_hs",
-            "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak"]
+            "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak", "rb_set_option"]
 
 
 def _p(a):
@@ -146,6 +148,9 @@ class Engine:
         rc = L.rb_create(C.byref(sysd), int(device), C.byref(h))
         _check(rc, None, "rb_create")
         self.h = h
+
+    def set_option(self, key: str, value: int):
+        _check(lib().rb_set_option(self.h, key.encode(), int(value)), self.h, "rb_set_option")
 
     def close(self):
         if getattr(self, "h", None):

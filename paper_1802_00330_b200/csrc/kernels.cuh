@@ -36,6 +36,11 @@ struct TabMeta {
     int ops_eq[MAX_N];              // algorithmic ops per equation
     int ops_hs_pre;                 // ops of HS preconditioning per box
     int ops_hs_row;                 // ops of one sweep row
+    // tabulated filter (k_filter_tab): per-parent term tables
+    int ftab;                       // 1 when the tables fit the shared-memory budget
+    int e_max;                      // max table entries of one equation (per parent)
+    int ent_total;                  // total (term, combo) entries over the equations
+    int off_tbase, off_ent_off, off_ent, bytes2;  // byte offsets (tbase u16[TF], ent_off u16[n+1], ent u32[])
 };
 
 struct STab {
@@ -419,6 +424,194 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
     ops_acc = warp_sum(ops_acc);
     exact_acc = warp_sum(exact_acc);
     if ((threadIdx.x & 31) == 0) {
+        if (ops_acc) atomicAdd(&ctr->filter_ops, ops_acc);
+        if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
+    }
+}
+
+// ------------------------------------------------------------------ K1' tabulated filter
+//
+// Every child of a parent is a product of half intervals of the parent:
+// component j is [lo_j, m_j] or [m_j, hi_j].  A term c * x_v1^e1 * ... * x_vd^ed
+// therefore takes at most 2^d distinct values over the 2^n children.  The block
+// computes those values once per parent (same operands, same operation order as
+// the per-child evaluation, so the bits are identical), and each child thread
+// evaluates an equation as the canonical-order sum of table lookups.  Tables are
+// built lazily per equation, only while some child of the block is still alive
+// (the reference's short-circuit, bnb.py:149-154).
+
+template <int N>
+struct FtabShape {
+    static constexpr int LOGPPB = N >= 8 ? 0 : 8 - N;   // parents per 256-thread work unit (log2)
+    static constexpr int PPB = 1 << LOGPPB;
+    static constexpr int CHLOG = N > 8 ? N - 8 : 0;     // 256-child chunks per parent (log2)
+};
+
+__host__ __device__ inline int ftab_meta_bytes(const TabMeta& m) {
+    return align8(2 * m.TF) + align8(2 * (m.n + 1)) + align8(4 * m.ent_total);
+}
+
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+
+// dynamic shared memory layout of k_filter_tab
+template <int N>
+__host__ __device__ inline int ftab_off_sp(const TabMeta& m) {
+    return align16(stab_bytes(m, true) + ftab_meta_bytes(m));
+}
+template <int N>
+__host__ __device__ inline int ftab_off_table(const TabMeta& m) {
+    return align16(ftab_off_sp<N>(m) + FtabShape<N>::PPB * (3 * N + 1) * 8);
+}
+template <int N>
+__host__ __device__ inline int ftab_smem_bytes(const TabMeta& m) {
+    return ftab_off_table<N>(m) + FtabShape<N>::PPB * m.e_max * 16;
+}
+
+template <class A>
+__device__ __forceinline__ ival term_value(const STab& t, int q, int combo, const double* plo, const double* phi,
+                                           const double* pmid) {
+    const double c = t.coeff[q];
+    const int f0 = t.fac_off[q], f1 = t.fac_off[q + 1];
+    if (f0 == f1) return mk(c, c);
+    const int d = f1 - f0;
+    ival term = mk(c, c);
+    for (int f = f0; f < f1; f++) {
+        const uint32_t fv = t.fac[f];
+        const int v = fv & 0xff, k = fv >> 8;
+        const bool up = (combo >> (d - 1 - (f - f0))) & 1;
+        const ival half = up ? mk(pmid[v], phi[v]) : mk(plo[v], pmid[v]);
+        const ival pw = A::pow(half, k);
+        term = (f == f0) ? A::mul_point(c, pw) : A::mul(term, pw);
+    }
+    return term;
+}
+
+__device__ __noinline__ ival term_value_exact(const STab& t, int q, int combo, const double* plo, const double* phi,
+                                              const double* pmid) {
+    return term_value<Exact>(t, q, combo, plo, phi, pmid);
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
+                                                    const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
+                                                    int64_t* tags) {
+    using Sh = FtabShape<N>;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const STab tab = load_stab(meta, gtab, smem, true);
+    uint8_t* p8 = smem + stab_bytes(meta, true);
+    uint16_t* tbase = reinterpret_cast<uint16_t*>(p8);
+    uint16_t* ent_off = reinterpret_cast<uint16_t*>(p8 + align8(2 * meta.TF));
+    uint32_t* ent = reinterpret_cast<uint32_t*>(p8 + align8(2 * meta.TF) + align8(2 * (N + 1)));
+    double* sp = reinterpret_cast<double*>(smem + ftab_off_sp<N>(meta));  // [PPB][3N + 1]: lo, hi, mid, exact
+    double2* table = reinterpret_cast<double2*>(smem + ftab_off_table<N>(meta));
+    {
+        const uint16_t* g16 = reinterpret_cast<const uint16_t*>(gtab + meta.off_tbase);
+        for (int i = threadIdx.x; i < meta.TF; i += blockDim.x) tbase[i] = g16[i];
+        const uint16_t* g16b = reinterpret_cast<const uint16_t*>(gtab + meta.off_ent_off);
+        for (int i = threadIdx.x; i <= N; i += blockDim.x) ent_off[i] = g16b[i];
+        const uint32_t* g32 = reinterpret_cast<const uint32_t*>(gtab + meta.off_ent);
+        for (int i = threadIdx.x; i < meta.ent_total; i += blockDim.x) ent[i] = g32[i];
+    }
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const unsigned long long n_par = ctr->n_par;
+    const unsigned long long units =
+        N >= 8 ? (n_par << Sh::CHLOG) : ((n_par + Sh::PPB - 1) >> Sh::LOGPPB);
+    unsigned long long ops_acc = 0, exact_acc = 0;
+    for (unsigned long long u = blockIdx.x; u < units; u += gridDim.x) {
+        int lp;
+        unsigned long long pidx, pbase;
+        uint32_t c;
+        if (N >= 8) {
+            lp = 0;
+            pbase = pidx = u >> Sh::CHLOG;
+            c = (uint32_t)(((u & ((1ull << Sh::CHLOG) - 1)) << 8) | (unsigned)tid);
+        } else {
+            lp = tid >> N;
+            pbase = u << Sh::LOGPPB;
+            pidx = pbase + lp;
+            c = (uint32_t)(tid & ((1 << N) - 1));
+        }
+        const bool valid = pidx < n_par;
+        __syncthreads();  // the previous unit is done with sp / table
+        for (int k = tid; k < Sh::PPB * N; k += blockDim.x) {
+            const int l2 = k / N, j = k % N;
+            const unsigned long long p = pbase + l2;
+            double* q = sp + l2 * (3 * N + 1);
+            if (p < n_par) {
+                const uint32_t pe = parents[p];
+                const uint32_t row = pe & 0x7fffffffu;
+                const double lo = cur.lo[j * cur.cap + row], hi = cur.hi[j * cur.cap + row];
+                q[j] = lo;
+                q[N + j] = hi;
+                q[2 * N + j] = mid_of(lo, hi);
+                if (j == 0) q[3 * N] = (pe >> 31) ? 1.0 : 0.0;
+            }
+        }
+        __syncthreads();
+        const double* my = sp + lp * (3 * N + 1);
+        const bool exact = valid && my[3 * N] != 0.0;
+        bool alive = valid;
+        unsigned ops = 0;
+#pragma unroll 1
+        for (int e = 0; e < N; e++) {
+            if (!__syncthreads_or(alive)) break;  // also: everyone is done with the previous tables
+            const int e0 = ent_off[e], E = ent_off[e + 1] - e0;
+            for (int k = tid; k < Sh::PPB * E; k += blockDim.x) {
+                const int l2 = k / E, i = k % E;
+                if (pbase + l2 >= n_par) continue;
+                const uint32_t en = ent[e0 + i];
+                const double* q = sp + l2 * (3 * N + 1);
+                const ival v = (q[3 * N] != 0.0) ? term_value_exact(tab, en & 0xffff, en >> 16, q, q + N, q + 2 * N)
+                                                 : term_value<Fast>(tab, en & 0xffff, en >> 16, q, q + N, q + 2 * N);
+                table[l2 * meta.e_max + i] = make_double2(v.lo, v.hi);
+            }
+            __syncthreads();
+            if (alive) {
+                const double2* tb = table + lp * meta.e_max;
+                ival acc = mk(0.0, 0.0);
+                const int t0 = tab.poly_off[e], t1 = tab.poly_off[e + 1];
+                for (int q = t0; q < t1; q++) {
+                    int combo = 0;
+                    for (int f = tab.fac_off[q]; f < tab.fac_off[q + 1]; f++) {
+                        const int v = tab.fac[f] & 0xff;
+                        combo = (combo << 1) | (int)((c >> (N - 1 - v)) & 1u);
+                    }
+                    const double2 tv = tb[tbase[q] + combo];
+                    acc = exact ? Exact::add(acc, mk(tv.x, tv.y)) : Fast::add(acc, mk(tv.x, tv.y));
+                }
+                ops += meta.ops_eq[e];
+                alive = acc.lo <= 0.0 && 0.0 <= acc.hi;
+            }
+        }
+        ops_acc += ops;
+        exact_acc += exact ? 1 : 0;
+        // survivors -> S (warp ballot + one atomic per warp)
+        const bool keep = alive;
+        const unsigned long long slot = warp_append(keep, &ctr->n_surv);
+        double w = 0.0;
+        if (keep) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                const bool up = (c >> (N - 1 - j)) & 1u;
+                const double cl = up ? my[2 * N + j] : my[j];
+                const double ch = up ? my[N + j] : my[2 * N + j];
+                const double d = __dsub_rn(ch, cl);
+                w = j == 0 ? d : (d > w ? d : w);
+                if (slot < (unsigned long long)S.cap) {
+                    S.lo[j * S.cap + slot] = cl;
+                    S.hi[j * S.cap + slot] = ch;
+                }
+            }
+            if (tags && slot < (unsigned long long)S.cap) tags[slot] = (int64_t)((pidx << N) | c);
+        }
+        unsigned long long wb = keep ? (unsigned long long)__double_as_longlong(w) : 0ull;
+        wb = warp_max(wb);
+        if (lane == 0 && wb) atomicMax(&ctr->child_wmax, wb);
+    }
+    ops_acc = warp_sum(ops_acc);
+    exact_acc = warp_sum(exact_acc);
+    if (lane == 0) {
         if (ops_acc) atomicAdd(&ctr->filter_ops, ops_acc);
         if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
     }

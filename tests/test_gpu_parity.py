@@ -84,10 +84,14 @@ FILTER_SYSTEMS = ["circle_line", "broyden_tri6", "katsura6", "eco8", "brown8", "
                   "reimer5", "noon5", "kinema", "caprasse", "katsura4", "trinks1", "redeco8"]
 
 
+@pytest.mark.parametrize("mode", [1, 0], ids=["tabulated", "direct"])
 @pytest.mark.parametrize("name", FILTER_SYSTEMS)
-def test_filter_random_cells_vs_oracle(native, name):
+def test_filter_random_cells_vs_oracle(native, name, mode):
     spec = golden_spec(name)
-    eng = engine(name)
+    from paper_1802_00330_b200 import _native
+    from paper_1802_00330_b200.system import compile_tables
+    eng = _native.Engine(compile_tables(spec), 0)
+    eng.set_option("filter_tab", mode)
     osys = oracle_sys(name)
     for depth, seed in ((1, 1), (3, 2), (7, 3), (30, 4)):
         P = max(1, min(2048, (1 << 16) >> spec.n))
