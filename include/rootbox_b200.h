@@ -163,8 +163,10 @@ int rb_shard_load(rb_handle* h, const double* lo, const double* hi, const uint8_
 int rb_round_filter(rb_handle* h, int32_t round_no, int64_t* carried, int64_t* survivors,
                     double* child_width, int64_t* children);
 
-/* Round part 2: HS (hs_on decided globally by the caller) + per-shard dedup.
- * Outputs the local frontier size and max width. */
+/* Round part 2: HS (hs_on decided globally by the caller).  The new frontier is
+ * carried + HS rows, NOT yet deduplicated: route rows to their owners first
+ * (rb_shard_partition + exchange), then rb_shard_dedup.  Outputs the local
+ * frontier size and max width. */
 int rb_round_hs(rb_handle* h, int32_t hs_on, int32_t hs_contract, int64_t* n_out,
                 double* width, int64_t* hs_calls);
 
@@ -180,6 +182,22 @@ int rb_shard_import(rb_handle* h, int64_t keep, const double* lo, const double* 
 
 /* Current frontier size of the shard. */
 int64_t rb_shard_size(rb_handle* h);
+
+/* Reorder the shard owner-major: counts[r] rows (in rank order) belong to rank
+ * r = row_hash(row) % world, the ownership that makes per-shard dedup global
+ * (_batch.dedup_sorted, _batch.py:253-266). */
+int rb_shard_partition(rb_handle* h, int32_t world, int64_t* counts);
+
+/* Exact dedup of the shard with flag OR (after the owner exchange); outputs the
+ * number of rows removed and the shard's max RN width (bnb.py:329). */
+int rb_shard_dedup(rb_handle* h, int64_t* dups, double* width);
+
+/* Device-pointer variants of export/import (row-major, e.g. torch CUDA tensors
+ * exchanged with NCCL all_to_all).  Synchronous on the engine stream. */
+int rb_shard_export_device(rb_handle* h, int64_t start, int64_t count, double* dlo, double* dhi, uint8_t* dcert,
+                           uint8_t* duns);
+int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const double* dhi, const uint8_t* dcert,
+                           const uint8_t* duns, int64_t count);
 
 /* Engine tuning knobs (results never depend on them):
  *   "filter_tab"  1 (default): tabulated per-parent term filter when the tables fit;

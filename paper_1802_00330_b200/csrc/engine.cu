@@ -971,6 +971,48 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
         return RB_ERR_CUDA;                                                                \
     }
 
+template <int N>
+struct PartitionK {
+    static void run(rb_handle* h, int world, int64_t* counts) {
+        const int64_t n = h->n_cur;
+        unsigned* owner = nullptr;
+        unsigned long long* cnt = nullptr;
+        dalloc(&owner, (size_t)std::max<int64_t>(n, 1));
+        dalloc(&cnt, (size_t)2 * world);
+        ck(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2 * world, h->st), "memset");
+        const int blocks = grid_for(n, 256, h->sms * 8);
+        h->launches += 2;
+        if (n > 0) k_owner_count<N><<<blocks, 256, 0, h->st>>>(h->F[h->cur].f, n, world, owner, cnt);
+        std::vector<unsigned long long> hc(2 * world);
+        ck(cudaMemcpyAsync(hc.data(), cnt, sizeof(unsigned long long) * world, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaStreamSynchronize(h->st), "sync");
+        unsigned long long off = 0;
+        for (int r = 0; r < world; r++) {
+            counts[r] = (int64_t)hc[r];
+            hc[world + r] = off;
+            off += hc[r];
+        }
+        ck(cudaMemcpyAsync(cnt + world, hc.data() + world, sizeof(unsigned long long) * world, cudaMemcpyHostToDevice,
+                           h->st), "h2d");
+        if (n > 0) k_owner_scatter<N><<<blocks, 256, 0, h->st>>>(h->F[h->cur].f, n, owner, cnt + world,
+                                                                h->F[h->cur ^ 1].f);
+        ck(cudaGetLastError(), "partition");
+        h->cur ^= 1;
+        dfree(owner);
+        dfree(cnt);
+        ck(cudaStreamSynchronize(h->st), "sync");
+    }
+};
+
+template <int N>
+struct WidthK {
+    static void run(rb_handle* h) {
+        h->launches++;
+        k_width<N><<<grid_for(h->n_cur, 256, h->sms * 8), 256, 0, h->st>>>(h->F[h->cur].f, h->n_cur, h->d_ctr);
+        ck(cudaGetLastError(), "width");
+    }
+};
+
 extern "C" {
 
 const char* rb_version(void) { return RB_VERSION; }
@@ -1257,7 +1299,7 @@ int rb_round_hs(rb_handle* h, int32_t hs_on, int32_t hs_contract, int64_t* n_out
         prm.hs_mode = hs_on ? 1 : 2;
         prm.contract_output = hs_contract ? 1 : 0;
         for (;;) {
-            launch_hs_phase(h, prm, true);
+            launch_hs_phase(h, prm, false);  // exact dedup runs after the owner exchange (rb_shard_dedup)
             sync_counters(h);
             if (h->h_ctr->n_next > (unsigned long long)h->F[h->cur ^ 1].f.cap) {
                 // redo the round with a larger frontier (the input rows are preserved)
@@ -1334,6 +1376,92 @@ int rb_shard_import(rb_handle* h, int64_t keep, const double* lo, const double* 
 }
 
 int64_t rb_shard_size(rb_handle* h) { return h ? h->n_cur : -1; }
+
+int rb_shard_partition(rb_handle* h, int32_t world, int64_t* counts) {
+    if (!h || world < 1 || !counts) return RB_ERR_ARG;
+    std::lock_guard<std::mutex> lk(h->mu);
+    RB_GUARD(h, {
+        ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
+        fronts_reserve(h, std::max<int64_t>(h->n_cur, 1));
+        dispatch_n<PartitionK>(h->n, h, (int)world, counts);
+    })
+}
+
+int rb_shard_dedup(rb_handle* h, int64_t* dups, double* width) {
+    if (!h) return RB_ERR_ARG;
+    std::lock_guard<std::mutex> lk(h->mu);
+    RB_GUARD(h, {
+        ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
+        fronts_reserve(h, std::max<int64_t>(h->n_cur, 1));
+        // the dedup kernels read the row count from the counters (n_next) and skip
+        // on overflow (n_surv <= S.cap is trivially true here)
+        Counters c{};
+        c.n_next = (unsigned long long)h->n_cur;
+        ck(cudaMemcpyAsync(h->d_ctr, &c, sizeof(Counters), cudaMemcpyHostToDevice, h->st), "ctr h2d");
+        if (h->n_cur >= 2) dispatch_n<DedupK>(h->n, h, h->F[h->cur].f, h->F[h->cur ^ 1].f);
+        sync_counters(h);
+        const int64_t d = (int64_t)h->h_ctr->dups;
+        if (d > 0) h->cur ^= 1;  // compacted into the other buffer
+        h->n_cur -= d;
+        ck(cudaMemsetAsync(&h->d_ctr->wmax, 0, sizeof(unsigned long long), h->st), "memset");
+        if (h->n_cur > 0) dispatch_n<WidthK>(h->n, h);
+        sync_counters(h);
+        if (dups) *dups = d;
+        if (width) *width = h->n_cur ? bits_to_double(h->h_ctr->wmax) : 0.0;
+    })
+}
+
+// row-major device buffers (e.g. torch CUDA tensors) <-> the shard; synchronous on the engine stream
+int rb_shard_export_device(rb_handle* h, int64_t start, int64_t count, double* dlo, double* dhi, uint8_t* dcert,
+                           uint8_t* duns) {
+    if (!h || start < 0 || count < 0) return RB_ERR_ARG;
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (start + count > h->n_cur) {
+        h->err = "export range beyond the shard";
+        return RB_ERR_ARG;
+    }
+    RB_GUARD(h, {
+        ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
+        if (count == 0) return RB_OK;
+        Front f = h->F[h->cur].f, sub = f;
+        sub.lo = f.lo + start;
+        sub.hi = f.hi + start;
+        sub.cert = f.cert + start;
+        sub.unsplit = f.unsplit + start;
+        h->launches++;
+        k_gather_rows<<<grid_for(count, 256, h->sms * 8), 256, 0, h->st>>>(sub, h->n, count, nullptr, dlo, dhi,
+                                                                            dcert, duns);
+        ck(cudaGetLastError(), "export gather");
+        ck(cudaStreamSynchronize(h->st), "export sync");
+    })
+}
+
+int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const double* dhi, const uint8_t* dcert,
+                           const uint8_t* duns, int64_t count) {
+    if (!h || keep < 0 || count < 0) return RB_ERR_ARG;
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (keep > h->n_cur) {
+        h->err = "keep beyond the shard";
+        return RB_ERR_ARG;
+    }
+    RB_GUARD(h, {
+        ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
+        h->n_cur = keep;
+        fronts_reserve(h, keep + count);
+        if (count > 0) {
+            h->launches++;
+            k_rows_to_soa<<<grid_for(count, 256, h->sms * 8), 256, 0, h->st>>>(dlo, dhi, dcert, duns, h->n, count,
+                                                                                h->F[h->cur].f, keep);
+            ck(cudaGetLastError(), "import");
+            ck(cudaStreamSynchronize(h->st), "import sync");
+        }
+        h->n_cur = keep + count;
+    })
+}
 
 int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     if (!h || !key) return RB_ERR_ARG;

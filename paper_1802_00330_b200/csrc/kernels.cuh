@@ -1288,6 +1288,55 @@ __global__ void k_dedup_finish(Front src, Front dst, unsigned* table, const unsi
     }
 }
 
+// ------------------------------------------------------------------ sharding
+
+// Owner rank of a row = row_hash % world (the same function is restated in
+// paper_1802_00330_b200/dist.py).  Routing every row to its owner each round keeps
+// exact duplicates on one shard, so per-shard dedup is global dedup.
+template <int N>
+__global__ void k_owner_count(Front f, int64_t n, int world, unsigned* owner, unsigned long long* counts) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned o = (unsigned)(row_hash<N>(f, i) % (unsigned long long)world);
+        owner[i] = o;
+        atomicAdd(&counts[o], 1ull);
+    }
+}
+
+template <int N>
+__global__ void k_owner_scatter(Front src, int64_t n, const unsigned* owner, unsigned long long* cursor, Front dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long slot = atomicAdd(&cursor[owner[i]], 1ull);
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            dst.lo[j * dst.cap + slot] = src.lo[j * src.cap + i];
+            dst.hi[j * dst.cap + slot] = src.hi[j * src.cap + i];
+        }
+        dst.cert[slot] = src.cert[i];
+        dst.unsplit[slot] = src.unsplit[i];
+    }
+}
+
+// max RN width over rows (bnb.py:329)
+template <int N>
+__global__ void k_width(Front f, int64_t n, Counters* ctr) {
+    unsigned long long wb = 0;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        if (i < n) {
+            double w = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                const double d = __dsub_rn(f.hi[j * f.cap + i], f.lo[j * f.cap + i]);
+                w = j == 0 ? d : (d > w ? d : w);
+            }
+            const unsigned long long b = (unsigned long long)__double_as_longlong(w);
+            wb = b > wb ? b : wb;
+        }
+    }
+    wb = warp_max(wb);
+    if ((threadIdx.x & 31) == 0 && wb) atomicMax(&ctr->wmax, wb);
+}
+
 // ------------------------------------------------------------------ canonical order
 
 __device__ __forceinline__ unsigned long long order_key(double v) {

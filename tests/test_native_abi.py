@@ -8,7 +8,7 @@ from conftest import ROOT
 def declared_symbols():
     with open(os.path.join(ROOT, "include", "rootbox_b200.h")) as f:
         txt = f.read()
-    return sorted(set(re.findall(r"\b(rb_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(rb_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_library_exports_header_symbols():
