@@ -201,7 +201,10 @@ int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const 
 
 /* Engine tuning knobs (results never depend on them):
  *   "filter_tab"  1 (default): tabulated per-parent term filter when the tables fit;
- *                 0: direct per-child evaluation (k_filter). */
+ *                 0: direct per-child evaluation (k_filter).
+ *   "graph"       1 (default): rounds whose worst case fits the survivor buffer run
+ *                 in one CUDA graph (device-side WHILE loop, no host round trip);
+ *                 0: host-driven rounds (per-kernel CUDA-event timings in the stats). */
 int rb_set_option(rb_handle* h, const char* key, int64_t value);
 
 /* ---- measurement utility ----------------------------------------------------

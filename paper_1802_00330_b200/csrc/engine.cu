@@ -123,6 +123,16 @@ struct rb_handle {
     std::vector<uint8_t> hr_cert, hr_uns;
     bool have_result = false;
     std::vector<rb_round_stats> stats;
+    // device-resident round loop (CUDA graph with a WHILE node)
+    bool use_graph = true;
+    DevState* d_state = nullptr;
+    DevState* h_state = nullptr;  // pinned
+    DevRoundStats* d_rstats = nullptr;
+    int cap_rstats = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    std::vector<uintptr_t> graph_key;
+    int64_t graph_launches_per_round = 0;
     // sharded protocol state
     double shard_target = 0.0;
     int64_t shard_carried = 0;
@@ -231,11 +241,11 @@ struct SetupK {
 
 template <int N>
 struct ClassifyK {
-    static void run(rb_handle* h, double target) {
+    static void run(rb_handle* h, double target, const DevState* st = nullptr, int64_t bound = -1) {
         Front cur = h->F[h->cur].f, next = h->F[h->cur ^ 1].f;
-        const int blocks = grid_for(h->n_cur, 256, h->sms * 8);
+        const int blocks = grid_for(bound >= 0 ? bound : h->n_cur, 256, h->sms * 8);
         h->launches++;
-        k_classify<N><<<blocks, 256, 0, h->st>>>(h->meta, cur, h->n_cur, next, h->parents, h->d_ctr, target);
+        k_classify<N><<<blocks, 256, 0, h->st>>>(h->meta, cur, h->n_cur, next, h->parents, h->d_ctr, target, st);
         ck(cudaGetLastError(), "classify launch");
     }
 };
@@ -291,6 +301,14 @@ struct HsK {
         k_hs_sweep<N><<<grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem, h->st>>>(
             h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
         ck(cudaGetLastError(), "hs launch");
+    }
+};
+
+template <int N>
+struct SettleK {
+    static void run(rb_handle* h, int64_t bound) {
+        k_settle<N><<<grid_for(bound, 256, h->sms * 8), 256, 0, h->st>>>(h->F[1].f, h->F[0].f, h->d_ctr);
+        ck(cudaGetLastError(), "settle launch");
     }
 };
 
@@ -711,6 +729,14 @@ static void run_round(rb_handle* h, double target, const HsParams& prm, bool ded
     }
 }
 
+static void graph_release(rb_handle* h) {
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    if (h->graph) cudaGraphDestroy(h->graph);
+    h->graph_exec = nullptr;
+    h->graph = nullptr;
+    h->graph_key.clear();
+}
+
 static void release_all(rb_handle* h) {
     h->F[0].release();
     h->F[1].release();
@@ -723,6 +749,8 @@ static void release_all(rb_handle* h) {
     fr(h->d_table);
     fr(h->d_dead);
     fr(h->d_slot);
+    fr(h->d_rstats);
+    fr(h->d_state);
     fr(h->d_cub);
     fr(h->d_keys[0]);
     fr(h->d_keys[1]);
@@ -741,7 +769,10 @@ static void release_all(rb_handle* h) {
     fr(h->W.flags);
     if (h->st) cudaStreamSynchronize(h->st);  // frees are stream-ordered; the pool is shared
     h->pool = nullptr;
+    graph_release(h);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
+    if (h->h_state) cudaFreeHost(h->h_state);
+    h->h_state = nullptr;
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     if (h->st) cudaStreamDestroy(h->st);
@@ -848,6 +879,144 @@ static double now_s() {
     return duration<double>(steady_clock::now().time_since_epoch()).count();
 }
 
+// ---------------------------------------------------------------- device round loop
+
+// Rounds whose worst case (n_cur * 2^n children) fits the survivor buffer run
+// inside one CUDA graph: a WHILE node whose body is one round (classify, filter,
+// HS, dedup, settle, k_round_end).  No host round trip per round; the frontier
+// always comes back to F[0] (k_settle), so the body's parameters are fixed.
+static int64_t graph_small_cap(int n) {
+    int64_t c = (int64_t)1 << std::min(30, n + 10);
+    return std::min<int64_t>(std::max<int64_t>(c, (int64_t)1 << 16), (int64_t)1 << 18);
+}
+
+__global__ void k_state_start(DevState* st) { st->t_round_ns = gtimer(); }
+
+static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int64_t scap,
+                              const std::vector<uintptr_t>& key) {
+    graph_release(h);
+    const int n = h->n;
+    cudaGraph_t g = nullptr;
+    ck(cudaGraphCreate(&g, 0), "graph create");
+    cudaGraphConditionalHandle hw;
+    ck(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault), "cond handle");
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hw;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    ck(cudaGraphAddNode(&node, g, nullptr, 0, &cp), "while node");
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    ck(cudaStreamBeginCaptureToGraph(h->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+       "begin capture");
+    const int64_t l0 = h->launches;
+    h->cur = 0;
+    const int64_t fcap = h->F[0].f.cap;
+    dispatch_n<ClassifyK>(n, h, 0.0, (const DevState*)h->d_state, std::min<int64_t>(fcap, scap));
+    dispatch_n<FilterK>(n, h, std::max<int64_t>(1, scap >> n), (int64_t*)nullptr);
+    HsParams p = prm;
+    p.count_from_ctr = 1;
+    p.st = h->d_state;
+    launch_hs_batches(h, scap, 0, p, nullptr);
+    if (dedup) dispatch_n<DedupK>(n, h, h->F[1].f, h->F[0].f);
+    dispatch_n<SettleK>(n, h, std::min<int64_t>(fcap, 3 * scap));
+    h->launches++;
+    k_round_end<<<1, 32, 0, h->st>>>(h->d_state, h->d_ctr, h->d_rstats, n, scap, hw);
+    h->launches++;
+    cudaGraph_t captured = nullptr;
+    ck(cudaStreamEndCapture(h->st, &captured), "end capture");
+    h->graph_launches_per_round = h->launches - l0;
+    h->launches = l0;
+    ck(cudaGraphInstantiate(&h->graph_exec, g, 0), "graph instantiate");
+    h->graph = g;
+    h->graph_key = key;
+}
+
+// Runs rounds on the device while they fit; returns true when the solve finished
+// (status in *status), false when the host must continue from h->stats.size() + 1.
+static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool hs_possible, int* status) {
+    const int n = h->n;
+    int64_t scap = graph_small_cap(n);
+    surv_reserve(h, scap);
+    scap = std::min<int64_t>(h->S.cap, (int64_t)1 << 20);
+    scratch_reserve(h, scap);
+    if (h->W.B < scap) scap = h->W.B;
+    fronts_reserve(h, (scap >> n) + 2 * scap + 1);
+    parents_reserve(h, std::max<int64_t>(1, (scap >> n) + 1));
+    if (h->cap_rstats < cfg->max_rounds) {
+        dalloc(&h->d_rstats, (size_t)cfg->max_rounds);
+        h->cap_rstats = cfg->max_rounds;
+    }
+    if (!h->d_state) dalloc(&h->d_state, 1);
+    HsParams prm{};
+    prm.hs_mode = 0;
+    prm.hs_enable_round = cfg->hs_enable_round;
+    prm.hs_possible = hs_possible ? 1 : 0;
+    prm.hs_enable_width = cfg->hs_enable_width;
+    prm.contract_output = cfg->hs_contract ? 1 : 0;
+    const bool dedup = cfg->exact_round_dedup != 0;
+    uint64_t hw_bits;
+    std::memcpy(&hw_bits, &cfg->hs_enable_width, 8);
+    std::vector<uintptr_t> key = {
+        (uintptr_t)h->F[0].f.lo, (uintptr_t)h->F[0].f.hi, (uintptr_t)h->F[0].f.cert, (uintptr_t)h->F[0].f.unsplit,
+        (uintptr_t)h->F[1].f.lo, (uintptr_t)h->F[1].f.hi, (uintptr_t)h->F[1].f.cert, (uintptr_t)h->F[1].f.unsplit,
+        (uintptr_t)h->F[0].f.cap, (uintptr_t)h->F[1].f.cap, (uintptr_t)h->S.lo, (uintptr_t)h->S.hi,
+        (uintptr_t)h->S.cap, (uintptr_t)h->parents, (uintptr_t)h->W.x, (uintptr_t)h->W.jl, (uintptr_t)h->W.jh,
+        (uintptr_t)h->W.fl, (uintptr_t)h->W.fh, (uintptr_t)h->W.flags, (uintptr_t)h->W.B, (uintptr_t)h->d_table,
+        (uintptr_t)h->table_slots, (uintptr_t)h->d_slot, (uintptr_t)h->d_dead, (uintptr_t)h->d_rstats,
+        (uintptr_t)h->d_state, (uintptr_t)scap, (uintptr_t)dedup, (uintptr_t)prm.hs_enable_round,
+        (uintptr_t)prm.hs_possible, (uintptr_t)hw_bits, (uintptr_t)prm.contract_output,
+        (uintptr_t)(h->use_ftab ? 1 : 0)};
+    if (key != h->graph_key || !h->graph_exec) build_round_graph(h, prm, dedup, scap, key);
+    DevState st{};
+    st.n_cur = (unsigned long long)h->n_cur;
+    st.target = target;
+    st.max_boxes = cfg->max_boxes;
+    st.round_no = (int)h->stats.size() + 1;
+    st.max_rounds = cfg->max_rounds;
+    st.status = RB_BUDGET_EXHAUSTED;
+    *h->h_state = st;
+    ck(cudaMemcpyAsync(h->d_state, h->h_state, sizeof(DevState), cudaMemcpyHostToDevice, h->st), "state h2d");
+    ck(cudaMemsetAsync(h->d_ctr, 0, sizeof(Counters), h->st), "ctr memset");
+    k_state_start<<<1, 1, 0, h->st>>>(h->d_state);
+    ck(cudaGraphLaunch(h->graph_exec, h->st), "graph launch");
+    ck(cudaMemcpyAsync(h->h_state, h->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, h->st), "state d2h");
+    ck(cudaStreamSynchronize(h->st), "graph sync");
+    const DevState& r = *h->h_state;
+    const int first = (int)h->stats.size();
+    const int nr = r.nrounds - first;
+    if (nr > 0) {
+        std::vector<DevRoundStats> rs(nr);
+        ck(cudaMemcpy(rs.data(), h->d_rstats + first, sizeof(DevRoundStats) * nr, cudaMemcpyDeviceToHost),
+           "stats d2h");
+        for (const auto& x : rs) {
+            rb_round_stats o{};
+            o.round = (int32_t)x.round;
+            o.hs_on = (int32_t)x.hs_on;
+            o.boxes_in = x.boxes_in;
+            o.boxes_after_filter = x.after_filter;
+            o.boxes_after_hs = x.after_hs;
+            o.width = x.width;
+            o.elapsed_seconds = x.elapsed;
+            o.children = x.children;
+            o.hs_calls = x.hs_calls;
+            o.filter_ops = x.filter_ops;
+            o.hs_ops = x.hs_ops;
+            o.dups = x.dups;
+            o.exact_boxes = x.exact;
+            o.attempts = 1;
+            o.classify_bytes = x.boxes_in * (16 * n + 2) + (x.after_filter - 0) * 0;
+            h->stats.push_back(o);
+        }
+        h->launches += (int64_t)nr * h->graph_launches_per_round + 3;
+    }
+    h->cur = 0;
+    h->n_cur = (int64_t)r.n_cur;
+    if (r.done) *status = r.status;
+    return r.done != 0;
+}
+
 static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info) {
     const int n = h->n;
     const double t_start = now_s();
@@ -881,10 +1050,15 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
     const bool hs_possible = cfg->hs_enable_round >= 0 || !std::isnan(cfg->hs_enable_width);
     const bool has_max_seconds = cfg->max_seconds >= 0;
     int status = RB_BUDGET_EXHAUSTED;
+    bool finished = false;
     if (init_width <= target) {
         status = RB_WIDTH_REACHED;
-    } else {
-        for (int round_no = 1; round_no <= cfg->max_rounds; round_no++) {
+        finished = true;
+    } else if (h->use_graph && !has_max_seconds) {
+        finished = graph_rounds(h, cfg, target, hs_possible, &status);
+    }
+    if (!finished) {
+        for (int round_no = (int)h->stats.size() + 1; round_no <= cfg->max_rounds; round_no++) {
             const double t0 = now_s();
             RoundOut ro{};
             HsParams prm{};
@@ -1053,6 +1227,7 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         h->mem_budget = (size_t)(0.80 * (double)free_b);
         dalloc(&h->d_ctr, 1);
         ck(cudaMallocHost((void**)&h->h_ctr, sizeof(Counters)), "pinned ctr");
+        ck(cudaMallocHost((void**)&h->h_state, sizeof(DevState)), "pinned state");
         dispatch_n<SetupK>(h->n, h);
         *out = h;
         return RB_OK;
@@ -1469,6 +1644,10 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     const std::string k(key);
     if (k == "filter_tab") {
         h->use_ftab = value != 0;
+        return RB_OK;
+    }
+    if (k == "graph") {
+        h->use_graph = value != 0;
         return RB_OK;
     }
     h->err = "unknown option " + k;

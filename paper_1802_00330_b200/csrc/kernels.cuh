@@ -250,6 +250,33 @@ __device__ __forceinline__ unsigned long long warp_append(bool pred, unsigned lo
     return base + (unsigned long long)__popc(b & lanemask_lt()) * mult;
 }
 
+// ------------------------------------------------------------------ device-resident round loop state
+
+// State of a solve whose round loop runs on the device (a CUDA graph WHILE node,
+// engine.cu): the kernels read the frontier size, target and round number here
+// instead of from launch parameters, and k_round_end advances it.
+struct DevState {
+    unsigned long long n_cur;   // rows of the current frontier (always in F[0] in graph mode)
+    double target;
+    long long max_boxes;
+    int round_no;               // round being executed (1-based)
+    int max_rounds;
+    int done, bail, status, nrounds;
+    int n_small_log2;           // bail when n_cur << n exceeds S capacity
+    unsigned long long t_round_ns;
+};
+
+struct DevRoundStats {
+    long long round, boxes_in, after_filter, after_hs, children, hs_calls, filter_ops, hs_ops, dups, exact, hs_on;
+    double width, elapsed;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ------------------------------------------------------------------ K3 classify
 
 // bnb.py:249-269.  Carried rows (done: width <= target or unsplittable; or
@@ -257,8 +284,11 @@ __device__ __forceinline__ unsigned long long warp_append(bool pred, unsigned lo
 // their flags (degenerate -> cert 0, unsplit 1); the rest become parents.
 // Parent entries carry the filter guard verdict in bit 31 (1 = exact path).
 template <int N>
-__global__ void __launch_bounds__(256) k_classify(TabMeta meta, Front cur, int64_t n_cur, Front next,
-                                                  uint32_t* parents, Counters* ctr, double target) {
+__global__ void __launch_bounds__(256) k_classify(TabMeta meta, Front cur, int64_t n_cur_arg, Front next,
+                                                  uint32_t* parents, Counters* ctr, double target_arg,
+                                                  const DevState* st) {
+    const int64_t n_cur = st ? (int64_t)st->n_cur : n_cur_arg;
+    const double target = st ? st->target : target_arg;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_cur; base += stride) {
         const int64_t i = base + threadIdx.x;
@@ -640,6 +670,7 @@ struct HsParams {
     double hs_enable_width;// NaN: None
     int contract_output;   // SolverConfig.hs_contract
     int count_from_ctr;    // n_in = ctr->n_surv instead of n_in arg
+    const DevState* st;    // graph mode: the round number comes from the device state
 };
 
 struct HsScratch {         // SoA with stride B (batch capacity)
@@ -671,9 +702,10 @@ __device__ __forceinline__ int64_t hs_count(const HsParams& prm, const Counters*
     else if (prm.hs_mode == 2) hs_on = false;
     else {  // bnb.py:289-296 on the max width of the filter survivors
         const double cw = __longlong_as_double((long long)ctr->child_wmax);
+        const int round_no = prm.st ? prm.st->round_no : prm.round_no;
         hs_on = false;
         if (n_in > 0 && prm.hs_possible) {
-            if (prm.hs_enable_round >= 0 && prm.round_no >= prm.hs_enable_round) hs_on = true;
+            if (prm.hs_enable_round >= 0 && round_no >= prm.hs_enable_round) hs_on = true;
             if (!isnan(prm.hs_enable_width) && cw <= prm.hs_enable_width) hs_on = true;
         }
     }
@@ -1286,6 +1318,69 @@ __global__ void k_dedup_finish(Front src, Front dst, unsigned* table, const unsi
             dst.unsplit[slot] = src.unsplit[i];
         }
     }
+}
+
+// ------------------------------------------------------------------ graph-mode round end
+
+// Bring the round's frontier back into F[0]: k_dedup_finish already compacted
+// into F[0] when duplicates were removed; otherwise copy F[1] -> F[0].
+template <int N>
+__global__ void k_settle(Front f1, Front f0, const Counters* ctr) {
+    if (ctr->dups != 0) return;
+    const int64_t n = (int64_t)ctr->n_next;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            f0.lo[j * f0.cap + i] = f1.lo[j * f1.cap + i];
+            f0.hi[j * f0.cap + i] = f1.hi[j * f1.cap + i];
+        }
+        f0.cert[i] = f1.cert[i];
+        f0.unsplit[i] = f1.unsplit[i];
+    }
+}
+
+// Round statistics, termination (bnb.py:339-352) and the WHILE condition of the
+// device round loop; also clears the counters for the next round.
+__global__ void k_round_end(DevState* st, Counters* ctr, DevRoundStats* stats, int n, int64_t s_cap,
+                            cudaGraphConditionalHandle h_while) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const Counters c = *ctr;
+    const unsigned long long after = c.n_next - c.dups;
+    const double width = after ? __longlong_as_double((long long)c.wmax) : 0.0;
+    const unsigned long long now = gtimer();
+    DevRoundStats& r = stats[st->round_no - 1];
+    r.round = st->round_no;
+    r.boxes_in = (long long)st->n_cur;
+    r.after_filter = (long long)(c.n_carried + c.n_surv);
+    r.after_hs = (long long)after;
+    r.children = (long long)(c.n_par << n);
+    r.hs_calls = (long long)c.hs_calls;
+    r.filter_ops = (long long)c.filter_ops;
+    r.hs_ops = (long long)c.hs_ops;
+    r.dups = (long long)c.dups;
+    r.exact = (long long)c.exact_boxes;
+    r.hs_on = (long long)c.hs_on;
+    r.width = width;
+    r.elapsed = (double)(now - st->t_round_ns) * 1e-9;
+    st->t_round_ns = now;
+    st->n_cur = after;
+    st->nrounds = st->round_no;
+    if (after == 0) {
+        st->done = 1;
+        st->status = 0;  // no_real_solution
+    } else if (width <= st->target) {
+        st->done = 1;
+        st->status = 1;  // width_reached
+    } else if ((long long)after > st->max_boxes || st->round_no >= st->max_rounds) {
+        st->done = 1;
+        st->status = 2;  // budget_exhausted
+    } else {
+        st->round_no += 1;
+        if ((after << n) > (unsigned long long)s_cap) st->bail = 1;  // next round needs the host
+    }
+    unsigned long long* w = reinterpret_cast<unsigned long long*>(ctr);
+    for (int i = 0; i < (int)(sizeof(Counters) / 8); i++) w[i] = 0ull;
+    cudaGraphSetConditional(h_while, (st->done || st->bail) ? 0u : 1u);
 }
 
 // ------------------------------------------------------------------ sharding

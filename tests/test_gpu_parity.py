@@ -187,12 +187,20 @@ def check_against_golden(case, out, meta):
     assert not np.any(np.signbit(lo) & (lo == 0)) and not np.any(np.signbit(hi) & (hi == 0))
 
 
+@pytest.mark.parametrize("graph", [1, 0], ids=["device_loop", "host_loop"])
 @pytest.mark.parametrize("case", solve_cases())
-def test_solve_vs_reference_golden(native, case):
+def test_solve_vs_reference_golden(native, case, graph):
+    """Whole solves, with the round loop on the device (CUDA graph WHILE node)
+    and host-driven, against the reference's recorded results."""
     from paper_1802_00330_b200 import bnb
     meta = load_solve(case)
     spec = golden_spec(meta["system"])
-    out = bnb.solve_arrays(spec, bnb.SolverConfig(**meta["config"]))
+    eng = bnb.engine_for(spec)
+    eng.set_option("graph", graph)
+    try:
+        out = eng.solve(bnb.native_config(bnb.SolverConfig(**meta["config"])))
+    finally:
+        eng.set_option("graph", 1)
     check_against_golden(case, out, meta)
 
 
