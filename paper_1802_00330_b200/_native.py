@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "librootbox_b200.so")
+LIB_PATH = os.environ.get("RB_LIB_PATH") or os.path.join(PKG, "librootbox_b200.so")  # override: A/B builds
 
 RB_NO_REAL_SOLUTION, RB_WIDTH_REACHED, RB_BUDGET_EXHAUSTED = 0, 1, 2
 STATUS_NAMES = {0: "no_real_solution", 1: "width_reached", 2: "budget_exhausted"}

@@ -856,6 +856,18 @@ struct LinLayout {
     static constexpr int doubles = N * N + N + 1;
 };
 
+// [a,a] * [l,h] as min/max of both directed products (no sign selects): for a >= 0
+// the minimum is RD(a l), for a < 0 it is RD(a h) -- the 4-product min/max of
+// interval.py:322-326 for a point left operand.
+__device__ __forceinline__ ival pmul_minmax(double a, ival y) {
+    return mk(fmin(__dmul_rd(a, y.lo), __dmul_rd(a, y.hi)), fmax(__dmul_ru(a, y.lo), __dmul_ru(a, y.hi)));
+}
+template <class A>
+__device__ __forceinline__ ival pmul(double a, ival y) {
+    if constexpr (A::exact) return A::mul_point(a, y);
+    else return pmul_minmax(a, y);
+}
+
 // M = A J and g = A F(x) (linalg.py:102-129): acc = [0,0]; acc += [a,a] * B[u][j], u ascending.
 // Lane (col, half) holds J[:, col] in registers and produces rows of its half.
 template <int N, class A>
@@ -870,7 +882,7 @@ __device__ __forceinline__ void lin_products(const double* Am, const ival* jcol,
             if (i < N) {
                 ival acc = mk(0.0, 0.0);
 #pragma unroll
-                for (int u = 0; u < N; u++) acc = A::add(acc, A::mul_point(Am[i * N + u], jcol[u]));
+                for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A>(Am[i * N + u], jcol[u]));
                 W.jl[(i * N + col) * W.B + t] = acc.lo;
                 W.jh[(i * N + col) * W.B + t] = acc.hi;
             }
@@ -880,7 +892,7 @@ __device__ __forceinline__ void lin_products(const double* Am, const ival* jcol,
     if (l < N) {
 #pragma unroll
         for (int u = 0; u < N; u++)
-            acc = A::add(acc, A::mul_point(Am[l * N + u], mk(W.fl[u * W.B + t], W.fh[u * W.B + t])));
+            acc = A::add(acc, pmul<A>(Am[l * N + u], mk(W.fl[u * W.B + t], W.fh[u * W.B + t])));
     }
     __syncwarp(gmask);  // every lane has read F(x) before g overwrites it
     if (l < N) {
