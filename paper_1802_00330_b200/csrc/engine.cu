@@ -207,7 +207,7 @@ template <int N>
 struct SetupK {
     static void run(rb_handle* h) {
         const int T = h->hs_threads;
-        h->filter_smem = stab_bytes(h->meta, true) + (size_t)2 * N * h->filter_threads * sizeof(double);
+        h->filter_smem = filter_off_xs(h->meta) + (size_t)2 * N * h->filter_threads * sizeof(double);
         h->eval_smem = stab_bytes(h->meta, false) + (size_t)3 * N * T * sizeof(double);
         h->lin_smem = (size_t)(T / 32) * LinLayout<N>::BPW * LinLayout<N>::doubles * sizeof(double);
         h->sweep_smem = (size_t)2 * N * T * sizeof(double);
@@ -501,7 +501,22 @@ static void build_tables(rb_handle* h, const rb_system* sys) {
     m.off_ent_off = m.off_tbase + align8(2 * std::max(1, m.TF));
     m.off_ent = m.off_ent_off + align8(2 * (n + 1));
     m.bytes2 = m.off_ent + align8(4 * std::max(1, m.ent_total));
-    std::vector<uint8_t> buf(m.bytes2, 0);
+    m.off_termp = align16(m.bytes2);
+    m.bytes3 = m.off_termp + 16 * std::max(1, m.TF);
+    std::vector<uint8_t> buf(m.bytes3, 0);
+    for (int q = 0; q < m.TF; q++) {
+        TermP tp{};
+        tp.c = sys->coeff[q];
+        const int f0 = sys->fac_off[q], f1 = sys->fac_off[q + 1];
+        tp.nf = (uint16_t)(f1 - f0);
+        tp.packed = (f1 - f0) <= 4 ? 1 : 0;
+        for (int f = f0; f < f1 && tp.packed; f++) {
+            if (sys->fac_var[f] >= 16 || sys->fac_exp[f] < 1 || sys->fac_exp[f] > 16) tp.packed = 0;
+            else tp.fpack |= (uint32_t)(sys->fac_var[f] | ((sys->fac_exp[f] - 1) << 4)) << (8 * (f - f0));
+        }
+        if (!tp.packed) tp.fpack = 0;
+        std::memcpy(buf.data() + m.off_termp + 16 * q, &tp, sizeof(TermP));
+    }
     std::memcpy(buf.data() + m.off_tbase, tbase.data(), 2 * (size_t)std::max(1, m.TF));
     std::memcpy(buf.data() + m.off_ent_off, ent_off.data(), 2 * (size_t)(n + 1));
     if (!ent.empty()) std::memcpy(buf.data() + m.off_ent, ent.data(), 4 * ent.size());
@@ -560,8 +575,8 @@ static void build_tables(rb_handle* h, const rb_system* sys) {
     m.ops_hs_pre = ops_j + 2 * n * n + ops_gj + 2 * n + ops_f + 4 * n * n + 4 * n * n * n;
     m.ops_hs_row = 6 * (n - 1) + 8;
     h->meta = m;
-    dalloc(&h->d_tab, (size_t)m.bytes2);
-    ck(cudaMemcpyAsync(h->d_tab, buf.data(), m.bytes2, cudaMemcpyHostToDevice, h->st), "tables h2d");
+    dalloc(&h->d_tab, (size_t)m.bytes3);
+    ck(cudaMemcpyAsync(h->d_tab, buf.data(), m.bytes3, cudaMemcpyHostToDevice, h->st), "tables h2d");
     ck(cudaStreamSynchronize(h->st), "tables sync");
     h->init_lo.assign(sys->init_lo, sys->init_lo + n);
     h->init_hi.assign(sys->init_hi, sys->init_hi + n);

@@ -41,6 +41,16 @@ struct TabMeta {
     int e_max;                      // max table entries of one equation (per parent)
     int ent_total;                  // total (term, combo) entries over the equations
     int off_tbase, off_ent_off, off_ent, bytes2;  // byte offsets (tbase u16[TF], ent_off u16[n+1], ent u32[])
+    int off_termp, bytes3;          // packed F terms (TermP[TF]) for the direct filter
+};
+
+// One F term packed for the direct filter: up to 4 factors of (var < 16,
+// exponent 1..16) in one word, so a term costs a single 16-byte shared load.
+struct __align__(16) TermP {
+    double c;
+    uint32_t fpack;   // factor f: bits 8f..8f+3 var, 8f+4..8f+7 exponent - 1
+    uint16_t nf;      // number of factors
+    uint16_t packed;  // 1: fpack holds every factor; 0: use the general tables
 };
 
 struct STab {
@@ -51,6 +61,7 @@ struct STab {
 };
 
 __host__ __device__ inline int align8(int x) { return (x + 7) & ~7; }
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
 // bytes of the shared-memory copy (F only when f_only)
 __host__ __device__ inline int stab_bytes(const TabMeta& m, bool f_only) {
@@ -379,17 +390,62 @@ struct SBuf {  // survivor buffer (HS input), SoA
     int64_t cap;
 };
 
+// Polynomial.eval_interval (poly.py:187-203) over packed terms; x component j is
+// xs2[j * stride] = (lo, hi).  Same operation order as eval_poly.
+template <class A>
+__device__ __forceinline__ ival eval_poly_packed(const TermP* tp, const STab& t, int p, const double2* xs2,
+                                                 int stride) {
+    ival acc = mk(0.0, 0.0);
+    const int t0 = t.poly_off[p], t1 = t.poly_off[p + 1];
+    for (int q = t0; q < t1; ++q) {
+        const TermP T = tp[q];
+        ival term;
+        if (T.nf == 0) {
+            term = mk(T.c, T.c);
+        } else if (T.packed) {
+            uint32_t f = T.fpack;
+            double2 x = xs2[(f & 15u) * stride];
+            term = A::mul_point(T.c, A::pow(mk(x.x, x.y), (int)((f >> 4) & 15u) + 1));
+            for (int k = 1; k < T.nf; k++) {
+                f >>= 8;
+                x = xs2[(f & 15u) * stride];
+                term = A::mul(term, A::pow(mk(x.x, x.y), (int)((f >> 4) & 15u) + 1));
+            }
+        } else {
+            const int f0 = t.fac_off[q], f1 = t.fac_off[q + 1];
+            term = mk(T.c, T.c);
+            for (int f = f0; f < f1; ++f) {
+                const uint32_t fv = t.fac[f];
+                const double2 x = xs2[(fv & 0xff) * stride];
+                const ival pw = A::pow(mk(x.x, x.y), (int)(fv >> 8));
+                term = (f == f0) ? A::mul_point(T.c, pw) : A::mul(term, pw);
+            }
+        }
+        acc = A::add(acc, term);
+    }
+    return acc;
+}
+
+__device__ __noinline__ ival eval_poly_packed_exact(const TermP* tp, const STab& t, int p, const double2* xs2,
+                                                    int stride) {
+    return eval_poly_packed<Exact>(tp, t, p, xs2, stride);
+}
+
 template <int N, class A>
-__device__ __forceinline__ bool feasible(const TabMeta& meta, const STab& t, const double* xlo,
-                                         const double* xhi, int stride, unsigned& ops) {
+__device__ __forceinline__ bool feasible(const TabMeta& meta, const TermP* tp, const STab& t, const double2* xs2,
+                                         int stride, unsigned& ops) {
 #pragma unroll 1
     for (int e = 0; e < N; e++) {
-        const ival v = A::exact ? eval_poly_exact(t, e, xlo, xhi, stride) : eval_poly<A>(t, e, xlo, xhi, stride);
+        const ival v = A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride)
+                                : eval_poly_packed<A>(tp, t, e, xs2, stride);
         ops += meta.ops_eq[e];
         if (!(v.lo <= 0.0 && 0.0 <= v.hi)) return false;  // bnb.py:149-154 short-circuit
     }
     return true;
 }
+
+__host__ __device__ inline int filter_off_termp(const TabMeta& m) { return align16(stab_bytes(m, true)); }
+__host__ __device__ inline int filter_off_xs(const TabMeta& m) { return filter_off_termp(m) + 16 * m.TF; }
 
 // One thread per child.  Child c of parent p takes the low half of component j
 // iff bit (n-1-j) of c is 0 (_batch.py:226-238).  Survivors are compacted by
@@ -401,10 +457,13 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
                                                 int64_t* tags) {
     extern __shared__ __align__(16) uint8_t smem[];
     const STab tab = load_stab(meta, gtab, smem, true);
-    double* xs = reinterpret_cast<double*>(smem + stab_bytes(meta, true));
-    double* xlo = xs + threadIdx.x;
-    double* xhi = xs + N * blockDim.x + threadIdx.x;
+    TermP* tp = reinterpret_cast<TermP*>(smem + filter_off_termp(meta));
+    {
+        const TermP* g = reinterpret_cast<const TermP*>(gtab + meta.off_termp);
+        for (int i = threadIdx.x; i < meta.TF; i += blockDim.x) tp[i] = g[i];
+    }
     const int stride = blockDim.x;
+    double2* xs2 = reinterpret_cast<double2*>(smem + filter_off_xs(meta)) + threadIdx.x;
     __syncthreads();
     const unsigned long long total = ctr->n_par << N;
     const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
@@ -426,14 +485,13 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
                 const double m = mid_of(lo, hi);
                 const bool up = (c >> (N - 1 - j)) & 1u;
                 const double cl = up ? m : lo, ch = up ? hi : m;
-                xlo[j * stride] = cl;
-                xhi[j * stride] = ch;
+                xs2[j * stride] = make_double2(cl, ch);
                 const double d = __dsub_rn(ch, cl);
                 w = j == 0 ? d : (d > w ? d : w);
             }
-            if (!exact) keep = feasible<N, Fast>(meta, tab, xlo, xhi, stride, ops);
+            if (!exact) keep = feasible<N, Fast>(meta, tp, tab, xs2, stride, ops);
             else {
-                keep = feasible<N, Exact>(meta, tab, xlo, xhi, stride, ops);
+                keep = feasible<N, Exact>(meta, tp, tab, xs2, stride, ops);
                 exact_acc++;
             }
             ops_acc += ops;
@@ -442,8 +500,9 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
         if (keep && slot < (unsigned long long)S.cap) {
 #pragma unroll
             for (int j = 0; j < N; j++) {
-                S.lo[j * S.cap + slot] = xlo[j * stride];
-                S.hi[j * S.cap + slot] = xhi[j * stride];
+                const double2 x = xs2[j * stride];
+                S.lo[j * S.cap + slot] = x.x;
+                S.hi[j * S.cap + slot] = x.y;
             }
             if (tags) tags[slot] = (int64_t)idx;
         }
@@ -480,8 +539,6 @@ struct FtabShape {
 __host__ __device__ inline int ftab_meta_bytes(const TabMeta& m) {
     return align8(2 * m.TF) + align8(2 * (m.n + 1)) + align8(4 * m.ent_total);
 }
-
-__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
 // dynamic shared memory layout of k_filter_tab
 template <int N>
