@@ -123,6 +123,9 @@ struct rb_handle {
     std::vector<uint8_t> hr_cert, hr_uns;
     bool have_result = false;
     std::vector<rb_round_stats> stats;
+    // adaptive filter equation order (device copy; host mirror for host-driven rounds)
+    int* d_order = nullptr;
+    int h_order[16] = {};
     // device-resident round loop (CUDA graph with a WHILE node)
     bool use_graph = true;
     DevState* d_state = nullptr;
@@ -203,6 +206,15 @@ static int grid_for(int64_t work, int threads, int max_blocks) {
     return (int)b;
 }
 
+// dynamic shared memory limit = opt-in maximum minus the kernel's static shared memory
+template <typename K>
+static void set_max_dyn_smem(K kernel, int optin) {
+    cudaFuncAttributes fa;
+    ck(cudaFuncGetAttributes(&fa, kernel), "func attrs");
+    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes),
+       "attr");
+}
+
 template <int N>
 struct SetupK {
     static void run(rb_handle* h) {
@@ -218,11 +230,11 @@ struct SetupK {
         // the attribute is per kernel (shared by every handle of this n): set it to the opt-in maximum
         const size_t mx = std::max({h->filter_smem, h->eval_smem, h->lin_smem, h->sweep_smem});
         if ((int)mx > h->smem_optin) throw ArgError{RB_ERR_LIMIT, "system tables exceed the shared-memory budget"};
-        ck(cudaFuncSetAttribute(k_filter<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr");
-        ck(cudaFuncSetAttribute(k_filter_tab<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr");
-        ck(cudaFuncSetAttribute(k_hs_eval<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr");
-        ck(cudaFuncSetAttribute(k_hs_lin<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr");
-        ck(cudaFuncSetAttribute(k_hs_sweep<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_optin), "attr");
+        set_max_dyn_smem(k_filter<N>, h->smem_optin);
+        set_max_dyn_smem(k_filter_tab<N>, h->smem_optin);
+        set_max_dyn_smem(k_hs_eval<N>, h->smem_optin);
+        set_max_dyn_smem(k_hs_lin<N>, h->smem_optin);
+        set_max_dyn_smem(k_hs_sweep<N>, h->smem_optin);
         int nb = 0;
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter<N>, h->filter_threads, h->filter_smem), "occ");
         h->filter_blocks_per_sm = std::max(1, nb);
@@ -269,7 +281,7 @@ struct FilterK {
             const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)h->sms * h->ftab_blocks_per_sm));
             h->launches++;
             k_filter_tab<N><<<blocks, 256, h->ftab_smem, h->st>>>(h->meta, h->d_tab, h->F[h->cur].f, h->parents,
-                                                                 h->d_ctr, h->S, tags);
+                                                                 h->d_ctr, h->S, tags, h->d_order);
             ck(cudaGetLastError(), "filter_tab launch");
             return;
         }
@@ -277,7 +289,7 @@ struct FilterK {
         const int blocks = grid_for(work, h->filter_threads, h->sms * h->filter_blocks_per_sm);
         h->launches++;
         k_filter<N><<<blocks, h->filter_threads, h->filter_smem, h->st>>>(h->meta, h->d_tab, h->F[h->cur].f,
-                                                                         h->parents, h->d_ctr, h->S, tags);
+                                                                         h->parents, h->d_ctr, h->S, tags, h->d_order);
         ck(cudaGetLastError(), "filter launch");
     }
 };
@@ -431,6 +443,18 @@ static void sync_counters(rb_handle* h) {
     ck(cudaStreamSynchronize(h->st), "ctr sync");
 }
 
+static void reset_order(rb_handle* h) {
+    for (int k = 0; k < 16; k++) h->h_order[k] = k;  // reference order to start
+    ck(cudaMemcpyAsync(h->d_order, h->h_order, sizeof(h->h_order), cudaMemcpyHostToDevice, h->st), "order h2d");
+    ck(cudaStreamSynchronize(h->st), "order sync");
+}
+
+// host-driven rounds: next round's filter order from this round's counts
+static void update_order(rb_handle* h) {
+    filter_order(h->h_ctr->f_eval, h->h_ctr->f_rej, h->meta.cost_eq, h->n, h->h_order);
+    ck(cudaMemcpyAsync(h->d_order, h->h_order, sizeof(h->h_order), cudaMemcpyHostToDevice, h->st), "order h2d");
+}
+
 static double bits_to_double(unsigned long long b) {
     double d;
     std::memcpy(&d, &b, 8);
@@ -565,9 +589,17 @@ static void build_tables(rb_handle* h, const rb_system* sys) {
     group(0, n, m.f_ecmin, m.f_ecmax, m.f_deg, ops_f);
     group(n, P, m.j_ecmin, m.j_ecmax, m.j_deg, ops_j);
     for (int e = 0; e < n; e++) {
-        int ops = 0;
-        for (int q = sys->poly_off[e]; q < sys->poly_off[e + 1]; q++) ops += term_ops(q);
+        int ops = 0, cost = 0;
+        for (int q = sys->poly_off[e]; q < sys->poly_off[e + 1]; q++) {
+            ops += term_ops(q);
+            // instruction-cost model of one term in k_filter: point x interval product,
+            // full interval products, power chains, the accumulate
+            const int nf = sys->fac_off[q + 1] - sys->fac_off[q];
+            cost += 4 + (nf >= 1 ? 8 : 0) + 20 * std::max(0, nf - 1);
+            for (int f = sys->fac_off[q]; f < sys->fac_off[q + 1]; f++) cost += 6 * (sys->fac_exp[f] - 1);
+        }
         m.ops_eq[e] = ops;
+        m.cost_eq[e] = std::max(1, cost);
     }
     int ops_gj = 0;
     for (int k = 0; k < n; k++) ops_gj += (2 * n - k) + 1 + 2 * (n - 1) * (2 * n - k);
@@ -736,6 +768,7 @@ static void run_round(rb_handle* h, double target, const HsParams& prm, bool ded
             continue;
         }
         fill_round_out(h, ro);
+        update_order(h);
         ro.attempts = attempt;
         ro.classify_ms = elapsed(h, 0, 1);
         ro.filter_ms = elapsed(h, 1, 2);
@@ -765,6 +798,7 @@ static void release_all(rb_handle* h) {
     fr(h->d_dead);
     fr(h->d_slot);
     fr(h->d_rstats);
+    fr(h->d_order);
     fr(h->d_state);
     fr(h->d_cub);
     fr(h->d_keys[0]);
@@ -937,7 +971,7 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     if (dedup) dispatch_n<DedupK>(n, h, h->F[1].f, h->F[0].f);
     dispatch_n<SettleK>(n, h, std::min<int64_t>(fcap, 3 * scap));
     h->launches++;
-    k_round_end<<<1, 32, 0, h->st>>>(h->d_state, h->d_ctr, h->d_rstats, n, scap, hw);
+    k_round_end<<<1, 32, 0, h->st>>>(h->d_state, h->d_ctr, h->d_rstats, n, scap, hw, h->d_order, h->meta);
     h->launches++;
     cudaGraph_t captured = nullptr;
     ck(cudaStreamEndCapture(h->st, &captured), "end capture");
@@ -1028,6 +1062,7 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     }
     h->cur = 0;
     h->n_cur = (int64_t)r.n_cur;
+    ck(cudaMemcpy(h->h_order, h->d_order, sizeof(h->h_order), cudaMemcpyDeviceToHost), "order d2h");
     if (r.done) *status = r.status;
     return r.done != 0;
 }
@@ -1036,6 +1071,7 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
     const int n = h->n;
     const double t_start = now_s();
     h->launches = 0;
+    reset_order(h);
     ck(cudaEventRecord(h->ev[5], h->st), "ev start");
     h->stats.clear();
     h->have_result = false;
@@ -1241,6 +1277,8 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
         h->mem_budget = (size_t)(0.80 * (double)free_b);
         dalloc(&h->d_ctr, 1);
+        dalloc(&h->d_order, 16);
+        reset_order(h);
         ck(cudaMallocHost((void**)&h->h_ctr, sizeof(Counters)), "pinned ctr");
         ck(cudaMallocHost((void**)&h->h_state, sizeof(DevState)), "pinned state");
         dispatch_n<SetupK>(h->n, h);
@@ -1470,6 +1508,7 @@ int rb_round_filter(rb_handle* h, int32_t round_no, int64_t* carried, int64_t* s
         }
         h->shard_round = round_no;
         h->shard_need_f = need_f;
+        update_order(h);
         const Counters& c = *h->h_ctr;
         if (carried) *carried = (int64_t)c.n_carried;
         if (survivors) *survivors = (int64_t)c.n_surv;

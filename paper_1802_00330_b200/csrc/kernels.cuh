@@ -34,6 +34,7 @@ struct TabMeta {
     int f_ecmin, f_ecmax, f_deg;    // guard constants: coefficient exponent range, max degree
     int j_ecmin, j_ecmax, j_deg;
     int ops_eq[MAX_N];              // algorithmic ops per equation
+    int cost_eq[MAX_N];             // estimated instruction cost per equation (filter ordering)
     int ops_hs_pre;                 // ops of HS preconditioning per box
     int ops_hs_row;                 // ops of one sweep row
     // tabulated filter (k_filter_tab): per-parent term tables
@@ -220,6 +221,11 @@ struct Counters {
     unsigned long long hs_on;
     unsigned long long n_compact;
     unsigned long long pad[3];
+    // per-equation filter statistics (evaluations, rejections): the next round
+    // evaluates the equations in descending rejections-per-op order.  Any order
+    // gives the same survivor set -- a child is kept iff every equation encloses 0.
+    unsigned long long f_eval[16];
+    unsigned long long f_rej[16];
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -433,15 +439,44 @@ __device__ __noinline__ ival eval_poly_packed_exact(const TermP* tp, const STab&
 
 template <int N, class A>
 __device__ __forceinline__ bool feasible(const TabMeta& meta, const TermP* tp, const STab& t, const double2* xs2,
-                                         int stride, unsigned& ops) {
+                                         int stride, const int* order, unsigned* s_eval, unsigned* s_rej,
+                                         bool sample, unsigned& ops) {
+    if (!sample) {  // plain short-circuit (bnb.py:149-154) in the adaptive order
 #pragma unroll 1
-    for (int e = 0; e < N; e++) {
-        const ival v = A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride)
-                                : eval_poly_packed<A>(tp, t, e, xs2, stride);
-        ops += meta.ops_eq[e];
-        if (!(v.lo <= 0.0 && 0.0 <= v.hi)) return false;  // bnb.py:149-154 short-circuit
+        for (int k = 0; k < N; k++) {
+            const int e = order[k];
+            const ival v = A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride)
+                                    : eval_poly_packed<A>(tp, t, e, xs2, stride);
+            ops += meta.ops_eq[e];
+            if (!(v.lo <= 0.0 && 0.0 <= v.hi)) return false;
+        }
+        return true;
     }
-    return true;
+    // sampled blocks also count evaluations / rejections per equation
+    const unsigned m = __activemask();
+    const int leader = __ffs(m) - 1;
+    const int lane = threadIdx.x & 31;
+    bool alive = true;
+#pragma unroll 1
+    for (int k = 0; k < N; k++) {
+        const unsigned live = __ballot_sync(m, alive);
+        if (live == 0) break;
+        const int e = order[k];
+        bool rej = false;
+        if (alive) {
+            const ival v = A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride)
+                                    : eval_poly_packed<A>(tp, t, e, xs2, stride);
+            ops += meta.ops_eq[e];
+            rej = !(v.lo <= 0.0 && 0.0 <= v.hi);
+        }
+        const unsigned rm = __ballot_sync(m, rej);
+        if (lane == leader) {
+            atomicAdd(&s_eval[e], (unsigned)__popc(live));
+            if (rm) atomicAdd(&s_rej[e], (unsigned)__popc(rm));
+        }
+        if (rej) alive = false;
+    }
+    return alive;
 }
 
 __host__ __device__ inline int filter_off_termp(const TabMeta& m) { return align16(stab_bytes(m, true)); }
@@ -454,8 +489,15 @@ __host__ __device__ inline int filter_off_xs(const TabMeta& m) { return filter_o
 template <int N>
 __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                 const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
-                                                int64_t* tags) {
+                                                int64_t* tags, const int* __restrict__ eq_order) {
     extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int s_order[16];
+    __shared__ unsigned s_eval[16], s_rej[16];
+    if (threadIdx.x < 16) {
+        s_order[threadIdx.x] = (eq_order && threadIdx.x < N) ? eq_order[threadIdx.x] : (int)threadIdx.x;
+        s_eval[threadIdx.x] = 0;
+        s_rej[threadIdx.x] = 0;
+    }
     const STab tab = load_stab(meta, gtab, smem, true);
     TermP* tp = reinterpret_cast<TermP*>(smem + filter_off_termp(meta));
     {
@@ -489,9 +531,10 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
                 const double d = __dsub_rn(ch, cl);
                 w = j == 0 ? d : (d > w ? d : w);
             }
-            if (!exact) keep = feasible<N, Fast>(meta, tp, tab, xs2, stride, ops);
+            const bool sample = (blockIdx.x & 3) == 0;  // statistics from a quarter of the blocks
+            if (!exact) keep = feasible<N, Fast>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
             else {
-                keep = feasible<N, Exact>(meta, tp, tab, xs2, stride, ops);
+                keep = feasible<N, Exact>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
                 exact_acc++;
             }
             ops_acc += ops;
@@ -516,6 +559,33 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
         if (ops_acc) atomicAdd(&ctr->filter_ops, ops_acc);
         if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
     }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        if (s_eval[threadIdx.x]) atomicAdd(&ctr->f_eval[threadIdx.x], (unsigned long long)s_eval[threadIdx.x]);
+        if (s_rej[threadIdx.x]) atomicAdd(&ctr->f_rej[threadIdx.x], (unsigned long long)s_rej[threadIdx.x]);
+    }
+}
+
+// Next round's equation order: descending rejections per algorithmic op, from
+// this round's counts (equations not evaluated keep their relative position).
+__host__ __device__ inline void filter_order(const unsigned long long* ev, const unsigned long long* rj,
+                                             const int* ops_eq, int n, int* order) {
+    double key[16];
+    for (int e = 0; e < n; e++)
+        key[e] = ev[e] ? ((double)rj[e] / (double)ev[e]) / (double)(ops_eq[e] > 0 ? ops_eq[e] : 1) : -1.0;
+    int cur[16];
+    for (int k = 0; k < n; k++) cur[k] = order[k];
+    // stable insertion sort of the current order by key (unknown keys stay in place relative to each other)
+    for (int a = 1; a < n; a++) {
+        const int e = cur[a];
+        int b = a - 1;
+        while (b >= 0 && key[cur[b]] < key[e] && key[e] >= 0.0) {
+            cur[b + 1] = cur[b];
+            b--;
+        }
+        cur[b + 1] = e;
+    }
+    for (int k = 0; k < n; k++) order[k] = cur[k];
 }
 
 // ------------------------------------------------------------------ K1' tabulated filter
@@ -581,8 +651,15 @@ __device__ __noinline__ ival term_value_exact(const STab& t, int q, int combo, c
 template <int N>
 __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                     const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
-                                                    int64_t* tags) {
+                                                    int64_t* tags, const int* __restrict__ eq_order) {
     using Sh = FtabShape<N>;
+    __shared__ int s_order[16];
+    __shared__ unsigned s_eval[16], s_rej[16];
+    if (threadIdx.x < 16) {
+        s_order[threadIdx.x] = (eq_order && threadIdx.x < N) ? eq_order[threadIdx.x] : (int)threadIdx.x;
+        s_eval[threadIdx.x] = 0;
+        s_rej[threadIdx.x] = 0;
+    }
     extern __shared__ __align__(16) uint8_t smem[];
     const STab tab = load_stab(meta, gtab, smem, true);
     uint8_t* p8 = smem + stab_bytes(meta, true);
@@ -641,8 +718,11 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
         bool alive = valid;
         unsigned ops = 0;
 #pragma unroll 1
-        for (int e = 0; e < N; e++) {
-            if (!__syncthreads_or(alive)) break;  // also: everyone is done with the previous tables
+        for (int k = 0; k < N; k++) {
+            const int e = s_order[k];
+            const int n_alive = __syncthreads_count(alive);  // also: everyone is done with the previous tables
+            if (n_alive == 0) break;
+            if (tid == 0) atomicAdd(&s_eval[e], (unsigned)n_alive);
             const int e0 = ent_off[e], E = ent_off[e + 1] - e0;
             for (int k = tid; k < Sh::PPB * E; k += blockDim.x) {
                 const int l2 = k / E, i = k % E;
@@ -669,6 +749,7 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
                 }
                 ops += meta.ops_eq[e];
                 alive = acc.lo <= 0.0 && 0.0 <= acc.hi;
+                if (!alive) atomicAdd(&s_rej[e], 1u);
             }
         }
         ops_acc += ops;
@@ -701,6 +782,11 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
     if (lane == 0) {
         if (ops_acc) atomicAdd(&ctr->filter_ops, ops_acc);
         if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        if (s_eval[threadIdx.x]) atomicAdd(&ctr->f_eval[threadIdx.x], (unsigned long long)s_eval[threadIdx.x]);
+        if (s_rej[threadIdx.x]) atomicAdd(&ctr->f_rej[threadIdx.x], (unsigned long long)s_rej[threadIdx.x]);
     }
 }
 
@@ -1411,9 +1497,10 @@ __global__ void k_settle(Front f1, Front f0, const Counters* ctr) {
 // Round statistics, termination (bnb.py:339-352) and the WHILE condition of the
 // device round loop; also clears the counters for the next round.
 __global__ void k_round_end(DevState* st, Counters* ctr, DevRoundStats* stats, int n, int64_t s_cap,
-                            cudaGraphConditionalHandle h_while) {
+                            cudaGraphConditionalHandle h_while, int* eq_order, TabMeta meta) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const Counters c = *ctr;
+    filter_order(c.f_eval, c.f_rej, meta.cost_eq, n, eq_order);
     const unsigned long long after = c.n_next - c.dups;
     const double width = after ? __longlong_as_double((long long)c.wmax) : 0.0;
     const unsigned long long now = gtimer();
