@@ -207,6 +207,19 @@ int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const 
  *                 0: host-driven rounds (per-kernel CUDA-event timings in the stats). */
 int rb_set_option(rb_handle* h, const char* key, int64_t value);
 
+/* ---- post-processing -----------------------------------
+ * Backtracking merge of a solve result: snap_to_grid of every box, then
+ * merge_to_width (rootbox/backtrack.py:118-242), in exact integer arithmetic on
+ * the host.  lo/hi [N x n] row-major, cert [N]; stop_width < 0 or NaN = None.
+ * Outputs the merged boxes in canonical order (out_lo/out_hi [M x n], out_cert
+ * [M]) and the merge levels (levels [K x 2] = (width, count)); *M and *K get
+ * the true sizes even when they exceed cap / cap_levels.  Errors (the
+ * reference's NotOnGrid) return RB_ERR_ARG with the message in err. */
+int rb_merge(int n, const double* init_lo, const double* init_hi, const double* lo, const double* hi,
+             const uint8_t* cert, int64_t N, double stop_width, int stop_on_plateau, double* out_lo,
+             double* out_hi, uint8_t* out_cert, int64_t cap, int64_t* M, double* levels, int64_t cap_levels,
+             int64_t* K, char* err, int64_t err_len);
+
 /* ---- measurement utility ----------------------------------------------------
  * Measured throughput of the FP64 pipe on `device` for the directed-rounding
  * instructions the engine issues (DMUL.RM/RP, DADD.RM/RP; one op each), in

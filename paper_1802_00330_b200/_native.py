@@ -109,6 +109,9 @@ def lib():
     L.rb_shard_export_device.restype = i32
     L.rb_shard_import_device.argtypes = [P, i64, P, P, P, P, i64]
     L.rb_shard_import_device.restype = i32
+    L.rb_merge.argtypes = [i32, P, P, P, P, P, i64, C.c_double, i32, P, P, P, i64, C.POINTER(i64), P, i64,
+                           C.POINTER(i64), C.c_char_p, i64]
+    L.rb_merge.restype = i32
     L.rb_set_option.argtypes = [P, C.c_char_p, i64]
     L.rb_set_option.restype = i32
     L.rb_fp64_peak.argtypes = [i32, C.POINTER(C.c_double)]
@@ -120,7 +123,8 @@ def lib():
 EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch", "rb_filter", "rb_hs",
             "rb_last_error", "rb_destroy", "rb_shard_load", "rb_round_filter", "rb_round_hs",
             "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak", "rb_set_option",
-            "rb_shard_partition", "rb_shard_dedup", "rb_shard_export_device", "rb_shard_import_device"]
+            "rb_shard_partition", "rb_shard_dedup", "rb_shard_export_device", "rb_shard_import_device",
+            "rb_merge"]
 
 
 def _p(a):

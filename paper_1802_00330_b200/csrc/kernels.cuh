@@ -1139,7 +1139,9 @@ __global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_
                         for (int i = 0; i < N; i++) {
                             if (i == k) continue;
                             const double f = sCol[i == pr ? k : i];  // column k after the row swap
-                            if (f != 0.0) c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
+                            // the reference skips f == 0 (linalg.py:168); c - 0*c[k] == c for the finite
+                            // values here (only a zero's sign could differ), so no test is needed
+                            c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
                         }
                     }
                 }

@@ -1,0 +1,139 @@
+"""Solve + backtracking merge + report: the native counterpart of
+``rootbox.cli.run_pipeline`` (cli.py:172-205).
+
+The merge (snap_to_grid + merge_to_width, backtrack.py:118-242) runs in exact
+integer arithmetic in librootbox_b200.so (``rb_merge``); the report has the
+reference's JSON / CSV / text formats (cli.py:42-123).  When the reference
+package is importable and the system is a reference ``PolySystem``, the
+reference's own ``RunReport`` class is returned.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import __version__, _native
+from .bnb import BUDGET_EXHAUSTED, Box, Interval, RootBox, SolverConfig, _reference_types, solve
+from .system import as_spec
+
+SCHEMA_VERSION = 1
+
+
+def merge_arrays(init_lo, init_hi, lo, hi, cert, stop_width=None, stop_on_plateau=True):
+    """rb_merge: merged boxes (canonical order), certified flags and the merge
+    levels [(width, count), ...] of merge_to_width(snap_to_grid(boxes))."""
+    L = _native.lib()
+    ilo = np.ascontiguousarray(init_lo, np.float64)
+    ihi = np.ascontiguousarray(init_hi, np.float64)
+    n = ilo.size
+    lo = np.ascontiguousarray(lo, np.float64).reshape(-1, n)
+    hi = np.ascontiguousarray(hi, np.float64).reshape(-1, n)
+    c = np.ascontiguousarray(cert, np.uint8).reshape(-1)
+    N = lo.shape[0]
+    cap, cap_lv = max(1, N), 64
+    err = C.create_string_buffer(512)
+    for _ in range(2):
+        olo = np.empty((cap, n)); ohi = np.empty((cap, n)); oc = np.empty(cap, np.uint8)
+        lv = np.empty((cap_lv, 2))
+        M = C.c_int64(); K = C.c_int64()
+        p = _native._p
+        rc = L.rb_merge(n, p(ilo), p(ihi), p(lo), p(hi), p(c), N,
+                        -1.0 if stop_width is None else float(stop_width), int(bool(stop_on_plateau)),
+                        p(olo), p(ohi), p(oc), cap, C.byref(M), p(lv), cap_lv, C.byref(K), err, 512)
+        if rc != 0:
+            raise ValueError(f"rb_merge: {err.value.decode()}")
+        if M.value <= cap and K.value <= cap_lv:
+            break
+        cap, cap_lv = max(cap, M.value), max(cap_lv, K.value)
+    m, k = M.value, K.value
+    levels = tuple((float(lv[i, 0]), int(lv[i, 1])) for i in range(k))
+    return olo[:m].copy(), ohi[:m].copy(), oc[:m].astype(bool), levels
+
+
+@dataclass
+class RunReport:
+    """Mirror of rootbox.cli.RunReport (cli.py:42-123), same output formats."""
+
+    system: str
+    config: dict
+    status: str
+    result: object
+    roots: tuple
+    merge_levels: tuple
+    wall_seconds: float
+
+    def to_json_dict(self) -> dict:
+        return {
+            "schema_version": SCHEMA_VERSION,
+            "solver_version": "0.1.0",  # the reference's version: the report format is its
+            "system": self.system,
+            "config": self.config,
+            "status": self.status,
+            "rounds": [{"round": st.round, "boxes_in": st.boxes_in, "boxes_after_filter": st.boxes_after_filter,
+                        "boxes_after_hs": st.boxes_after_hs, "width": st.width,
+                        "elapsed_seconds": st.elapsed_seconds} for st in self.result.stats],
+            "roots": [{"intervals": [[iv.lo, iv.hi] for iv in rb.box], "certified": rb.certified}
+                      for rb in self.roots],
+            "merge_levels": [{"width": w, "count": c} for w, c in self.merge_levels],
+            "wall_seconds": self.wall_seconds,
+        }
+
+    def to_json(self) -> str:
+        return json.dumps(self.to_json_dict(), indent=2)
+
+    def to_csv(self, var_names) -> str:
+        header = []
+        for nm in var_names:
+            header += [f"{nm}_lo", f"{nm}_hi"]
+        header.append("certified")
+        lines = [",".join(header)]
+        for rb in self.roots:
+            row = []
+            for iv in rb.box:
+                row += [repr(iv.lo), repr(iv.hi)]
+            row.append("true" if rb.certified else "false")
+            lines.append(",".join(row))
+        return "\n".join(lines) + "\n"
+
+
+def config_echo(cfg, merge: bool) -> dict:
+    """cli._config_echo (cli.py:156-169)."""
+    return {"target_width": cfg.target_width, "hs_enable_round": cfg.hs_enable_round,
+            "hs_enable_width": cfg.hs_enable_width, "max_rounds": cfg.max_rounds, "max_boxes": cfg.max_boxes,
+            "max_seconds": cfg.max_seconds, "worker_count": cfg.worker_count, "batch_size": cfg.batch_size,
+            "hs_contract": cfg.hs_contract, "engine": cfg.engine, "backtrack": merge}
+
+
+def run_pipeline(s, cfg=None, merge: bool = True, merge_width=None):
+    """solve + grid normalisation + backtracking merge, as one report (cli.py:172-205)."""
+    cfg = cfg or SolverConfig()
+    t0 = time.perf_counter()
+    result = solve(s, cfg)
+    spec = as_spec(s)
+    types = _reference_types(s)
+    if types is None:
+        RB, BX, IV, Report = RootBox, Box, Interval, RunReport
+    else:
+        from rootbox import cli as rcli  # type: ignore
+        _, RB, _, BX, IV = types
+        Report = rcli.RunReport
+    if result.status == BUDGET_EXHAUSTED or not merge:
+        roots, levels = result.boxes, ()
+    elif not result.boxes:
+        roots, levels = (), ()
+    else:
+        n = spec.n
+        lo = np.array([[iv.lo for iv in rb.box] for rb in result.boxes]).reshape(-1, n)
+        hi = np.array([[iv.hi for iv in rb.box] for rb in result.boxes]).reshape(-1, n)
+        cert = np.array([rb.certified for rb in result.boxes], bool)
+        mlo, mhi, mc, levels = merge_arrays(spec.init_lo, spec.init_hi, lo, hi, cert, stop_width=merge_width)
+        roots = tuple(RB(BX(tuple(IV(a, b) for a, b in zip(mlo[r].tolist(), mhi[r].tolist()))), bool(mc[r]))
+                      for r in range(mlo.shape[0]))
+    wall = time.perf_counter() - t0
+    return Report(system=getattr(s, "name", "") or spec.name or "?", config=config_echo(cfg, merge),
+                  status=result.status, result=result, roots=roots, merge_levels=levels, wall_seconds=wall)

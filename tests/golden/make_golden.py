@@ -517,6 +517,74 @@ def part_solve(which):
             print(f"solve {cname}: {status} boxes={N} wall={wall:.1f}s", flush=True)
 
 
+# ---------------------------------------------------------------- merge (backtrack.py)
+
+
+def _merge_case(init_lo, init_hi, lo, hi, cert, stop_width):
+    from rootbox import backtrack
+    g = backtrack.GridContext.from_box(poly.Box.from_bounds(init_lo, init_hi))
+    try:
+        snapped = [backtrack.snap_to_grid(poly.Box.from_bounds(lo[r], hi[r]), g) for r in range(lo.shape[0])]
+        m = backtrack.merge_to_width(snapped, g, stop_width=stop_width, certified=list(cert))
+    except ValueError as exc:
+        return {"error": type(exc).__name__}
+    return {"levels": [[w.hex(), c] for w, c in m.levels],
+            "lo": [[iv.lo.hex() for iv in b] for b in m.boxes],
+            "hi": [[iv.hi.hex() for iv in b] for b in m.boxes],
+            "cert": [int(f) for f in m.certified]}
+
+
+def part_merge():
+    rng = np.random.default_rng(17)
+    cases = []
+    # solve outputs (the pipeline's real inputs), with and without a stop width
+    for fn in sorted(os.listdir(HERE)):
+        if not (fn.startswith("solve_") and fn.endswith(".json")):
+            continue
+        d = json.load(open(os.path.join(HERE, fn)))
+        if "lo" not in d or not d["lo"] or d["status"] == "budget_exhausted":
+            continue
+        sysd = json.load(open(os.path.join(HERE, "systems.json")))["systems"][d["system"]]
+        ilo = np.array([float.fromhex(v) for v in sysd["init_lo"]]); ihi = np.array([float.fromhex(v) for v in sysd["init_hi"]])
+        lo = np.array([[float.fromhex(v) for v in r] for r in d["lo"]]); hi = np.array([[float.fromhex(v) for v in r] for r in d["hi"]])
+        cert = np.array(d["cert"], bool)
+        for sw in (None, 0.01):
+            cases.append({"name": f"{d['case']}_sw{sw}", "init_lo": ilo, "init_hi": ihi, "lo": lo, "hi": hi,
+                          "cert": cert, "stop_width": sw})
+    # synthetic sets: aligned cells, contracted sub-boxes, boundary-straddling boxes, point boxes
+    for t, (L0, H0) in enumerate([(-2.0, 2.0), (-8.0, 8.0), (0.0, 1.0), (-1.0, 3.0), (-0.75, 0.25), (0.0, 3.0)]):
+        n = 3
+        ilo = np.full(n, L0); ihi = np.full(n, H0)
+        W = H0 - L0
+        m = 300
+        lev = rng.integers(3, 30, m)
+        k = (rng.random((m, n)) * (2.0 ** lev[:, None])).astype(np.int64)
+        cl = L0 + k * (W / 2.0 ** lev[:, None]); ch = L0 + (k + 1) * (W / 2.0 ** lev[:, None])
+        f = rng.random((m, 1))
+        sub_lo = cl + (ch - cl) * rng.random((m, n)) * 0.3
+        sub_hi = ch - (ch - cl) * rng.random((m, n)) * 0.3
+        straddle = rng.random(m) < 0.2
+        sub_hi[straddle] = np.minimum(ch[straddle] + (ch - cl)[straddle] * 0.5, H0)
+        pt = rng.random(m) < 0.05
+        sub_hi[pt] = sub_lo[pt]
+        lo = np.where(f < 0.5, cl, sub_lo); hi = np.where(f < 0.5, ch, sub_hi)
+        cert = rng.random(m) < 0.3
+        for sw in (None, 0.5):
+            cases.append({"name": f"synthetic{t}_sw{sw}", "init_lo": ilo, "init_hi": ihi, "lo": lo, "hi": hi,
+                          "cert": cert, "stop_width": sw})
+    out = []
+    for c in cases:
+        r = _merge_case(c["init_lo"], c["init_hi"], c["lo"], c["hi"], c["cert"], c["stop_width"])
+        out.append({"name": c["name"], "init_lo": [v.hex() for v in c["init_lo"]],
+                    "init_hi": [v.hex() for v in c["init_hi"]],
+                    "lo": [[float(v).hex() for v in r_] for r_ in c["lo"]],
+                    "hi": [[float(v).hex() for v in r_] for r_ in c["hi"]],
+                    "cert": [int(v) for v in c["cert"]], "stop_width": c["stop_width"], "result": r})
+    with open(os.path.join(HERE, "merge_cases.json"), "w") as f:
+        json.dump(out, f)
+    print(f"merge: {len(out)} cases, {sum('error' in o['result'] for o in out)} raise")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--part", nargs="*", default=["systems", "interval", "poly", "gj", "hs", "solve"])
@@ -537,6 +605,8 @@ def main():
             part_solve("fast")
         elif p == "solve_slow":
             part_solve("slow")
+        elif p == "merge":
+            part_merge()
         print(f"[{p}] {time.time() - t0:.1f}s", flush=True)
 
 

@@ -310,3 +310,23 @@ def test_shard_export_import_roundtrip(native):
     assert np.array_equal(gc[o2], c[o1].astype(bool)) and np.array_equal(gu[o2], u[o1].astype(bool))
     # device-side owner hash == host twin
     assert np.array_equal(row_owner(glo, ghi, 4), row_owner(glo, ghi, 4))
+
+
+# ------------------------------------------------------------------ pipeline (solve + native merge + report)
+
+REPORT_CASES = [c for c in solve_cases() if "report" in load_solve(c)]
+
+
+@pytest.mark.parametrize("case", REPORT_CASES)
+def test_run_pipeline_report_equals_reference(native, case):
+    """pipeline.run_pipeline JSON == the reference's cli.run_pipeline JSON
+    (cli.py:54-83), timing fields excluded."""
+    from paper_1802_00330_b200 import SolverConfig
+    from paper_1802_00330_b200.pipeline import run_pipeline
+    meta = load_solve(case)
+    spec = golden_spec(meta["system"])
+    rep = run_pipeline(spec, SolverConfig(**meta["config"])).to_json_dict()
+    for st in rep["rounds"]:
+        st["elapsed_seconds"] = 0.0
+    rep["wall_seconds"] = 0.0
+    assert rep == meta["report"], case
