@@ -10,6 +10,6 @@ __version__ = "0.1.0"
 
 from .system import SystemSpec, compile_tables, as_spec  # noqa: F401
 from .bnb import (  # noqa: F401
-    BUDGET_EXHAUSTED, NO_REAL_SOLUTION, WIDTH_REACHED, Box, Interval, RootBox, RoundStats, SolveResult,
+    BUDGET_EXHAUSTED, NO_REAL_SOLUTION, WIDTH_REACHED, Box, Interval, RootBox, RootBoxes, RoundStats, SolveResult,
     SolverConfig, solve, solve_arrays,
 )

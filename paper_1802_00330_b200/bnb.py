@@ -18,6 +18,7 @@ from __future__ import annotations
 import math
 import os
 import threading
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -25,7 +26,7 @@ import numpy as np
 from . import _native
 from .system import SystemSpec, as_spec, compile_tables
 
-__all__ = ["SolverConfig", "RoundStats", "RootBox", "SolveResult", "Interval", "Box", "solve",
+__all__ = ["SolverConfig", "RoundStats", "RootBox", "RootBoxes", "SolveResult", "Interval", "Box", "solve",
            "solve_arrays", "NO_REAL_SOLUTION", "WIDTH_REACHED", "BUDGET_EXHAUSTED"]
 
 NO_REAL_SOLUTION = "no_real_solution"
@@ -233,6 +234,56 @@ def _reference_types(s):
     return rbnb.SolveResult, rbnb.RootBox, rbnb.RoundStats, rpoly.Box, RInterval
 
 
+# Results above this many boxes come back as a lazy RootBoxes sequence.
+LAZY_THRESHOLD = 16384
+
+
+class RootBoxes(Sequence):
+    """``SolveResult.boxes`` for large results: RootBox objects are built on
+    access instead of up front (the reference materialises every box,
+    ``_to_rootboxes`` bnb.py:357-361, ~30 us each).  Indexing, slicing,
+    iteration, ``len`` and equality with a tuple behave like the tuple the
+    reference returns; ``.lo/.hi/.cert/.unsplit`` expose the arrays."""
+
+    __slots__ = ("lo", "hi", "cert", "unsplit", "_types")
+
+    def __init__(self, lo, hi, cert, unsplit, types):
+        self.lo, self.hi, self.cert, self.unsplit, self._types = lo, hi, cert, unsplit, types
+
+    def __len__(self):
+        return self.lo.shape[0]
+
+    def _make(self, r):
+        RB, BX, IV = self._types
+        return RB(BX(tuple(IV(a, b) for a, b in zip(self.lo[r].tolist(), self.hi[r].tolist()))),
+                  bool(self.cert[r]), bool(self.unsplit[r]))
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return tuple(self._make(r) for r in range(*i.indices(len(self))))
+        n = len(self)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError("RootBoxes index out of range")
+        return self._make(i)
+
+    def __iter__(self):
+        for r in range(len(self)):
+            yield self._make(r)
+
+    def __eq__(self, other):
+        if isinstance(other, RootBoxes):
+            return (np.array_equal(self.lo, other.lo) and np.array_equal(self.hi, other.hi)
+                    and np.array_equal(self.cert, other.cert) and np.array_equal(self.unsplit, other.unsplit))
+        if isinstance(other, (tuple, list)):
+            return len(other) == len(self) and all(a == b for a, b in zip(self, other))
+        return NotImplemented
+
+    def __repr__(self):
+        return f"RootBoxes({len(self)} boxes)"
+
+
 def solve(s, cfg=None) -> SolveResult:
     """Isolate all real roots of the system inside its initial box (bnb.py:224)."""
     out = solve_arrays(s, cfg)
@@ -242,9 +293,12 @@ def solve(s, cfg=None) -> SolveResult:
     else:
         SR, RB, RS, BX, IV = types
     lo, hi, cert, uns = out["lo"], out["hi"], out["cert"], out["unsplit"]
-    boxes = tuple(
-        RB(BX(tuple(IV(a, b) for a, b in zip(lo[r].tolist(), hi[r].tolist()))), bool(cert[r]), bool(uns[r]))
-        for r in range(lo.shape[0]))
+    if lo.shape[0] > LAZY_THRESHOLD:
+        boxes = RootBoxes(lo, hi, cert, uns, (RB, BX, IV))
+    else:
+        boxes = tuple(
+            RB(BX(tuple(IV(a, b) for a, b in zip(lo[r].tolist(), hi[r].tolist()))), bool(cert[r]), bool(uns[r]))
+            for r in range(lo.shape[0]))
     stats = tuple(RS(round=int(st["round"]), boxes_in=int(st["boxes_in"]),
                      boxes_after_filter=int(st["boxes_after_filter"]), boxes_after_hs=int(st["boxes_after_hs"]),
                      width=float(st["width"]), elapsed_seconds=float(st["elapsed_seconds"]))

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import __version__, _native
-from .bnb import BUDGET_EXHAUSTED, Box, Interval, RootBox, SolverConfig, _reference_types, solve
+from .bnb import BUDGET_EXHAUSTED, Box, Interval, RootBox, RootBoxes, SolverConfig, _reference_types, solve
 from .system import as_spec
 
 SCHEMA_VERSION = 1
@@ -128,9 +128,12 @@ def run_pipeline(s, cfg=None, merge: bool = True, merge_width=None):
         roots, levels = (), ()
     else:
         n = spec.n
-        lo = np.array([[iv.lo for iv in rb.box] for rb in result.boxes]).reshape(-1, n)
-        hi = np.array([[iv.hi for iv in rb.box] for rb in result.boxes]).reshape(-1, n)
-        cert = np.array([rb.certified for rb in result.boxes], bool)
+        if isinstance(result.boxes, RootBoxes):  # large result: arrays, no per-box objects
+            lo, hi, cert = result.boxes.lo, result.boxes.hi, result.boxes.cert
+        else:
+            lo = np.array([[iv.lo for iv in rb.box] for rb in result.boxes]).reshape(-1, n)
+            hi = np.array([[iv.hi for iv in rb.box] for rb in result.boxes]).reshape(-1, n)
+            cert = np.array([rb.certified for rb in result.boxes], bool)
         mlo, mhi, mc, levels = merge_arrays(spec.init_lo, spec.init_hi, lo, hi, cert, stop_width=merge_width)
         roots = tuple(RB(BX(tuple(IV(a, b) for a, b in zip(mlo[r].tolist(), mhi[r].tolist()))), bool(mc[r]))
                       for r in range(mlo.shape[0]))
