@@ -145,6 +145,13 @@ int rb_filter(rb_handle* h, const double* plo, const double* phi, int64_t P, dou
 int rb_hs(rb_handle* h, const double* lo, const double* hi, int64_t M, int contract_output,
           double* olo, double* ohi, uint8_t* cert, int64_t cap, int64_t* M2);
 
+/* hansen.krawczyk (hansen.py:141-170) on M boxes (row-major M x n): the
+ * Krawczyk operator K(X) intersected with X.  ok[r] = 0 where the reference
+ * returns None (singular midpoint Jacobian or empty intersection); those rows
+ * of olo/ohi are NaN.  Shares the HS preconditioning kernels (x, A J, A F(x)). */
+int rb_krawczyk(rb_handle* h, const double* lo, const double* hi, int64_t M, double* olo, double* ohi,
+                uint8_t* ok);
+
 /* Last error message of this handle (or of the last failed rb_create when h is NULL). */
 const char* rb_last_error(rb_handle* h);
 

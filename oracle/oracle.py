@@ -43,6 +43,7 @@ def lib():
         L.o_gj_inverse.argtypes = [C.c_int, P, P]
         L.o_gj_inverse.restype = C.c_int
         L.o_contract_vec.argtypes = [P, i64, P, P, P, P, P, P]
+        L.o_krawczyk_vec.argtypes = [P, i64, P, P, P, P, P]
         L.o_chunk_filter.argtypes = [P, i64, P, P, i64, P, P]
         L.o_chunk_filter.restype = i64
         L.o_hs_pass.argtypes = [P, i64, P, P, C.c_int, i64, P, P, P]
@@ -134,6 +135,13 @@ class OSystem:
         cert = np.empty(m, np.uint8)
         lib().o_contract_vec(self.h, m, _p(lo), _p(hi), _p(kind), _p(olo), _p(ohi), _p(cert))
         return kind, olo, ohi, cert.astype(bool)
+
+    def krawczyk(self, lo, hi):
+        lo = np.ascontiguousarray(lo, np.float64); hi = np.ascontiguousarray(hi, np.float64)
+        m = lo.shape[0]
+        ok = np.empty(m, np.uint8); olo = np.empty((m, self.n)); ohi = np.empty((m, self.n))
+        lib().o_krawczyk_vec(self.h, m, _p(lo), _p(hi), _p(ok), _p(olo), _p(ohi))
+        return ok.astype(bool), olo, ohi
 
     def chunk_filter(self, plo, phi):
         plo = np.ascontiguousarray(plo, np.float64); phi = np.ascontiguousarray(phi, np.float64)

@@ -9,6 +9,7 @@ include/rootbox_b200.h; there is no CPU fallback.
 __version__ = "0.1.0"
 
 from .system import SystemSpec, compile_tables, as_spec  # noqa: F401
+from .hansen import krawczyk, krawczyk_arrays  # noqa: F401, E402
 from .bnb import (  # noqa: F401
     BUDGET_EXHAUSTED, NO_REAL_SOLUTION, WIDTH_REACHED, Box, Interval, RootBox, RootBoxes, RoundStats, SolveResult,
     SolverConfig, solve, solve_arrays,

@@ -85,6 +85,8 @@ def lib():
     L.rb_filter.restype = i32
     L.rb_hs.argtypes = [P, P, P, i64, i32, P, P, P, i64, C.POINTER(i64)]
     L.rb_hs.restype = i32
+    L.rb_krawczyk.argtypes = [P, P, P, i64, P, P, P]
+    L.rb_krawczyk.restype = i32
     L.rb_last_error.argtypes = [P]
     L.rb_last_error.restype = C.c_char_p
     L.rb_destroy.argtypes = [P]
@@ -124,7 +126,7 @@ EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch"
             "rb_last_error", "rb_destroy", "rb_shard_load", "rb_round_filter", "rb_round_hs",
             "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak", "rb_set_option",
             "rb_shard_partition", "rb_shard_dedup", "rb_shard_export_device", "rb_shard_import_device",
-            "rb_merge"]
+            "rb_merge", "rb_krawczyk"]
 
 
 def _p(a):
@@ -215,6 +217,13 @@ class Engine:
                            C.byref(M2)), self.h, "rb_hs")
         m = M2.value
         return olo[:m].copy(), ohi[:m].copy(), oc[:m].astype(bool)
+
+    def krawczyk(self, lo, hi):
+        lo = np.ascontiguousarray(lo, np.float64); hi = np.ascontiguousarray(hi, np.float64)
+        M = lo.shape[0]
+        olo = np.empty((M, self.n)); ohi = np.empty((M, self.n)); ok = np.empty(M, np.uint8)
+        _check(lib().rb_krawczyk(self.h, _p(lo), _p(hi), M, _p(olo), _p(ohi), _p(ok)), self.h, "rb_krawczyk")
+        return ok.astype(bool), olo, ohi
 
 
 def device_count() -> int:

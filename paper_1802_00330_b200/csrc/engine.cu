@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -313,6 +314,27 @@ struct HsK {
         k_hs_sweep<N><<<grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem, h->st>>>(
             h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
         ck(cudaGetLastError(), "hs launch");
+    }
+};
+
+// K2a + K2b + Krawczyk over rows [b0, b_end) of S; results at the same rows of `out`
+template <int N>
+struct KrawczykK {
+    static void run(rb_handle* h, int64_t b0, int64_t b_end, Front out, uint8_t* ok) {
+        const int T = h->hs_threads;
+        const int64_t B = h->W.B;
+        HsParams prm{};
+        prm.hs_mode = 1;
+        h->launches += 3;
+        const int64_t bound = b_end - b0;
+        const int64_t target = (int64_t)h->sms * 1024;
+        const int R = (int)std::max<int64_t>(1, std::min<int64_t>(N * N + N, (target + bound - 1) / bound));
+        k_hs_eval<N><<<grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem, h->st>>>(
+            h->meta, h->d_tab, h->S, b_end, b0, prm, h->W, out, h->d_ctr, nullptr, R);
+        k_hs_lin<N><<<grid_for(std::min(B, bound), (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T,
+                      h->lin_smem, h->st>>>(h->S, b_end, b0, prm, h->W, h->d_ctr);
+        k_krawczyk<N><<<grid_for(bound, 128, h->sms * 16), 128, 0, h->st>>>(h->S, b_end, b0, h->W, out, ok);
+        ck(cudaGetLastError(), "krawczyk launch");
     }
 };
 
@@ -1445,6 +1467,48 @@ int rb_hs(rb_handle* h, const double* lo, const double* hi, int64_t M, int contr
             }
             if (cert) cert[r] = c[order[r]];
         }
+    })
+}
+
+int rb_krawczyk(rb_handle* h, const double* lo, const double* hi, int64_t M, double* olo, double* ohi,
+                uint8_t* ok) {
+    if (!h || M < 0 || (M > 0 && (!lo || !hi || !olo || !ohi || !ok))) return RB_ERR_ARG;
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->have_result = false;
+    RB_GUARD(h, {
+        ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        PoolScope ps(h);
+        const int n = h->n;
+        if (M == 0) return RB_OK;
+        for (int64_t k = 0; k < M * n; k++)  // hansen.py:154-155
+            if (!std::isfinite(lo[k]) || !std::isfinite(hi[k])) throw ArgError{RB_ERR_ARG, "box must be bounded"};
+        surv_reserve(h, M);
+        Front sview{h->S.lo, h->S.hi, nullptr, nullptr, h->S.cap};
+        DevFront tmp;
+        tmp.f = sview;
+        load_rows(h, tmp, 0, lo, hi, nullptr, nullptr, M);
+        h->cur = 0;
+        DevFront& out = h->F[1];
+        front_reserve(h, out, M, 0);
+        scratch_reserve(h, M);
+        ck(cudaMemsetAsync(h->d_ctr, 0, sizeof(Counters), h->st), "ctr memset");
+        for (int64_t b0 = 0; b0 < M; b0 += h->W.B)
+            dispatch_n<KrawczykK>(n, h, b0, std::min<int64_t>(M, b0 + h->W.B), out.f, out.f.cert);
+        std::vector<double> slo((size_t)M * n), shi((size_t)M * n);
+        for (int j = 0; j < n; j++) {
+            ck(cudaMemcpyAsync(slo.data() + (size_t)j * M, out.f.lo + (size_t)j * out.f.cap, sizeof(double) * M,
+                               cudaMemcpyDeviceToHost, h->st), "d2h");
+            ck(cudaMemcpyAsync(shi.data() + (size_t)j * M, out.f.hi + (size_t)j * out.f.cap, sizeof(double) * M,
+                               cudaMemcpyDeviceToHost, h->st), "d2h");
+        }
+        ck(cudaMemcpyAsync(ok, out.f.cert, M, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaStreamSynchronize(h->st), "sync");
+        const double qnan = std::numeric_limits<double>::quiet_NaN();
+        for (int64_t r = 0; r < M; r++)
+            for (int j = 0; j < n; j++) {
+                olo[r * n + j] = ok[r] ? slo[(size_t)j * M + r] : qnan;
+                ohi[r * n + j] = ok[r] ? shi[(size_t)j * M + r] : qnan;
+            }
     })
 }
 

@@ -1185,6 +1185,57 @@ __global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_
     (void)exact_acc;
 }
 
+// K2k: the Krawczyk operator (hansen.py:141-170) on the K2a/K2b scratch (x, M, g),
+// thread per box.  Row i: acc = [x_i,x_i] - g_i + sum_{j, (I - M)_ij != [0,0]}
+// (I - M)_ij (X_j - [x_j,x_j]), left to right, then acc intersected with X_i.
+// ok[b] = 0 for None (singular midpoint Jacobian or an empty intersection).
+template <int N>
+__global__ void __launch_bounds__(128) k_krawczyk(SBuf S, int64_t b_end, int64_t b0, HsScratch W, Front out,
+                                                  uint8_t* ok) {
+    for (int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < b_end;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = b - b0;
+        bool good = !(W.flags[t] & HSF_SINGULAR);
+        double xl[N], xh[N], xv[N];
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            xl[j] = S.lo[j * S.cap + b];
+            xh[j] = S.hi[j * S.cap + b];
+            xv[j] = W.x[j * W.B + t];
+        }
+        ival d[N];
+#pragma unroll
+        for (int j = 0; j < N; j++) d[j] = Fast::sub(mk(xl[j], xh[j]), mk(xv[j], xv[j]));
+#pragma unroll 1
+        for (int i = 0; i < N && good; i++) {
+            ival acc = Fast::sub(mk(xv[i], xv[i]), mk(W.fl[i * W.B + t], W.fh[i * W.B + t]));
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                const ival m = mk(W.jl[(i * N + j) * W.B + t], W.jh[(i * N + j) * W.B + t]);
+                const double e = (i == j) ? 1.0 : 0.0;
+                const ival c = Fast::sub(mk(e, e), m);
+                if (c.lo == 0.0 && c.hi == 0.0) continue;
+                acc = Fast::add(acc, gmul(c, d[j]));
+            }
+            double xi_lo = xl[0], xi_hi = xh[0];
+#pragma unroll
+            for (int j = 1; j < N; j++)
+                if (j == i) {
+                    xi_lo = xl[j];
+                    xi_hi = xh[j];
+                }
+            const double lo = py_max(acc.lo, xi_lo), hi = py_min(acc.hi, xi_hi);  // Interval.intersect
+            if (lo > hi) {
+                good = false;
+                break;
+            }
+            out.lo[i * out.cap + b] = canon0(lo);
+            out.hi[i * out.cap + b] = canon0(hi);
+        }
+        ok[b] = good ? 1 : 0;
+    }
+}
+
 // fast reciprocal-based single case of div_extended; exact emulation elsewhere
 __device__ __forceinline__ int div_extended_fast(ival p, ival y, ival& q0, ival& q1) {
     if (!contains_zero(y)) {

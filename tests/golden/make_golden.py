@@ -585,6 +585,30 @@ def part_merge():
     print(f"merge: {len(out)} cases, {sum('error' in o['result'] for o in out)} raise")
 
 
+def part_krawczyk():
+    rng = np.random.default_rng(19)
+    res = {}
+    for name in ["circle_line", "broyden_tri6", "katsura6", "brown8", "mickey", "noon3", "broyden_banded6",
+                 "quirk17b", "eco8"]:
+        s = load_system(name)
+        jac = s.jacobian()
+        los, his = [], []
+        for depth in (2, 6, 12, 24, 40):
+            lo, hi = random_cells(rng, s, 40, depth)
+            los.append(lo); his.append(hi)
+        lo = np.concatenate(los); hi = np.concatenate(his)
+        ok, olo, ohi = [], [], []
+        for r in range(lo.shape[0]):
+            k = hansen.krawczyk(s, jac, poly.Box.from_bounds(lo[r], hi[r]))
+            ok.append(k is not None)
+            olo.append([iv.lo for iv in k] if k is not None else [np.nan] * s.dimension)
+            ohi.append([iv.hi for iv in k] if k is not None else [np.nan] * s.dimension)
+        res[f"{name}_lo"] = lo; res[f"{name}_hi"] = hi
+        res[f"{name}_ok"] = np.array(ok); res[f"{name}_olo"] = np.array(olo); res[f"{name}_ohi"] = np.array(ohi)
+    np.savez_compressed(os.path.join(HERE, "kat_krawczyk.npz"), **res)
+    print("krawczyk:", {k[:-3]: int(v.sum()) for k, v in res.items() if k.endswith("_ok")})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--part", nargs="*", default=["systems", "interval", "poly", "gj", "hs", "solve"])
@@ -607,6 +631,8 @@ def main():
             part_solve("slow")
         elif p == "merge":
             part_merge()
+        elif p == "krawczyk":
+            part_krawczyk()
         print(f"[{p}] {time.time() - t0:.1f}s", flush=True)
 
 

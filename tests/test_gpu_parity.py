@@ -153,6 +153,51 @@ def test_hs_random_cells_vs_oracle(native, name):
             assert np.array_equal(gc, oc), (name, depth)
 
 
+# ------------------------------------------------------------------ Krawczyk
+
+
+def test_krawczyk_kat_vs_reference(native):
+    """rb_krawczyk == hansen.krawczyk (hansen.py:141-170) on the reference's own outputs."""
+    d = np.load(os.path.join(GOLDEN, "kat_krawczyk.npz"))
+    names = sorted({k.rsplit("_", 1)[0] for k in d.files if k.endswith("_ok")})
+    assert names
+    for name in names:
+        ok, olo, ohi = engine(name).krawczyk(d[f"{name}_lo"], d[f"{name}_hi"])
+        assert np.array_equal(ok, d[f"{name}_ok"]), name
+        assert_bits_equal(olo[ok], d[f"{name}_olo"][ok], f"{name} krawczyk lo")
+        assert_bits_equal(ohi[ok], d[f"{name}_ohi"][ok], f"{name} krawczyk hi")
+        assert np.isnan(olo[~ok]).all()
+
+
+@pytest.mark.parametrize("name", HS_SYSTEMS)
+def test_krawczyk_random_cells_vs_oracle(native, name):
+    spec = golden_spec(name)
+    eng = engine(name)
+    osys = oracle_sys(name)
+    for depth, seed in ((2, 15), (8, 16), (20, 17), (45, 18)):
+        plo, phi = random_cells(spec, 700, depth, seed)
+        ok, glo, ghi = eng.krawczyk(plo, phi)
+        ook, olo, ohi = osys.krawczyk(plo, phi)
+        assert np.array_equal(ok, ook), (name, depth)
+        assert_bits_equal(glo[ok], olo[ok], f"{name} d={depth} lo")
+        assert_bits_equal(ghi[ok], ohi[ok], f"{name} d={depth} hi")
+
+
+def test_krawczyk_public_api(native):
+    import math
+    from paper_1802_00330_b200 import Box, krawczyk
+    spec = golden_spec("circle_line")
+    b = Box.from_bounds([0.5, 0.5], [0.9, 0.9])
+    out = krawczyk(spec, None, b)
+    ook, olo, ohi = oracle_sys("circle_line").krawczyk(np.array([[0.5, 0.5]]), np.array([[0.9, 0.9]]))
+    if ook[0]:
+        assert [iv.lo for iv in out] == olo[0].tolist() and [iv.hi for iv in out] == ohi[0].tolist()
+    else:
+        assert out is None
+    with pytest.raises(ValueError):
+        krawczyk(spec, None, Box.from_bounds([0.0, -math.inf], [1.0, 1.0]))
+
+
 # ------------------------------------------------------------------ whole solves
 
 

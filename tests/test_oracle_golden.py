@@ -197,3 +197,15 @@ def test_oracle_solve(case):
     s, spec = osys(meta["system"])
     res = s.solve(spec.init_lo, spec.init_hi, threads=2, **meta["config"])
     check_solution(case, res, meta)
+
+
+def test_krawczyk():
+    """hansen.krawczyk (hansen.py:141-170): K(X) intersected with X, None when singular or empty."""
+    d = np.load(os.path.join(GOLDEN, "kat_krawczyk.npz"))
+    names = sorted({k.rsplit("_", 1)[0] for k in d.files if k.endswith("_ok")})
+    for name in names:
+        s, _ = osys(name)
+        ok, olo, ohi = s.krawczyk(d[f"{name}_lo"], d[f"{name}_hi"])
+        assert np.array_equal(ok, d[f"{name}_ok"]), name
+        assert_bits_equal(olo[ok], d[f"{name}_olo"][ok], f"{name} lo")
+        assert_bits_equal(ohi[ok], d[f"{name}_ohi"][ok], f"{name} hi")
