@@ -16,8 +16,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -151,6 +153,16 @@ struct rb_handle {
     size_t filter_smem = 0, eval_smem = 0, lin_smem = 0, sweep_smem = 0, ftab_smem = 0;
     int ftab_blocks_per_sm = 1;
     bool use_ftab = true;
+    bool hs_fused = true;        // k_hs_fused (tile in shared memory) for small HS batches
+    int64_t fused_rows = 0;      // largest HS batch k_hs_fused takes (set from the SM count)
+    cudaStream_t st_side = nullptr;  // captures the IF branch of the round graph
+    bool hs_cond = true;         // graph: IF node around eval/lin/sweep (else they early-exit)
+    // RB_TRACE=1: device timestamps (%globaltimer) at the phase boundaries of every
+    // round, printed to stderr after each solve (a profiling aid; adds one tiny launch per phase)
+    bool trace = false;
+    unsigned long long* d_trace = nullptr;
+    size_t fused_smem = 0;
+    int fused_blocks_per_sm = 1;
     HsScratch W{};
     int smem_optin = 48 * 1024;
 };
@@ -230,12 +242,16 @@ struct SetupK {
         }
         // the attribute is per kernel (shared by every handle of this n): set it to the opt-in maximum
         const size_t mx = std::max({h->filter_smem, h->eval_smem, h->lin_smem, h->sweep_smem});
+        h->fused_smem = fused_off_tiles(h->meta) +
+                        (size_t)(T / 32) * FusedLayout<N>::BPW * FusedLayout<N>::doubles * sizeof(double);
         if ((int)mx > h->smem_optin) throw ArgError{RB_ERR_LIMIT, "system tables exceed the shared-memory budget"};
         set_max_dyn_smem(k_filter<N>, h->smem_optin);
         set_max_dyn_smem(k_filter_tab<N>, h->smem_optin);
         set_max_dyn_smem(k_hs_eval<N>, h->smem_optin);
         set_max_dyn_smem(k_hs_lin<N>, h->smem_optin);
         set_max_dyn_smem(k_hs_sweep<N>, h->smem_optin);
+        set_max_dyn_smem(k_hs_fused<N>, h->smem_optin);
+        if ((int)h->fused_smem > h->smem_optin) h->hs_fused = false;
         int nb = 0;
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter<N>, h->filter_threads, h->filter_smem), "occ");
         h->filter_blocks_per_sm = std::max(1, nb);
@@ -249,6 +265,10 @@ struct SetupK {
         h->lin_blocks_per_sm = std::max(1, nb);
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_sweep<N>, T, h->sweep_smem), "occ");
         h->sweep_blocks_per_sm = std::max(1, nb);
+        if (h->hs_fused) {
+            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_fused<N>, T, h->fused_smem), "occ");
+            h->fused_blocks_per_sm = std::max(1, nb);
+        }
     }
 };
 
@@ -314,6 +334,20 @@ struct HsK {
         k_hs_sweep<N><<<grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem, h->st>>>(
             h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
         ck(cudaGetLastError(), "hs launch");
+    }
+};
+
+// fused K2 over all n_in rows of S (n_in read on the device when prm.count_from_ctr); `bound`
+// is the most rows it can see, which sizes the grid
+template <int N>
+struct HsFusedK {
+    static void run(rb_handle* h, int64_t n_in, HsParams prm, int64_t* tags, int64_t bound) {
+        const int T = h->hs_threads;
+        h->launches++;
+        const int64_t lanes = std::max<int64_t>(1, bound) * FusedLayout<N>::G;
+        k_hs_fused<N><<<grid_for(lanes, T, h->sms * h->fused_blocks_per_sm), T, h->fused_smem, h->st>>>(
+            h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
+        ck(cudaGetLastError(), "hs fused launch");
     }
 };
 
@@ -439,11 +473,71 @@ static void scratch_reserve(rb_handle* h, int64_t want) {
 }
 
 // all batches of the HS pipeline over at most `bound` survivors
-static void launch_hs_batches(rb_handle* h, int64_t bound, int64_t n_in, const HsParams& prm, int64_t* tags) {
+static void launch_hs_three(rb_handle* h, int64_t bound, int64_t n_in, const HsParams& prm, int64_t* tags) {
     scratch_reserve(h, std::max<int64_t>(bound, 1));
     const int64_t B = h->W.B;
     for (int64_t b0 = 0; b0 == 0 || b0 < bound; b0 += B)
         dispatch_n<HsK>(h->n, h, b0, n_in, prm, tags, std::min<int64_t>(B, bound - b0));
+}
+
+// HS over the survivors: k_hs_fused (one launch, latency-optimal) for counts up to
+// h->fused_rows, eval/lin/sweep (throughput-optimal) above.  When the count is only
+// known on the device both are enqueued and each exits unless the count is its own;
+// inside a graph capture the fused kernel instead sets an IF node around the other three.
+static void launch_hs_batches(rb_handle* h, int64_t bound, int64_t n_in, const HsParams& prm0, int64_t* tags) {
+    HsParams prm = prm0;
+    prm.has_cond = 0;
+    const int64_t thr = h->hs_fused ? h->fused_rows : -1;
+    const int64_t rows = prm.count_from_ctr ? bound : n_in;
+    if (rows <= thr) {
+        prm.fused_max = LLONG_MAX;
+        dispatch_n<HsFusedK>(h->n, h, n_in, prm, tags, bound);
+        return;
+    }
+    if (!prm.count_from_ctr || thr < 0) {
+        prm.fused_max = -1;
+        launch_hs_three(h, bound, n_in, prm, tags);
+        return;
+    }
+    prm.fused_max = thr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    ck(cudaStreamIsCapturing(h->st, &cs), "capture status");
+    if (cs != cudaStreamCaptureStatusActive || !h->hs_cond) {
+        dispatch_n<HsFusedK>(h->n, h, n_in, prm, tags, thr);
+        launch_hs_three(h, bound, n_in, prm, tags);
+        return;
+    }
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    ck(cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &cg, &deps, &ndeps), "capture info");
+    ck(cudaGraphConditionalHandleCreate(&prm.big_cond, cg, 0, 0), "cond handle");
+    prm.has_cond = 1;
+    dispatch_n<HsFusedK>(h->n, h, n_in, prm, tags, thr);
+    ck(cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &cg, &deps, &ndeps), "capture info");
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = prm.big_cond;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    ck(cudaGraphAddNode(&node, cg, deps, ndeps, &cp), "if node");
+    ck(cudaStreamUpdateCaptureDependencies(h->st, &node, 1, cudaStreamSetCaptureDependencies), "capture deps");
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaStream_t main_st = h->st;
+    ck(cudaStreamBeginCaptureToGraph(h->st_side, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+       "begin side capture");
+    h->st = h->st_side;
+    prm.has_cond = 0;
+    try {
+        launch_hs_three(h, bound, n_in, prm, tags);
+    } catch (...) {
+        h->st = main_st;
+        throw;
+    }
+    h->st = main_st;
+    cudaGraph_t side = nullptr;
+    ck(cudaStreamEndCapture(h->st_side, &side), "end side capture");
 }
 
 static void parents_reserve(rb_handle* h, int64_t need) {
@@ -708,14 +802,46 @@ static float elapsed(rb_handle* h, int a, int b) {
 }
 
 // K3 classify + K1 filter (no sync)
-static void launch_filter_phase(rb_handle* h, double target) {
+constexpr int kTraceRounds = 256, kTracePhases = 8;
+__global__ void k_stamp(unsigned long long* buf, const DevState* st, int round_host, int phase) {
+    const int r = st ? st->round_no : round_host;
+    if (r >= 0 && r < kTraceRounds) buf[r * kTracePhases + phase] = gtimer();
+}
+static void stamp(rb_handle* h, const DevState* st, int round_host, int phase) {
+    if (!h->trace) return;
+    k_stamp<<<1, 1, 0, h->st>>>(h->d_trace, st, round_host, phase);
+}
+static void trace_report(rb_handle* h, int rounds) {
+    if (!h->trace) return;
+    std::vector<unsigned long long> t((size_t)kTraceRounds * kTracePhases);
+    ck(cudaMemcpy(t.data(), h->d_trace, t.size() * 8, cudaMemcpyDeviceToHost), "trace d2h");
+    static const char* names[] = {"classify", "filter", "hs", "dedup", "settle+end"};
+    for (int r = 1; r <= std::min(rounds, kTraceRounds - 1); r++) {
+        const unsigned long long* p = &t[(size_t)r * kTracePhases];
+        if (!p[0]) continue;
+        std::fprintf(stderr, "[rb trace] round %2d:", r);
+        const unsigned long long end = (r + 1 < kTraceRounds && t[(size_t)(r + 1) * kTracePhases]) ?
+                                       t[(size_t)(r + 1) * kTracePhases] : p[5];
+        for (int k = 0; k < 5; k++) {
+            const unsigned long long b = k < 4 ? p[k + 1] : end;
+            if (p[k] && b >= p[k]) std::fprintf(stderr, " %s %.1f us", names[k], (b - p[k]) * 1e-3);
+        }
+        std::fprintf(stderr, "\n");
+    }
+    ck(cudaMemset(h->d_trace, 0, t.size() * 8), "trace clear");
+}
+
+static void launch_filter_phase(rb_handle* h, double target, int round_no = -1) {
     const int n = h->n;
     ck(cudaMemsetAsync(h->d_ctr, 0, sizeof(Counters), h->st), "ctr memset");
+    stamp(h, nullptr, round_no, 0);
     record(h, 0);
     if (h->n_cur > 0) dispatch_n<ClassifyK>(n, h, target);
     record(h, 1);
+    stamp(h, nullptr, round_no, 1);
     if (h->n_cur > 0) dispatch_n<FilterK>(n, h, h->n_cur, (int64_t*)nullptr);
     record(h, 2);
+    stamp(h, nullptr, round_no, 2);
 }
 
 // K2 HS (or pass-through) + exact dedup (no sync)
@@ -724,7 +850,9 @@ static void launch_hs_phase(rb_handle* h, const HsParams& prm0, bool dedup) {
     prm.count_from_ctr = 1;
     if (h->n_cur > 0) launch_hs_batches(h, std::min<int64_t>(h->S.cap, h->n_cur << h->n), 0, prm, nullptr);
     record(h, 3);
+    stamp(h, nullptr, prm0.round_no, 3);
     if (dedup) dispatch_n<DedupK>(h->n, h, h->F[h->cur ^ 1].f, h->F[h->cur].f);
+    stamp(h, nullptr, prm0.round_no, 4);
 }
 
 // Capacities for the coming round.  S keeps the largest size a round has
@@ -775,9 +903,10 @@ static void run_round(rb_handle* h, double target, const HsParams& prm, bool ded
         surv_reserve(h, need_s);
         parents_reserve(h, std::max<int64_t>(h->n_cur, 1));
         scratch_reserve(h, std::max<int64_t>(1, std::min<int64_t>(h->S.cap, h->n_cur << h->n)));
-        launch_filter_phase(h, target);
+        launch_filter_phase(h, target, prm.round_no);
         launch_hs_phase(h, prm, dedup);
         record(h, 4);
+        stamp(h, nullptr, prm.round_no, 5);
         sync_counters(h);
         const Counters& c = *h->h_ctr;
         if (c.n_surv > (unsigned long long)h->S.cap) {
@@ -838,6 +967,7 @@ static void release_all(rb_handle* h) {
     fr(h->W.fl);
     fr(h->W.fh);
     fr(h->W.flags);
+    fr(h->d_trace);
     if (h->st) cudaStreamSynchronize(h->st);  // frees are stream-ordered; the pool is shared
     h->pool = nullptr;
     graph_release(h);
@@ -847,6 +977,7 @@ static void release_all(rb_handle* h) {
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     if (h->st) cudaStreamDestroy(h->st);
+    if (h->st_side) cudaStreamDestroy(h->st_side);
 }
 
 // canonical order of F[cur] rows [0, N) -> result buffers (row-major)
@@ -963,6 +1094,7 @@ static int64_t graph_small_cap(int n) {
 
 __global__ void k_state_start(DevState* st) { st->t_round_ns = gtimer(); }
 
+
 static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int64_t scap,
                               const std::vector<uintptr_t>& key) {
     graph_release(h);
@@ -984,13 +1116,18 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     const int64_t l0 = h->launches;
     h->cur = 0;
     const int64_t fcap = h->F[0].f.cap;
+    stamp(h, h->d_state, 0, 0);
     dispatch_n<ClassifyK>(n, h, 0.0, (const DevState*)h->d_state, std::min<int64_t>(fcap, scap));
+    stamp(h, h->d_state, 0, 1);
     dispatch_n<FilterK>(n, h, std::max<int64_t>(1, scap >> n), (int64_t*)nullptr);
+    stamp(h, h->d_state, 0, 2);
     HsParams p = prm;
     p.count_from_ctr = 1;
     p.st = h->d_state;
     launch_hs_batches(h, scap, 0, p, nullptr);
+    stamp(h, h->d_state, 0, 3);
     if (dedup) dispatch_n<DedupK>(n, h, h->F[1].f, h->F[0].f);
+    stamp(h, h->d_state, 0, 4);
     dispatch_n<SettleK>(n, h, std::min<int64_t>(fcap, 3 * scap));
     h->launches++;
     k_round_end<<<1, 32, 0, h->st>>>(h->d_state, h->d_ctr, h->d_rstats, n, scap, hw, h->d_order, h->meta);
@@ -1038,7 +1175,9 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         (uintptr_t)h->table_slots, (uintptr_t)h->d_slot, (uintptr_t)h->d_dead, (uintptr_t)h->d_rstats,
         (uintptr_t)h->d_state, (uintptr_t)scap, (uintptr_t)dedup, (uintptr_t)prm.hs_enable_round,
         (uintptr_t)prm.hs_possible, (uintptr_t)hw_bits, (uintptr_t)prm.contract_output,
-        (uintptr_t)(h->use_ftab ? 1 : 0)};
+        (uintptr_t)(h->use_ftab ? 1 : 0), (uintptr_t)(h->hs_fused ? 1 : 0), (uintptr_t)h->fused_rows};
+    key.push_back((uintptr_t)h->hs_cond);
+    key.push_back((uintptr_t)h->trace);
     if (key != h->graph_key || !h->graph_exec) build_round_graph(h, prm, dedup, scap, key);
     DevState st{};
     st.n_cur = (unsigned long long)h->n_cur;
@@ -1185,6 +1324,7 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
         }
     }
     finalize_sorted(h);
+    trace_report(h, (int)h->stats.size());
     ck(cudaEventRecord(h->ev[6], h->st), "ev end");
     ck(cudaEventSynchronize(h->ev[6]), "ev sync");
     float dev_ms = 0.f;
@@ -1291,6 +1431,9 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         h->sms = prop.multiProcessorCount;
         h->smem_optin = (int)prop.sharedMemPerBlockOptin;
         ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&h->st_side, cudaStreamNonBlocking), "stream");
+        h->fused_rows = (int64_t)h->sms * 80;  // measured crossover, tools/hs_ab.py
+        if (const char* tr = std::getenv("RB_TRACE")) h->trace = tr[0] == '1';
         h->pool = device_pool(device);  // process-wide per device: memory outlives handles
         PoolScope ps(h);
         for (auto& e : h->ev) ck(cudaEventCreate(&e), "event");
@@ -1299,6 +1442,10 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
         h->mem_budget = (size_t)(0.80 * (double)free_b);
         dalloc(&h->d_ctr, 1);
+        if (h->trace) {
+            dalloc(&h->d_trace, (size_t)kTraceRounds * kTracePhases);
+            ck(cudaMemsetAsync(h->d_trace, 0, (size_t)kTraceRounds * kTracePhases * 8, h->st), "trace clear");
+        }
         dalloc(&h->d_order, 16);
         reset_order(h);
         ck(cudaMallocHost((void**)&h->h_ctr, sizeof(Counters)), "pinned ctr");
@@ -1762,6 +1909,15 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     const std::string k(key);
     if (k == "filter_tab") {
         h->use_ftab = value != 0;
+        return RB_OK;
+    }
+    if (k == "hs_fused") {  // 0: eval/lin/sweep only, 1: by batch size, 2: fused only
+        h->hs_fused = value != 0 && h->fused_smem <= (size_t)h->smem_optin;
+        h->fused_rows = value == 2 ? INT64_MAX : (int64_t)h->sms * 80;
+        return RB_OK;
+    }
+    if (k == "hs_cond") {
+        h->hs_cond = value != 0;
         return RB_OK;
     }
     if (k == "graph") {

@@ -814,6 +814,9 @@ struct HsParams {
     int contract_output;   // SolverConfig.hs_contract
     int count_from_ctr;    // n_in = ctr->n_surv instead of n_in arg
     const DevState* st;    // graph mode: the round number comes from the device state
+    long long fused_max;   // k_hs_fused takes n_in <= fused_max rows, eval/lin/sweep take larger counts
+    int has_cond;          // graph mode: k_hs_fused selects the eval/lin/sweep branch (IF node)
+    cudaGraphConditionalHandle big_cond;
 };
 
 struct HsScratch {         // SoA with stride B (batch capacity)
@@ -855,6 +858,39 @@ __device__ __forceinline__ int64_t hs_count(const HsParams& prm, const Counters*
     return n_in;
 }
 
+// HS off for this round: survivors join the frontier uncertified (bnb.py:580-581)
+template <int N>
+__device__ void hs_passthrough(const SBuf& S, int64_t n_in, const Front& out, Counters* ctr, int64_t* tags) {
+    const int lane = threadIdx.x & 31;
+    // pass-through: survivors join the frontier uncertified
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x < n_in;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool valid = i < n_in;
+        double w = 0.0;
+        const unsigned long long slot = warp_append(valid, &ctr->n_next);
+        if (valid) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                const double lo = S.lo[j * S.cap + i], hi = S.hi[j * S.cap + i];
+                const double d = __dsub_rn(hi, lo);
+                w = j == 0 ? d : (d > w ? d : w);
+                if (slot < (unsigned long long)out.cap) {
+                    out.lo[j * out.cap + slot] = lo;
+                    out.hi[j * out.cap + slot] = hi;
+                }
+            }
+            if (slot < (unsigned long long)out.cap) {
+                out.cert[slot] = 0;
+                out.unsplit[slot] = 0;
+                if (tags) tags[slot] = 2 * i;
+            }
+        }
+        unsigned long long wb = valid ? (unsigned long long)__double_as_longlong(w) : 0ull;
+        wb = warp_max(wb);
+        if (lane == 0 && wb) atomicMax(&ctr->wmax, wb);
+    }
+}
+
 // K2a: thread per box.  Rows [b0, b0 + B) of S.  When HS is off for this round the
 // first batch launch copies S into F_next instead (bnb.py:580-581).
 template <int N>
@@ -864,38 +900,11 @@ __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __
     extern __shared__ __align__(16) uint8_t smem[];
     bool hs_on;
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
-    if (n_in < 0) return;
+    if (n_in < 0 || n_in <= prm.fused_max) return;  // small counts: k_hs_fused
     if (blockIdx.x == 0 && threadIdx.x == 0 && b0 == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
     const int lane = threadIdx.x & 31;
     if (!hs_on) {
-        if (b0 != 0) return;
-        // pass-through: survivors join the frontier uncertified
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x < n_in;
-             i += (int64_t)gridDim.x * blockDim.x) {
-            const bool valid = i < n_in;
-            double w = 0.0;
-            const unsigned long long slot = warp_append(valid, &ctr->n_next);
-            if (valid) {
-#pragma unroll
-                for (int j = 0; j < N; j++) {
-                    const double lo = S.lo[j * S.cap + i], hi = S.hi[j * S.cap + i];
-                    const double d = __dsub_rn(hi, lo);
-                    w = j == 0 ? d : (d > w ? d : w);
-                    if (slot < (unsigned long long)out.cap) {
-                        out.lo[j * out.cap + slot] = lo;
-                        out.hi[j * out.cap + slot] = hi;
-                    }
-                }
-                if (slot < (unsigned long long)out.cap) {
-                    out.cert[slot] = 0;
-                    out.unsplit[slot] = 0;
-                    if (tags) tags[slot] = 2 * i;
-                }
-            }
-            unsigned long long wb = valid ? (unsigned long long)__double_as_longlong(w) : 0ull;
-            wb = warp_max(wb);
-            if (lane == 0 && wb) atomicMax(&ctr->wmax, wb);
-        }
+        if (b0 == 0) hs_passthrough<N>(S, n_in, out, ctr, tags);
         return;
     }
     const int64_t b_end = min(n_in, b0 + W.B);
@@ -1011,11 +1020,21 @@ __device__ __forceinline__ ival pmul(double a, ival y) {
     else return pmul_minmax(a, y);
 }
 
+// Where one box's HS operands live: J / M at jl, jh[(i*N + j) * ws], F(x) / g at
+// fl, fh[i * ws] -- the HBM scratch (ws = batch stride) or a shared-memory tile (ws = 1).
+struct LinSink {
+    double* jl;
+    double* jh;
+    double* fl;
+    double* fh;
+    int64_t ws;
+};
+
 // M = A J and g = A F(x) (linalg.py:102-129): acc = [0,0]; acc += [a,a] * B[u][j], u ascending.
 // Lane (col, half) holds J[:, col] in registers and produces rows of its half.
 template <int N, class A>
-__device__ __forceinline__ void lin_products(const double* Am, const ival* jcol, int l, int64_t t,
-                                             const HsScratch& W, unsigned gmask) {
+__device__ __forceinline__ void lin_products(const double* Am, const ival* jcol, int l, const LinSink& K,
+                                             unsigned gmask) {
     constexpr int H = (N + 1) / 2;
     if (l < 2 * N) {
         const int col = l % N, half = l / N;
@@ -1026,28 +1045,135 @@ __device__ __forceinline__ void lin_products(const double* Am, const ival* jcol,
                 ival acc = mk(0.0, 0.0);
 #pragma unroll
                 for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A>(Am[i * N + u], jcol[u]));
-                W.jl[(i * N + col) * W.B + t] = acc.lo;
-                W.jh[(i * N + col) * W.B + t] = acc.hi;
+                K.jl[(i * N + col) * K.ws] = acc.lo;
+                K.jh[(i * N + col) * K.ws] = acc.hi;
             }
         }
     }
     ival acc = mk(0.0, 0.0);
     if (l < N) {
 #pragma unroll
-        for (int u = 0; u < N; u++)
-            acc = A::add(acc, pmul<A>(Am[l * N + u], mk(W.fl[u * W.B + t], W.fh[u * W.B + t])));
+        for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A>(Am[l * N + u], mk(K.fl[u * K.ws], K.fh[u * K.ws])));
     }
     __syncwarp(gmask);  // every lane has read F(x) before g overwrites it
     if (l < N) {
-        W.fl[l * W.B + t] = acc.lo;
-        W.fh[l * W.B + t] = acc.hi;
+        K.fl[l * K.ws] = acc.lo;
+        K.fh[l * K.ws] = acc.hi;
     }
 }
 
 template <int N>
-__device__ __noinline__ void lin_products_exact(const double* Am, const ival* jcol, int l, int64_t t,
-                                                const HsScratch& W, unsigned gmask) {
-    lin_products<N, Exact>(Am, jcol, l, t, W, gmask);
+__device__ __noinline__ void lin_products_exact(const double* Am, const ival* jcol, int l, const LinSink& K,
+                                                unsigned gmask) {
+    lin_products<N, Exact>(Am, jcol, l, K, gmask);
+}
+
+// K2b on one box by the G lanes of a group: mid(J), Gauss-Jordan inverse A (lane =
+// column of [mid J | I], registers; pivot column broadcast through sCol), then
+// M = A J and g = A F(x) over J / F(x) in place.  Returns true when singular.
+template <int N, int G>
+__device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* sCol, int l, unsigned gmask,
+                                          bool& exact_lin) {
+    // J column (l % N), kept in registers for M
+    ival jcol[N];
+    double c[N];
+    double colmax = 0.0;
+    ExpRange rj;
+    rj.init();
+    if (l < 2 * N) {
+        const int col = l % N;
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            jcol[i] = mk(K.jl[(i * N + col) * K.ws], K.jh[(i * N + col) * K.ws]);
+            rj.add(jcol[i].lo);
+            rj.add(jcol[i].hi);
+        }
+    }
+    if (l < N) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            c[i] = mid_of(jcol[i].lo, jcol[i].hi);  // mid_matrix, linalg.py:132-134
+            colmax = fmax(colmax, fabs(c[i]));
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; i++) c[i] = (l - N == i) ? 1.0 : 0.0;
+    }
+    // Gauss-Jordan inverse (linalg.py:137-172), lane = column of [jc | I]
+    const double scale = group_max<G>(gmask, l < N ? colmax : 0.0);
+    bool singular = scale == 0.0;
+    const double threshold = __dmul_rn(1e-12, scale);
+#pragma unroll
+    for (int k = 0; k < N; k++) {
+        if (singular) break;  // group-uniform
+        if (l == k) {
+            int pr = k;  // first row r >= k with max |c[r][k]|
+            double best = fabs(c[k]);
+#pragma unroll
+            for (int r = k + 1; r < N; r++)
+                if (fabs(c[r]) > best) {
+                    best = fabs(c[r]);
+                    pr = r;
+                }
+#pragma unroll
+            for (int i = 0; i < N; i++) sCol[i] = c[i];
+            sCol[N] = (double)pr;
+        }
+        __syncwarp(gmask);
+        const int pr = (int)sCol[N];
+        const double pivot = sCol[pr];
+        if (fabs(pivot) < threshold) {
+            singular = true;
+        } else {
+#pragma unroll
+            for (int r = k + 1; r < N; r++)
+                if (r == pr) {
+                    const double tmp = c[k];
+                    c[k] = c[r];
+                    c[r] = tmp;
+                }
+            const double inv = __ddiv_rn(1.0, pivot);
+            if (l >= k && l < 2 * N) {
+                c[k] = __dmul_rn(c[k], inv);
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    if (i == k) continue;
+                    const double f = sCol[i == pr ? k : i];  // column k after the row swap
+                    // the reference skips f == 0 (linalg.py:168); c - 0*c[k] == c for the finite
+                    // values here (only a zero's sign could differ), so no test is needed
+                    c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
+                }
+            }
+        }
+        __syncwarp(gmask);
+    }
+    exact_lin = false;
+    if (singular) return true;
+    ExpRange ra, rf;
+    ra.init();
+    rf.init();
+    if (l >= N && l < 2 * N) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            Am[i * N + (l - N)] = c[i];
+            ra.add(c[i]);
+        }
+    }
+    if (l < N) {
+        rf.add(K.fl[l * K.ws]);
+        rf.add(K.fh[l * K.ws]);
+    }
+    group_reduce<G>(gmask, ra);
+    group_reduce<G>(gmask, rj);
+    group_reduce<G>(gmask, rf);
+    rj.emin = min(rj.emin, rf.emin);
+    rj.emax = max(rj.emax, rf.emax);
+    const bool fastM = prod_guard_ok(ra, rj);
+    __syncwarp(gmask);
+    if (fastM) lin_products<N, Fast>(Am, jcol, l, K, gmask);
+    else lin_products_exact<N>(Am, jcol, l, K, gmask);
+    exact_lin = !fastM;
+    return false;
 }
 
 // K2b: G lanes per box; boxes assigned warp-uniformly.
@@ -1059,130 +1185,26 @@ __global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_
     extern __shared__ __align__(16) uint8_t smem[];
     bool hs_on;
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
-    if (n_in < 0 || !hs_on) return;
+    if (n_in < 0 || !hs_on || n_in <= prm.fused_max) return;
     const int64_t b_end = min(n_in, b0 + W.B);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gi = lane / G, l = lane % G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
     double* s = reinterpret_cast<double*>(smem) + (size_t)(warp * L::BPW + gi) * L::doubles;
-    double* Am = s + L::oA;
-    double* sCol = s + L::oCol;
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t wglob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    unsigned long long exact_acc = 0;
     for (int64_t wb0 = b0 + wglob * L::BPW; wb0 < b_end; wb0 += warps_total * L::BPW) {
         const int64_t b = wb0 + gi;
         if (b < b_end) {
             const int64_t t = b - b0;
-            // J column (l % N), kept in registers for M
-            ival jcol[N];
-            double c[N];
-            double colmax = 0.0;
-            ExpRange rj;
-            rj.init();
-            if (l < 2 * N) {
-                const int col = l % N;
-#pragma unroll
-                for (int i = 0; i < N; i++) {
-                    jcol[i] = mk(W.jl[(i * N + col) * W.B + t], W.jh[(i * N + col) * W.B + t]);
-                    rj.add(jcol[i].lo);
-                    rj.add(jcol[i].hi);
-                }
-            }
-            if (l < N) {
-#pragma unroll
-                for (int i = 0; i < N; i++) {
-                    c[i] = mid_of(jcol[i].lo, jcol[i].hi);  // mid_matrix, linalg.py:132-134
-                    colmax = fmax(colmax, fabs(c[i]));
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < N; i++) c[i] = (l - N == i) ? 1.0 : 0.0;
-            }
-            // Gauss-Jordan inverse (linalg.py:137-172), lane = column of [jc | I]
-            const double scale = group_max<G>(gmask, l < N ? colmax : 0.0);
-            bool singular = scale == 0.0;
-            const double threshold = __dmul_rn(1e-12, scale);
-#pragma unroll
-            for (int k = 0; k < N; k++) {
-                if (singular) break;  // group-uniform
-                if (l == k) {
-                    int pr = k;  // first row r >= k with max |c[r][k]|
-                    double best = fabs(c[k]);
-#pragma unroll
-                    for (int r = k + 1; r < N; r++)
-                        if (fabs(c[r]) > best) {
-                            best = fabs(c[r]);
-                            pr = r;
-                        }
-#pragma unroll
-                    for (int i = 0; i < N; i++) sCol[i] = c[i];
-                    sCol[N] = (double)pr;
-                }
-                __syncwarp(gmask);
-                const int pr = (int)sCol[N];
-                const double pivot = sCol[pr];
-                if (fabs(pivot) < threshold) {
-                    singular = true;
-                } else {
-#pragma unroll
-                    for (int r = k + 1; r < N; r++)
-                        if (r == pr) {
-                            const double tmp = c[k];
-                            c[k] = c[r];
-                            c[r] = tmp;
-                        }
-                    const double inv = __ddiv_rn(1.0, pivot);
-                    if (l >= k && l < 2 * N) {
-                        c[k] = __dmul_rn(c[k], inv);
-#pragma unroll
-                        for (int i = 0; i < N; i++) {
-                            if (i == k) continue;
-                            const double f = sCol[i == pr ? k : i];  // column k after the row swap
-                            // the reference skips f == 0 (linalg.py:168); c - 0*c[k] == c for the finite
-                            // values here (only a zero's sign could differ), so no test is needed
-                            c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
-                        }
-                    }
-                }
-                __syncwarp(gmask);
-            }
-            if (singular) {
-                if (l == 0) W.flags[t] |= HSF_SINGULAR;
-            } else {
-                ExpRange ra, rf;
-                ra.init();
-                rf.init();
-                if (l >= N && l < 2 * N) {
-#pragma unroll
-                    for (int i = 0; i < N; i++) {
-                        Am[i * N + (l - N)] = c[i];
-                        ra.add(c[i]);
-                    }
-                }
-                if (l < N) {
-                    rf.add(W.fl[l * W.B + t]);
-                    rf.add(W.fh[l * W.B + t]);
-                }
-                group_reduce<G>(gmask, ra);
-                group_reduce<G>(gmask, rj);
-                group_reduce<G>(gmask, rf);
-                rj.emin = min(rj.emin, rf.emin);
-                rj.emax = max(rj.emax, rf.emax);
-                const bool fastM = prod_guard_ok(ra, rj);
-                __syncwarp(gmask);
-                if (fastM) lin_products<N, Fast>(Am, jcol, l, t, W, gmask);
-                else {
-                    lin_products_exact<N>(Am, jcol, l, t, W, gmask);
-                    if (l == 0) W.flags[t] |= HSF_EXACT_LIN;
-                }
-                exact_acc += (!fastM && l == 0) ? 1 : 0;
-            }
+            const LinSink K{W.jl + t, W.jh + t, W.fl + t, W.fh + t, W.B};
+            bool exact_lin;
+            const bool singular = lin_group<N, G>(K, s + L::oA, s + L::oCol, l, gmask, exact_lin);
+            if (l == 0) W.flags[t] |= singular ? HSF_SINGULAR : (exact_lin ? HSF_EXACT_LIN : 0);
             __syncwarp(gmask);
         }
         __syncwarp();
     }
-    (void)exact_acc;
 }
 
 // K2k: the Krawczyk operator (hansen.py:141-170) on the K2a/K2b scratch (x, M, g),
@@ -1258,7 +1280,7 @@ __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t 
     extern __shared__ __align__(16) uint8_t smem[];
     bool hs_on;
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
-    if (n_in < 0 || !hs_on) return;
+    if (n_in < 0 || !hs_on || n_in <= prm.fused_max) return;
     const int64_t b_end = min(n_in, b0 + W.B);
     const int lane = threadIdx.x & 31;
     const int stride = blockDim.x;
@@ -1427,6 +1449,251 @@ __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t 
     }
 }
 
+
+// ------------------------------------------------------------------ K2 fused
+//
+// k_hs_fused: the whole HS pass (K2a + K2b + K2c) for one box by the G lanes of a
+// group, operands in a shared-memory tile instead of the HBM scratch:
+//   eval   lane l evaluates polynomials l, l + G, ... of the n^2 + n (J(X), F(x))
+//   lin    lin_group (Gauss-Jordan + M = A J, g = A F(x)) on the tile
+//   sweep  row i: lane j forms M_ij (X_j - x_j) for its column in parallel, then
+//          every lane folds the products left to right (the reference order) and
+//          runs the same extended division, so control flow stays group-uniform
+// The arithmetic is operation-for-operation that of the three-kernel pipeline.
+template <int N>
+struct FusedLayout {
+    static constexpr int G = LinLayout<N>::G;
+    static constexpr int BPW = 32 / G;
+    static constexpr int oXl = 0, oXh = N, oXm = 2 * N;
+    static constexpr int oJl = 3 * N, oJh = 3 * N + N * N;
+    static constexpr int oFl = 3 * N + 2 * N * N, oFh = oFl + N;
+    static constexpr int oA = oFh + N;
+    static constexpr int oCol = oA + N * N;
+    static constexpr int doubles = oCol + N + 1;
+};
+
+__host__ __device__ inline int fused_off_tiles(const TabMeta& m) { return align16(stab_bytes(m, false)); }
+
+template <int N>
+__global__ void __launch_bounds__(128) k_hs_fused(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
+                                                  int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
+                                                  int64_t* tags) {
+    using L = FusedLayout<N>;
+    constexpr int G = L::G;
+    constexpr int P = N * N + N;
+    extern __shared__ __align__(16) uint8_t smem[];
+    bool hs_on;
+    const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
+    if (prm.has_cond && blockIdx.x == 0 && threadIdx.x == 0)
+        cudaGraphSetConditional(prm.big_cond, n_in > prm.fused_max ? 1u : 0u);
+    if (n_in < 0 || n_in > prm.fused_max) return;  // large counts: eval/lin/sweep
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
+    if (!hs_on) {
+        hs_passthrough<N>(S, n_in, out, ctr, tags);
+        return;
+    }
+    const STab tab = load_stab(meta, gtab, smem, false);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gi = lane / G, l = lane % G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
+    const unsigned below = (G == 32) ? 0u : ((1u << (gi * G)) - 1u);  // lanes of the groups before mine
+    double* s = reinterpret_cast<double*>(smem + fused_off_tiles(meta)) + (size_t)(warp * L::BPW + gi) * L::doubles;
+    const LinSink K{s + L::oJl, s + L::oJh, s + L::oFl, s + L::oFh, 1};
+    __syncthreads();
+    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t wglob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    unsigned long long ops_acc = 0, calls_acc = 0, exact_acc = 0;
+    for (int64_t wb0 = wglob * L::BPW; wb0 < n_in; wb0 += warps_total * L::BPW) {
+        const int64_t b = wb0 + gi;
+        const bool valid = b < n_in;
+        int kind = HS_EMPTY;
+        bool cert = false;
+        int fork_i = -1;
+        ival fp0 = mk(0.0, 0.0), fp1 = mk(0.0, 0.0);
+        ival cur = mk(0.0, 0.0);  // lane j < N: component j of the box being contracted
+        int rows = 0;
+        if (valid) {
+            if (l < N) {
+                const double lo = S.lo[l * S.cap + b], hi = S.hi[l * S.cap + b];
+                s[L::oXl + l] = lo;
+                s[L::oXh + l] = hi;
+                s[L::oXm + l] = mid_of(lo, hi);  // Box.midpoint, poly.py:114-115
+                cur = mk(lo, hi);
+            }
+            __syncwarp(gmask);
+            // ---- eval: J(X) (hansen.py:61-63) and F(x) (poly.py:205-207)
+            ExpRange rx, rm;
+            rx.init();
+            rm.init();
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                rx.add(s[L::oXl + j]);
+                rx.add(s[L::oXh + j]);
+                rm.add(s[L::oXm + j]);
+            }
+            const bool fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
+            const bool fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
+#pragma unroll 1
+            for (int q = l; q < P; q += G) {
+                if (q < N * N) {
+                    const ival v = fastJ ? eval_poly<Fast>(tab, N + q, s + L::oXl, s + L::oXh, 1)
+                                         : eval_poly_exact(tab, N + q, s + L::oXl, s + L::oXh, 1);
+                    s[L::oJl + q] = v.lo;
+                    s[L::oJh + q] = v.hi;
+                } else {
+                    const int i = q - N * N;
+                    const ival v = fastF ? eval_poly<Fast>(tab, i, s + L::oXm, s + L::oXm, 1)
+                                         : eval_poly_exact(tab, i, s + L::oXm, s + L::oXm, 1);
+                    s[L::oFl + i] = v.lo;
+                    s[L::oFh + i] = v.hi;
+                }
+            }
+            if (l == 0 && !(fastJ && fastF)) exact_acc++;
+            __syncwarp(gmask);
+            // ---- lin: A = mid(J)^-1, M = A J, g = A F(x)
+            bool exact_lin;
+            const bool singular = lin_group<N, G>(K, s + L::oA, s + L::oCol, l, gmask, exact_lin);
+            __syncwarp(gmask);
+            if (singular) {
+                kind = HS_SKIP;
+            } else {
+                // ---- sweep (hansen.py:91-138)
+                kind = HS_ONE;
+                const double xj = l < N ? s[L::oXm + l] : 0.0;
+#pragma unroll 1
+                for (int i = 0; i < N; i++) {
+                    rows = i + 1;
+                    ival prod = mk(0.0, 0.0);
+                    bool use = false;
+                    if (l < N && l != i) {
+                        const ival m = mk(s[L::oJl + i * N + l], s[L::oJh + i * N + l]);
+                        use = !(m.lo == 0.0 && m.hi == 0.0);
+                        if (use) prod = gmul(m, Fast::sub(cur, mk(xj, xj)));
+                    }
+                    const unsigned um = __ballot_sync(gmask, use) >> (gi * G);
+                    // p = -g_i - sum_{j != i, M_ij != [0,0]} M_ij (current_j - [x_j, x_j]), left to right
+                    ival p = mk(-s[L::oFh + i], -s[L::oFl + i]);
+#pragma unroll(N <= 8 ? N : 1)  // a fully unrolled fold of 12+ shuffles trips ptxas (C7600)
+                    for (int j = 0; j < N; j++) {
+                        const double plo = gshfl<G>(gmask, prod.lo, j);
+                        const double phi = gshfl<G>(gmask, prod.hi, j);
+                        if (um & (1u << j)) p = Fast::sub(p, mk(plo, phi));
+                    }
+                    const ival mii = mk(s[L::oJl + i * N + i], s[L::oJh + i * N + i]);
+                    const double xi = s[L::oXm + i];
+                    const ival cur_i = mk(gshfl<G>(gmask, cur.lo, i), gshfl<G>(gmask, cur.hi, i));
+                    ival q0 = mk(0.0, 0.0), q1 = mk(0.0, 0.0);
+                    const int dk = div_extended_fast(p, mii, q0, q1);
+                    if (dk == DIV_EMPTY) {
+                        kind = HS_EMPTY;
+                        break;
+                    }
+                    if (dk == DIV_WHOLE) continue;
+                    ival pieces[2];
+                    int npieces = 0;
+                    const int np = dk == DIV_SPLIT ? 2 : 1;
+#pragma unroll
+                    for (int q = 0; q < 2; q++) {
+                        if (q < np) {
+                            const ival y = Fast::add(mk(xi, xi), q == 0 ? q0 : q1);
+                            const double lo = py_max(y.lo, cur_i.lo);  // Interval.intersect
+                            const double hi = py_min(y.hi, cur_i.hi);
+                            if (!(lo > hi)) pieces[npieces++] = mk(lo, hi);
+                        }
+                    }
+                    if (npieces == 0) {
+                        kind = HS_EMPTY;
+                        break;
+                    }
+                    ival nc = pieces[0];
+                    if (npieces == 2) {
+                        nc = mk(py_min(pieces[0].lo, pieces[1].lo), py_max(pieces[0].hi, pieces[1].hi));  // hull
+                        if (fork_i < 0) {
+                            fork_i = i;
+                            fp0 = pieces[0];
+                            fp1 = pieces[1];
+                        }
+                    }
+                    if (l == i) cur = nc;
+                }
+                if (kind == HS_ONE && fork_i >= 0) kind = HS_TWO;
+                if (kind == HS_ONE) {  // certified iff strictly inside the input (hansen.py:129-132)
+                    const bool in = l >= N || (s[L::oXl + l] < cur.lo && cur.hi < s[L::oXh + l]);
+                    cert = __all_sync(gmask, in);
+                }
+            }
+            if (l == 0) {
+                calls_acc++;
+                ops_acc += meta.ops_hs_pre + (unsigned long long)meta.ops_hs_row * rows;
+            }
+        }
+        // outputs (bnb.py:197-210): group leaders reserve slots for the warp
+        int cnt = 0;
+        bool use_input = false;
+        if (valid) {
+            if (kind == HS_SKIP) {
+                cnt = 1;
+                use_input = true;
+                cert = false;
+            } else if (kind == HS_EMPTY) {
+                cnt = 0;
+            } else if (!prm.contract_output) {
+                cnt = 1;
+                use_input = true;
+            } else {
+                cnt = kind == HS_TWO ? 2 : 1;
+            }
+        }
+        const unsigned b1 = __ballot_sync(0xffffffffu, l == 0 && cnt == 1);
+        const unsigned b2 = __ballot_sync(0xffffffffu, l == 0 && cnt == 2);
+        const unsigned off = __popc(b1 & below) + 2 * __popc(b2 & below);
+        const unsigned total = __popc(b1) + 2 * __popc(b2);
+        unsigned long long wbase = 0;
+        if (lane == 0 && total) wbase = atomicAdd(&ctr->n_next, (unsigned long long)total);
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        double wmax = 0.0;
+        for (int q = 0; q < cnt; q++) {  // group-uniform
+            const unsigned long long slot = wbase + off + q;
+            double w = 0.0;
+            if (l < N) {
+                double lo, hi;
+                if (use_input) {
+                    lo = s[L::oXl + l];
+                    hi = s[L::oXh + l];
+                } else if (l == fork_i) {
+                    lo = q == 0 ? fp0.lo : fp1.lo;
+                    hi = q == 0 ? fp0.hi : fp1.hi;
+                } else {
+                    lo = cur.lo;
+                    hi = cur.hi;
+                }
+                w = __dsub_rn(hi, lo);
+                if (slot < (unsigned long long)out.cap) {
+                    out.lo[l * out.cap + slot] = canon0(lo);
+                    out.hi[l * out.cap + slot] = canon0(hi);
+                }
+            }
+            wmax = fmax(wmax, w);
+            if (l == 0 && slot < (unsigned long long)out.cap) {
+                out.cert[slot] = cert ? 1 : 0;
+                out.unsplit[slot] = 0;
+                if (tags) tags[slot] = 2 * b + q;
+            }
+        }
+        unsigned long long wbits = (unsigned long long)__double_as_longlong(wmax);
+        wbits = warp_max(wbits);
+        if (lane == 0 && wbits) atomicMax(&ctr->wmax, wbits);
+        __syncwarp();  // the tile is reused by the next box of this group
+    }
+    ops_acc = warp_sum(ops_acc);
+    calls_acc = warp_sum(calls_acc);
+    exact_acc = warp_sum(exact_acc);
+    if (lane == 0) {
+        if (ops_acc) atomicAdd(&ctr->hs_ops, ops_acc);
+        if (calls_acc) atomicAdd(&ctr->hs_calls, calls_acc);
+        if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
+    }
+}
 
 // ------------------------------------------------------------------ dedup
 

@@ -137,10 +137,13 @@ HS_SYSTEMS = ["circle_line", "broyden_tri6", "katsura6", "eco8", "brown8", "broy
               "noon5", "kinema", "caprasse", "reimer5", "katsura8", "cyclic9", "noon9"]
 
 
+@pytest.mark.parametrize("fused", [2, 0], ids=["fused", "three_kernel"])
 @pytest.mark.parametrize("name", HS_SYSTEMS)
-def test_hs_random_cells_vs_oracle(native, name):
+def test_hs_random_cells_vs_oracle(native, name, fused):
     spec = golden_spec(name)
-    eng = engine(name)
+    from paper_1802_00330_b200.system import compile_tables
+    eng = native.Engine(compile_tables(spec), 0)
+    eng.set_option("hs_fused", fused)
     osys = oracle_sys(name)
     for depth, seed in ((2, 5), (6, 6), (12, 7), (24, 8), (40, 9)):
         plo, phi = random_cells(spec, 512, depth, seed)
@@ -232,9 +235,10 @@ def check_against_golden(case, out, meta):
     assert not np.any(np.signbit(lo) & (lo == 0)) and not np.any(np.signbit(hi) & (hi == 0))
 
 
-@pytest.mark.parametrize("graph", [1, 0], ids=["device_loop", "host_loop"])
+@pytest.mark.parametrize("graph,fused", [(1, 1), (0, 1), (0, 0), (1, 2)],
+                         ids=["device_loop", "host_loop", "host_loop_three_kernel_hs", "device_loop_fused_hs"])
 @pytest.mark.parametrize("case", solve_cases())
-def test_solve_vs_reference_golden(native, case, graph):
+def test_solve_vs_reference_golden(native, case, graph, fused):
     """Whole solves, with the round loop on the device (CUDA graph WHILE node)
     and host-driven, against the reference's recorded results."""
     from paper_1802_00330_b200 import bnb
@@ -242,10 +246,12 @@ def test_solve_vs_reference_golden(native, case, graph):
     spec = golden_spec(meta["system"])
     eng = bnb.engine_for(spec)
     eng.set_option("graph", graph)
+    eng.set_option("hs_fused", fused)
     try:
         out = eng.solve(bnb.native_config(bnb.SolverConfig(**meta["config"])))
     finally:
         eng.set_option("graph", 1)
+        eng.set_option("hs_fused", 1)
     check_against_golden(case, out, meta)
 
 
