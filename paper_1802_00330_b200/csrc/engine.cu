@@ -15,6 +15,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -122,6 +123,16 @@ struct rb_handle {
     uint8_t* r_uns = nullptr;
     int64_t r_n = 0;
     bool r_on_host = false;  // small results are ordered on the host
+    bool r_ready = false;    // the result buffers already hold this solve's result
+    int64_t cap_r = 0;
+    // mapped pinned memory the round graph reads its start state from and writes back to
+    HostX* hx = nullptr;
+    HostX* hx_dev = nullptr;
+    DevRoundStats* hx_stats = nullptr;
+    DevRoundStats* hx_stats_dev = nullptr;
+    int cap_hx_stats = 0;
+    double *hx_lo = nullptr, *hx_hi = nullptr, *hx_lo_dev = nullptr, *hx_hi_dev = nullptr;
+    uint8_t *hx_c = nullptr, *hx_u = nullptr, *hx_c_dev = nullptr, *hx_u_dev = nullptr;
     std::vector<double> hr_lo, hr_hi;
     std::vector<uint8_t> hr_cert, hr_uns;
     bool have_result = false;
@@ -156,7 +167,14 @@ struct rb_handle {
     bool hs_fused = true;        // k_hs_fused (tile in shared memory) for small HS batches
     int64_t fused_rows = 0;      // largest HS batch k_hs_fused takes (set from the SM count)
     cudaStream_t st_side = nullptr;  // captures the IF branch of the round graph
-    bool hs_cond = true;         // graph: IF node around eval/lin/sweep (else they early-exit)
+    bool hs_cond = true;
+    bool pdl = false;            // programmatic dependent launch between round kernels
+    bool use_mk = false;         // k_small_rounds (persistent grid) for the smallest rounds (experimental)
+    int64_t mk_cap = 1 << 16;    // ... while n_cur * 2^n <= mk_cap
+    size_t mk_smem = 0;
+    int mk_blocks_per_sm = 0;
+    int mk_bps = 1;              // blocks per SM of k_small_rounds
+    unsigned* d_bar = nullptr;         // graph: IF node around eval/lin/sweep (else they early-exit)
     // RB_TRACE=1: device timestamps (%globaltimer) at the phase boundaries of every
     // round, printed to stderr after each solve (a profiling aid; adds one tiny launch per phase)
     bool trace = false;
@@ -269,8 +287,37 @@ struct SetupK {
             ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_fused<N>, T, h->fused_smem), "occ");
             h->fused_blocks_per_sm = std::max(1, nb);
         }
+        // persistent small-round kernel: 256 threads, shared memory for its largest phase
+        h->mk_smem = std::max<size_t>(filter_off_xs(h->meta) + (size_t)2 * N * 256 * sizeof(double),
+                                      fused_off_tiles(h->meta) + (size_t)(256 / 32) * FusedLayout<N>::BPW *
+                                                                     FusedLayout<N>::doubles * sizeof(double));
+        h->mk_blocks_per_sm = 0;
+        if ((int)h->mk_smem <= h->smem_optin) {
+            set_max_dyn_smem(k_small_rounds<N>, h->smem_optin);
+            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_small_rounds<N>, 256, h->mk_smem), "occ");
+            h->mk_blocks_per_sm = nb;
+        }
+        if (h->mk_blocks_per_sm < 1) h->use_mk = false;
     }
 };
+
+// Kernel launch on the handle's stream; with h->pdl the launch allows programmatic
+// dependent launch (the kernel's blocks start while the previous kernel drains and
+// wait in pdl_enter() for its completion).
+template <typename... KArgs, typename... Args>
+static void klaunch(rb_handle* h, void (*k)(KArgs...), int grid, int block, size_t smem, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h->st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = h->pdl ? 1 : 0;
+    ck(cudaLaunchKernelEx(&cfg, k, args...), "kernel launch");
+}
 
 template <int N>
 struct ClassifyK {
@@ -278,7 +325,7 @@ struct ClassifyK {
         Front cur = h->F[h->cur].f, next = h->F[h->cur ^ 1].f;
         const int blocks = grid_for(bound >= 0 ? bound : h->n_cur, 256, h->sms * 8);
         h->launches++;
-        k_classify<N><<<blocks, 256, 0, h->st>>>(h->meta, cur, h->n_cur, next, h->parents, h->d_ctr, target, st);
+        klaunch(h, k_classify<N>, blocks, 256, 0, h->meta, cur, h->n_cur, next, h->parents, h->d_ctr, target, st);
         ck(cudaGetLastError(), "classify launch");
     }
 };
@@ -288,7 +335,7 @@ struct AllParentsK {
     static void run(rb_handle* h) {
         const int blocks = grid_for(h->n_cur, 256, h->sms * 8);
         h->launches++;
-        k_all_parents<N><<<blocks, 256, 0, h->st>>>(h->meta, h->F[h->cur].f, h->n_cur, h->parents, h->d_ctr);
+        klaunch(h, k_all_parents<N>, blocks, 256, 0, h->meta, h->F[h->cur].f, h->n_cur, h->parents, h->d_ctr);
         ck(cudaGetLastError(), "parents launch");
     }
 };
@@ -301,7 +348,7 @@ struct FilterK {
             const int64_t units = N >= 8 ? (max_parents << Sh::CHLOG) : ((max_parents + Sh::PPB - 1) >> Sh::LOGPPB);
             const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)h->sms * h->ftab_blocks_per_sm));
             h->launches++;
-            k_filter_tab<N><<<blocks, 256, h->ftab_smem, h->st>>>(h->meta, h->d_tab, h->F[h->cur].f, h->parents,
+            klaunch(h, k_filter_tab<N>, blocks, 256, h->ftab_smem, h->meta, h->d_tab, h->F[h->cur].f, h->parents,
                                                                  h->d_ctr, h->S, tags, h->d_order);
             ck(cudaGetLastError(), "filter_tab launch");
             return;
@@ -309,7 +356,7 @@ struct FilterK {
         const int64_t work = max_parents << N;
         const int blocks = grid_for(work, h->filter_threads, h->sms * h->filter_blocks_per_sm);
         h->launches++;
-        k_filter<N><<<blocks, h->filter_threads, h->filter_smem, h->st>>>(h->meta, h->d_tab, h->F[h->cur].f,
+        klaunch(h, k_filter<N>, blocks, h->filter_threads, h->filter_smem, h->meta, h->d_tab, h->F[h->cur].f,
                                                                          h->parents, h->d_ctr, h->S, tags, h->d_order);
         ck(cudaGetLastError(), "filter launch");
     }
@@ -327,11 +374,10 @@ struct HsK {
         const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(B, batch_bound));
         const int64_t target = (int64_t)h->sms * 1024;
         const int R = (int)std::max<int64_t>(1, std::min<int64_t>(N * N + N, (target + bound - 1) / bound));
-        k_hs_eval<N><<<grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem, h->st>>>(
+        klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
             h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags, R);
-        k_hs_lin<N><<<grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem,
-                      h->st>>>(h->S, n_in, b0, prm, h->W, h->d_ctr);
-        k_hs_sweep<N><<<grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem, h->st>>>(
+        klaunch(h, k_hs_lin<N>, grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem, h->S, n_in, b0, prm, h->W, h->d_ctr);
+        klaunch(h, k_hs_sweep<N>, grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem,
             h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
         ck(cudaGetLastError(), "hs launch");
     }
@@ -345,7 +391,7 @@ struct HsFusedK {
         const int T = h->hs_threads;
         h->launches++;
         const int64_t lanes = std::max<int64_t>(1, bound) * FusedLayout<N>::G;
-        k_hs_fused<N><<<grid_for(lanes, T, h->sms * h->fused_blocks_per_sm), T, h->fused_smem, h->st>>>(
+        klaunch(h, k_hs_fused<N>, grid_for(lanes, T, h->sms * h->fused_blocks_per_sm), T, h->fused_smem,
             h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
         ck(cudaGetLastError(), "hs fused launch");
     }
@@ -363,19 +409,81 @@ struct KrawczykK {
         const int64_t bound = b_end - b0;
         const int64_t target = (int64_t)h->sms * 1024;
         const int R = (int)std::max<int64_t>(1, std::min<int64_t>(N * N + N, (target + bound - 1) / bound));
-        k_hs_eval<N><<<grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem, h->st>>>(
+        klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
             h->meta, h->d_tab, h->S, b_end, b0, prm, h->W, out, h->d_ctr, nullptr, R);
-        k_hs_lin<N><<<grid_for(std::min(B, bound), (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T,
-                      h->lin_smem, h->st>>>(h->S, b_end, b0, prm, h->W, h->d_ctr);
-        k_krawczyk<N><<<grid_for(bound, 128, h->sms * 16), 128, 0, h->st>>>(h->S, b_end, b0, h->W, out, ok);
+        klaunch(h, k_hs_lin<N>, grid_for(std::min(B, bound), (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem, h->S, b_end, b0, prm, h->W, h->d_ctr);
+        klaunch(h, k_krawczyk<N>, grid_for(bound, 128, h->sms * 16), 128, 0, h->S, b_end, b0, h->W, out, ok);
         ck(cudaGetLastError(), "krawczyk launch");
+    }
+};
+
+// persistent small rounds (cooperative: every block resident for the grid barrier)
+template <int N>
+struct SmallRoundsK {
+    static void run(rb_handle* h, const HsParams& prm, bool dedup, int64_t scap, cudaGraphConditionalHandle hw) {
+        SmallArgs a{};
+        a.dedup = dedup ? 1 : 0;
+        a.trace = h->trace ? h->d_trace : nullptr;
+        a.meta = h->meta;
+        a.gtab = h->d_tab;
+        a.f0 = h->F[0].f;
+        a.f1 = h->F[1].f;
+        a.S = h->S;
+        a.parents = h->parents;
+        a.ctr = h->d_ctr;
+        a.st = h->d_state;
+        a.rstats = h->d_rstats;
+        a.order = h->d_order;
+        a.table = h->d_table;
+        a.table_mask = (unsigned long long)(h->table_slots - 1);
+        a.slot_of = h->d_slot;
+        a.dead = h->d_dead;
+        a.prm = prm;
+        a.bar = h->d_bar;
+        a.mk_cap = std::min<int64_t>(h->mk_cap, scap);
+        a.graph_cap = scap;
+        a.h_while = hw;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(h->sms * std::min(h->mk_blocks_per_sm, h->mk_bps)));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = h->mk_smem;
+        cfg.stream = h->st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        h->launches++;
+        ck(cudaLaunchKernelEx(&cfg, k_small_rounds<N>, a), "small rounds launch");
+    }
+};
+
+template <int N>
+struct DedupInsertK {
+    static void run(rb_handle* h, Front next) {
+        const int blocks = grid_for(next.cap, 256, h->sms * 8);
+        h->launches++;
+        klaunch(h, k_dedup_insert<N>, blocks, 256, 0, next, h->d_table, (unsigned long long)(h->table_slots - 1),
+                h->d_slot, h->d_dead, h->d_ctr, h->S.cap);
+    }
+};
+
+// dedup finish + F[1] -> F[0] + round end (graph mode)
+template <int N>
+struct TailK {
+    static void run(rb_handle* h, bool dedup, int64_t bound, int64_t scap, cudaGraphConditionalHandle hw) {
+        const int blocks = grid_for(bound, 256, h->sms * 2);
+        h->launches++;
+        klaunch(h, k_round_tail<N>, blocks, 256, 0, h->F[1].f, h->F[0].f, h->d_table, (const unsigned*)h->d_slot,
+                (const uint8_t*)h->d_dead, dedup ? 1 : 0, h->d_state, h->d_ctr, h->d_rstats, scap, hw, h->d_order,
+                h->meta);
     }
 };
 
 template <int N>
 struct SettleK {
     static void run(rb_handle* h, int64_t bound) {
-        k_settle<N><<<grid_for(bound, 256, h->sms * 8), 256, 0, h->st>>>(h->F[1].f, h->F[0].f, h->d_ctr);
+        klaunch(h, k_settle<N>, grid_for(bound, 256, h->sms * 8), 256, 0, h->F[1].f, h->F[0].f, h->d_ctr);
         ck(cudaGetLastError(), "settle launch");
     }
 };
@@ -386,9 +494,9 @@ struct DedupK {
         // persistent grids: the row count is read on the device
         const int blocks = grid_for(next.cap, 256, h->sms * 8);
         h->launches += 2;
-        k_dedup_insert<N><<<blocks, 256, 0, h->st>>>(next, h->d_table, (unsigned long long)(h->table_slots - 1),
+        klaunch(h, k_dedup_insert<N>, blocks, 256, 0, next, h->d_table, (unsigned long long)(h->table_slots - 1),
                                                      h->d_slot, h->d_dead, h->d_ctr, h->S.cap);
-        k_dedup_finish<N><<<blocks, 256, 0, h->st>>>(next, other, h->d_table, h->d_slot, h->d_dead, h->d_ctr,
+        klaunch(h, k_dedup_finish<N>, blocks, 256, 0, next, other, h->d_table, h->d_slot, h->d_dead, h->d_ctr,
                                                      h->S.cap);
         ck(cudaGetLastError(), "dedup launch");
     }
@@ -562,7 +670,6 @@ static void sync_counters(rb_handle* h) {
 static void reset_order(rb_handle* h) {
     for (int k = 0; k < 16; k++) h->h_order[k] = k;  // reference order to start
     ck(cudaMemcpyAsync(h->d_order, h->h_order, sizeof(h->h_order), cudaMemcpyHostToDevice, h->st), "order h2d");
-    ck(cudaStreamSynchronize(h->st), "order sync");
 }
 
 // host-driven rounds: next round's filter order from this round's counts
@@ -803,29 +910,29 @@ static float elapsed(rb_handle* h, int a, int b) {
 
 // K3 classify + K1 filter (no sync)
 constexpr int kTraceRounds = 256, kTracePhases = 8;
-__global__ void k_stamp(unsigned long long* buf, const DevState* st, int round_host, int phase) {
-    const int r = st ? st->round_no : round_host;
+__global__ void k_stamp(unsigned long long* buf, const DevState* st, int round_host, int phase, int delta) {
+    const int r = (st ? st->round_no : round_host) + delta;
     if (r >= 0 && r < kTraceRounds) buf[r * kTracePhases + phase] = gtimer();
 }
-static void stamp(rb_handle* h, const DevState* st, int round_host, int phase) {
+static void stamp(rb_handle* h, const DevState* st, int round_host, int phase, int delta = 0) {
     if (!h->trace) return;
-    k_stamp<<<1, 1, 0, h->st>>>(h->d_trace, st, round_host, phase);
+    k_stamp<<<1, 1, 0, h->st>>>(h->d_trace, st, round_host, phase, delta);
 }
 static void trace_report(rb_handle* h, int rounds) {
     if (!h->trace) return;
     std::vector<unsigned long long> t((size_t)kTraceRounds * kTracePhases);
     ck(cudaMemcpy(t.data(), h->d_trace, t.size() * 8, cudaMemcpyDeviceToHost), "trace d2h");
-    static const char* names[] = {"classify", "filter", "hs", "dedup", "settle+end"};
+    static const char* names[] = {"classify", "filter", "hs", "dedup", "settle", "round_end", "loop"};
     for (int r = 1; r <= std::min(rounds, kTraceRounds - 1); r++) {
         const unsigned long long* p = &t[(size_t)r * kTracePhases];
         if (!p[0]) continue;
         std::fprintf(stderr, "[rb trace] round %2d:", r);
-        const unsigned long long end = (r + 1 < kTraceRounds && t[(size_t)(r + 1) * kTracePhases]) ?
-                                       t[(size_t)(r + 1) * kTracePhases] : p[5];
-        for (int k = 0; k < 5; k++) {
-            const unsigned long long b = k < 4 ? p[k + 1] : end;
-            if (p[k] && b >= p[k]) std::fprintf(stderr, " %s %.1f us", names[k], (b - p[k]) * 1e-3);
+        const unsigned long long nxt = r + 1 < kTraceRounds ? t[(size_t)(r + 1) * kTracePhases] : 0;
+        for (int k = 0; k < 7; k++) {
+            const unsigned long long b = k < 6 ? p[k + 1] : nxt;
+            if (p[k] && b >= p[k]) std::fprintf(stderr, " %s %.1f", names[k], (b - p[k]) * 1e-3);
         }
+        std::fprintf(stderr, " us");
         std::fprintf(stderr, "\n");
     }
     ck(cudaMemset(h->d_trace, 0, t.size() * 8), "trace clear");
@@ -968,12 +1075,17 @@ static void release_all(rb_handle* h) {
     fr(h->W.fh);
     fr(h->W.flags);
     fr(h->d_trace);
+    fr(h->d_bar);
     if (h->st) cudaStreamSynchronize(h->st);  // frees are stream-ordered; the pool is shared
     h->pool = nullptr;
     graph_release(h);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     if (h->h_state) cudaFreeHost(h->h_state);
     h->h_state = nullptr;
+    for (void* p : {(void*)h->hx, (void*)h->hx_stats, (void*)h->hx_lo, (void*)h->hx_hi, (void*)h->hx_c, (void*)h->hx_u})
+        if (p) cudaFreeHost(p);
+    h->hx = nullptr;
+    h->hx_stats = nullptr;
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     if (h->st) cudaStreamDestroy(h->st);
@@ -983,15 +1095,55 @@ static void release_all(rb_handle* h) {
 // canonical order of F[cur] rows [0, N) -> result buffers (row-major)
 constexpr int64_t kHostSortRows = 16384;
 
+// canonical order of N row-major rows on the host -> hr_* result arrays
+static void sort_on_host(rb_handle* h, int64_t N, const double* lo, const double* hi, const uint8_t* c,
+                         const uint8_t* u) {
+    const int n = h->n;
+    std::vector<int64_t> ord(N);
+    std::iota(ord.begin(), ord.end(), 0);
+    // np.lexsort keys: lo_0..lo_{n-1}, then hi_0..hi_{n-1} (_batch.py:244-250); stable
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+        for (int j = 0; j < n; j++) {
+            const double x = lo[a * n + j], y = lo[b * n + j];
+            if (x < y) return true;
+            if (y < x) return false;
+        }
+        for (int j = 0; j < n; j++) {
+            const double x = hi[a * n + j], y = hi[b * n + j];
+            if (x < y) return true;
+            if (y < x) return false;
+        }
+        return false;
+    });
+    h->hr_lo.resize((size_t)N * n);
+    h->hr_hi.resize((size_t)N * n);
+    h->hr_cert.resize(N);
+    h->hr_uns.resize(N);
+    for (int64_t r = 0; r < N; r++) {
+        std::memcpy(&h->hr_lo[r * n], &lo[ord[r] * n], sizeof(double) * n);
+        std::memcpy(&h->hr_hi[r * n], &hi[ord[r] * n], sizeof(double) * n);
+        h->hr_cert[r] = c[ord[r]];
+        h->hr_uns[r] = u[ord[r]];
+    }
+    h->r_n = N;
+    h->r_on_host = true;
+    h->r_ready = true;
+}
+
 static void finalize_sorted(rb_handle* h) {
     const int n = h->n;
     const int64_t N = h->n_cur;
     Front f = h->F[h->cur].f;
-    dalloc(&h->r_lo, (size_t)std::max<int64_t>(N, 1) * n);
-    dalloc(&h->r_hi, (size_t)std::max<int64_t>(N, 1) * n);
-    dalloc(&h->r_cert, (size_t)std::max<int64_t>(N, 1));
-    dalloc(&h->r_uns, (size_t)std::max<int64_t>(N, 1));
+    if (h->cap_r < std::max<int64_t>(N, 1)) {
+        const int64_t cap = grow_cap(std::max<int64_t>(N, 1));
+        dalloc(&h->r_lo, (size_t)cap * n);
+        dalloc(&h->r_hi, (size_t)cap * n);
+        dalloc(&h->r_cert, (size_t)cap);
+        dalloc(&h->r_uns, (size_t)cap);
+        h->cap_r = cap;
+    }
     h->r_n = N;
+    h->r_ready = true;
     h->r_on_host = false;
     if (N == 0) return;
     if (N <= kHostSortRows) {
@@ -1001,40 +1153,12 @@ static void finalize_sorted(rb_handle* h) {
         k_gather_rows<<<grid_for(N, 256, h->sms * 8), 256, 0, h->st>>>(f, n, N, nullptr, h->r_lo, h->r_hi,
                                                                         h->r_cert, h->r_uns);
         ck(cudaGetLastError(), "gather");
-        std::vector<double> lo((size_t)N * n), hi((size_t)N * n);
-        std::vector<uint8_t> c(N), u(N);
-        ck(cudaMemcpyAsync(lo.data(), h->r_lo, sizeof(double) * N * n, cudaMemcpyDeviceToHost, h->st), "d2h");
-        ck(cudaMemcpyAsync(hi.data(), h->r_hi, sizeof(double) * N * n, cudaMemcpyDeviceToHost, h->st), "d2h");
-        ck(cudaMemcpyAsync(c.data(), h->r_cert, N, cudaMemcpyDeviceToHost, h->st), "d2h");
-        ck(cudaMemcpyAsync(u.data(), h->r_uns, N, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaMemcpyAsync(h->hx_lo, h->r_lo, sizeof(double) * N * n, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaMemcpyAsync(h->hx_hi, h->r_hi, sizeof(double) * N * n, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaMemcpyAsync(h->hx_c, h->r_cert, N, cudaMemcpyDeviceToHost, h->st), "d2h");
+        ck(cudaMemcpyAsync(h->hx_u, h->r_uns, N, cudaMemcpyDeviceToHost, h->st), "d2h");
         ck(cudaStreamSynchronize(h->st), "finalize sync");
-        std::vector<int64_t> ord(N);
-        std::iota(ord.begin(), ord.end(), 0);
-        // np.lexsort keys: lo_0..lo_{n-1}, then hi_0..hi_{n-1} (_batch.py:244-250); stable
-        std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
-            for (int j = 0; j < n; j++) {
-                const double x = lo[a * n + j], y = lo[b * n + j];
-                if (x < y) return true;
-                if (y < x) return false;
-            }
-            for (int j = 0; j < n; j++) {
-                const double x = hi[a * n + j], y = hi[b * n + j];
-                if (x < y) return true;
-                if (y < x) return false;
-            }
-            return false;
-        });
-        h->hr_lo.resize((size_t)N * n);
-        h->hr_hi.resize((size_t)N * n);
-        h->hr_cert.resize(N);
-        h->hr_uns.resize(N);
-        for (int64_t r = 0; r < N; r++) {
-            std::memcpy(&h->hr_lo[r * n], &lo[ord[r] * n], sizeof(double) * n);
-            std::memcpy(&h->hr_hi[r * n], &hi[ord[r] * n], sizeof(double) * n);
-            h->hr_cert[r] = c[ord[r]];
-            h->hr_uns[r] = u[ord[r]];
-        }
-        h->r_on_host = true;
+        sort_on_host(h, N, h->hx_lo, h->hx_hi, h->hx_c, h->hx_u);
         return;
     }
     const unsigned* perm = nullptr;
@@ -1092,7 +1216,6 @@ static int64_t graph_small_cap(int n) {
     return std::min<int64_t>(std::max<int64_t>(c, (int64_t)1 << 16), (int64_t)1 << 18);
 }
 
-__global__ void k_state_start(DevState* st) { st->t_round_ns = gtimer(); }
 
 
 static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int64_t scap,
@@ -1103,14 +1226,41 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     ck(cudaGraphCreate(&g, 0), "graph create");
     cudaGraphConditionalHandle hw;
     ck(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault), "cond handle");
+    // top level: k_solve_start -> WHILE(round) -> k_solve_finish
+    ck(cudaStreamBeginCaptureToGraph(h->st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+       "begin capture");
+    {
+        InitBox box{};
+        for (int j = 0; j < n; j++) {
+            box.lo[j] = h->init_lo[j];
+            box.hi[j] = h->init_hi[j];
+        }
+        k_solve_start<<<1, 32, 0, h->st>>>(h->d_state, h->hx_dev, h->F[0].f, h->d_ctr, h->d_order, box, n);
+        ck(cudaGetLastError(), "start launch");
+    }
+    if (h->use_mk) dispatch_n<SmallRoundsK>(n, h, prm, dedup, scap, hw);
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaGraph_t cg = nullptr;
+    ck(cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &cg, &deps, &ndeps), "capture info");
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = hw;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
     cudaGraphNode_t node;
-    ck(cudaGraphAddNode(&node, g, nullptr, 0, &cp), "while node");
+    ck(cudaGraphAddNode(&node, cg, deps, ndeps, &cp), "while node");
+    ck(cudaStreamUpdateCaptureDependencies(h->st, &node, 1, cudaStreamSetCaptureDependencies), "capture deps");
     cudaGraph_t body = cp.conditional.phGraph_out[0];
+    k_solve_finish<<<grid_for(kHostSortRows, 256, h->sms * 4), 256, 0, h->st>>>(
+        h->d_state, h->d_rstats, h->d_order, h->hx_dev, h->hx_stats_dev, h->F[0].f, n, (long long)kHostSortRows,
+        h->hx_lo_dev, h->hx_hi_dev, h->hx_c_dev, h->hx_u_dev);
+    ck(cudaGetLastError(), "finish launch");
+    {
+        cudaGraph_t top = nullptr;
+        ck(cudaStreamEndCapture(h->st, &top), "end capture");
+    }
     ck(cudaStreamBeginCaptureToGraph(h->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
        "begin capture");
     const int64_t l0 = h->launches;
@@ -1126,11 +1276,10 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     p.st = h->d_state;
     launch_hs_batches(h, scap, 0, p, nullptr);
     stamp(h, h->d_state, 0, 3);
-    if (dedup) dispatch_n<DedupK>(n, h, h->F[1].f, h->F[0].f);
+    if (dedup) dispatch_n<DedupInsertK>(n, h, h->F[1].f);
     stamp(h, h->d_state, 0, 4);
-    dispatch_n<SettleK>(n, h, std::min<int64_t>(fcap, 3 * scap));
-    h->launches++;
-    k_round_end<<<1, 32, 0, h->st>>>(h->d_state, h->d_ctr, h->d_rstats, n, scap, hw, h->d_order, h->meta);
+    dispatch_n<TailK>(n, h, dedup, std::min<int64_t>(fcap, 3 * scap), scap, hw);
+    stamp(h, h->d_state, 0, 6, -1);
     h->launches++;
     cudaGraph_t captured = nullptr;
     ck(cudaStreamEndCapture(h->st, &captured), "end capture");
@@ -1156,6 +1305,14 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         dalloc(&h->d_rstats, (size_t)cfg->max_rounds);
         h->cap_rstats = cfg->max_rounds;
     }
+    if (h->cap_hx_stats < cfg->max_rounds) {
+        if (h->hx_stats) ck(cudaFreeHost(h->hx_stats), "free mapped stats");
+        h->hx_stats = nullptr;
+        ck(cudaHostAlloc((void**)&h->hx_stats, sizeof(DevRoundStats) * cfg->max_rounds, cudaHostAllocMapped),
+           "mapped stats");
+        ck(cudaHostGetDevicePointer((void**)&h->hx_stats_dev, h->hx_stats, 0), "mapped ptr");
+        h->cap_hx_stats = cfg->max_rounds;
+    }
     if (!h->d_state) dalloc(&h->d_state, 1);
     HsParams prm{};
     prm.hs_mode = 0;
@@ -1177,53 +1334,54 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         (uintptr_t)prm.hs_possible, (uintptr_t)hw_bits, (uintptr_t)prm.contract_output,
         (uintptr_t)(h->use_ftab ? 1 : 0), (uintptr_t)(h->hs_fused ? 1 : 0), (uintptr_t)h->fused_rows};
     key.push_back((uintptr_t)h->hs_cond);
+    key.push_back((uintptr_t)h->use_mk);
+    key.push_back((uintptr_t)h->mk_cap);
+    key.push_back((uintptr_t)h->mk_bps);
+    key.push_back((uintptr_t)h->hx_stats_dev);
+    key.push_back((uintptr_t)h->pdl);
     key.push_back((uintptr_t)h->trace);
     if (key != h->graph_key || !h->graph_exec) build_round_graph(h, prm, dedup, scap, key);
     DevState st{};
-    st.n_cur = (unsigned long long)h->n_cur;
+    st.n_cur = 1;
     st.target = target;
     st.max_boxes = cfg->max_boxes;
-    st.round_no = (int)h->stats.size() + 1;
+    st.round_no = 1;
     st.max_rounds = cfg->max_rounds;
     st.status = RB_BUDGET_EXHAUSTED;
-    *h->h_state = st;
-    ck(cudaMemcpyAsync(h->d_state, h->h_state, sizeof(DevState), cudaMemcpyHostToDevice, h->st), "state h2d");
-    ck(cudaMemsetAsync(h->d_ctr, 0, sizeof(Counters), h->st), "ctr memset");
-    k_state_start<<<1, 1, 0, h->st>>>(h->d_state);
+    HostX& X = *h->hx;
+    X.start = st;
+    X.rows = -1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
     ck(cudaGraphLaunch(h->graph_exec, h->st), "graph launch");
-    ck(cudaMemcpyAsync(h->h_state, h->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, h->st), "state d2h");
     ck(cudaStreamSynchronize(h->st), "graph sync");
-    const DevState& r = *h->h_state;
+    const DevState r = X.state;
     const int first = (int)h->stats.size();
     const int nr = r.nrounds - first;
-    if (nr > 0) {
-        std::vector<DevRoundStats> rs(nr);
-        ck(cudaMemcpy(rs.data(), h->d_rstats + first, sizeof(DevRoundStats) * nr, cudaMemcpyDeviceToHost),
-           "stats d2h");
-        for (const auto& x : rs) {
-            rb_round_stats o{};
-            o.round = (int32_t)x.round;
-            o.hs_on = (int32_t)x.hs_on;
-            o.boxes_in = x.boxes_in;
-            o.boxes_after_filter = x.after_filter;
-            o.boxes_after_hs = x.after_hs;
-            o.width = x.width;
-            o.elapsed_seconds = x.elapsed;
-            o.children = x.children;
-            o.hs_calls = x.hs_calls;
-            o.filter_ops = x.filter_ops;
-            o.hs_ops = x.hs_ops;
-            o.dups = x.dups;
-            o.exact_boxes = x.exact;
-            o.attempts = 1;
-            o.classify_bytes = x.boxes_in * (16 * n + 2) + (x.after_filter - 0) * 0;
-            h->stats.push_back(o);
-        }
-        h->launches += (int64_t)nr * h->graph_launches_per_round + 3;
+    for (int i = 0; i < nr; i++) {
+        const DevRoundStats& x = h->hx_stats[first + i];
+        rb_round_stats o{};
+        o.round = (int32_t)x.round;
+        o.hs_on = (int32_t)x.hs_on;
+        o.boxes_in = x.boxes_in;
+        o.boxes_after_filter = x.after_filter;
+        o.boxes_after_hs = x.after_hs;
+        o.width = x.width;
+        o.elapsed_seconds = x.elapsed;
+        o.children = x.children;
+        o.hs_calls = x.hs_calls;
+        o.filter_ops = x.filter_ops;
+        o.hs_ops = x.hs_ops;
+        o.dups = x.dups;
+        o.exact_boxes = x.exact;
+        o.attempts = 1;
+        o.classify_bytes = x.boxes_in * (16 * n + 2);
+        h->stats.push_back(o);
     }
+    h->launches += (int64_t)nr * h->graph_launches_per_round + 2;
     h->cur = 0;
     h->n_cur = (int64_t)r.n_cur;
-    ck(cudaMemcpy(h->h_order, h->d_order, sizeof(h->h_order), cudaMemcpyDeviceToHost), "order d2h");
+    for (int k = 0; k < 16; k++) h->h_order[k] = X.order[k];
+    if (r.done && X.rows >= 0) sort_on_host(h, X.rows, h->hx_lo, h->hx_hi, h->hx_c, h->hx_u);
     if (r.done) *status = r.status;
     return r.done != 0;
 }
@@ -1232,17 +1390,18 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
     const int n = h->n;
     const double t_start = now_s();
     h->launches = 0;
-    reset_order(h);
     ck(cudaEventRecord(h->ev[5], h->st), "ev start");
     h->stats.clear();
     h->have_result = false;
+    h->r_ready = false;
     if (cfg->max_rounds < 1) throw ArgError{RB_ERR_ARG, "max_rounds must be at least 1"};
     if (cfg->max_boxes < 1) throw ArgError{RB_ERR_ARG, "max_boxes must be at least 1"};
-    // initial frontier = the initial box (bnb.py:229-232): strided H2D into column 0
     h->cur = 0;
     h->n_cur = 0;
     fronts_reserve(h, 4096);
-    {
+    // initial frontier = the initial box (bnb.py:229-232); the device round loop writes it itself
+    auto host_init = [&]() {
+        reset_order(h);
         Front f = h->F[0].f;
         ck(cudaMemcpy2DAsync(f.lo, f.cap * sizeof(double), h->init_lo.data(), sizeof(double), sizeof(double), n,
                              cudaMemcpyHostToDevice, h->st), "init lo");
@@ -1250,7 +1409,7 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
                              cudaMemcpyHostToDevice, h->st), "init hi");
         ck(cudaMemsetAsync(f.cert, 0, 1, h->st), "init cert");
         ck(cudaMemsetAsync(f.unsplit, 0, 1, h->st), "init uns");
-    }
+    };
     h->n_cur = 1;
     double init_width = 0.0;
     for (int j = 0; j < n; j++) {
@@ -1264,10 +1423,13 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
     int status = RB_BUDGET_EXHAUSTED;
     bool finished = false;
     if (init_width <= target) {
+        host_init();
         status = RB_WIDTH_REACHED;
         finished = true;
     } else if (h->use_graph && !has_max_seconds) {
         finished = graph_rounds(h, cfg, target, hs_possible, &status);
+    } else {
+        host_init();
     }
     if (!finished) {
         for (int round_no = (int)h->stats.size() + 1; round_no <= cfg->max_rounds; round_no++) {
@@ -1323,7 +1485,7 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
             }
         }
     }
-    finalize_sorted(h);
+    if (!h->r_ready) finalize_sorted(h);
     trace_report(h, (int)h->stats.size());
     ck(cudaEventRecord(h->ev[6], h->st), "ev end");
     ck(cudaEventSynchronize(h->ev[6]), "ev sync");
@@ -1442,6 +1604,8 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
         h->mem_budget = (size_t)(0.80 * (double)free_b);
         dalloc(&h->d_ctr, 1);
+        dalloc(&h->d_bar, 2);
+        ck(cudaMemsetAsync(h->d_bar, 0, 2 * sizeof(unsigned), h->st), "barrier clear");
         if (h->trace) {
             dalloc(&h->d_trace, (size_t)kTraceRounds * kTracePhases);
             ck(cudaMemsetAsync(h->d_trace, 0, (size_t)kTraceRounds * kTracePhases * 8, h->st), "trace clear");
@@ -1450,6 +1614,16 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         reset_order(h);
         ck(cudaMallocHost((void**)&h->h_ctr, sizeof(Counters)), "pinned ctr");
         ck(cudaMallocHost((void**)&h->h_state, sizeof(DevState)), "pinned state");
+        ck(cudaHostAlloc((void**)&h->hx, sizeof(HostX), cudaHostAllocMapped), "mapped hx");
+        ck(cudaHostGetDevicePointer((void**)&h->hx_dev, h->hx, 0), "mapped hx ptr");
+        ck(cudaHostAlloc((void**)&h->hx_lo, sizeof(double) * kHostSortRows * h->n, cudaHostAllocMapped), "mapped lo");
+        ck(cudaHostAlloc((void**)&h->hx_hi, sizeof(double) * kHostSortRows * h->n, cudaHostAllocMapped), "mapped hi");
+        ck(cudaHostAlloc((void**)&h->hx_c, kHostSortRows, cudaHostAllocMapped), "mapped cert");
+        ck(cudaHostAlloc((void**)&h->hx_u, kHostSortRows, cudaHostAllocMapped), "mapped unsplit");
+        ck(cudaHostGetDevicePointer((void**)&h->hx_lo_dev, h->hx_lo, 0), "mapped ptr");
+        ck(cudaHostGetDevicePointer((void**)&h->hx_hi_dev, h->hx_hi, 0), "mapped ptr");
+        ck(cudaHostGetDevicePointer((void**)&h->hx_c_dev, h->hx_c, 0), "mapped ptr");
+        ck(cudaHostGetDevicePointer((void**)&h->hx_u_dev, h->hx_u, 0), "mapped ptr");
         dispatch_n<SetupK>(h->n, h);
         *out = h;
         return RB_OK;
@@ -1914,6 +2088,22 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     if (k == "hs_fused") {  // 0: eval/lin/sweep only, 1: by batch size, 2: fused only
         h->hs_fused = value != 0 && h->fused_smem <= (size_t)h->smem_optin;
         h->fused_rows = value == 2 ? INT64_MAX : (int64_t)h->sms * 80;
+        return RB_OK;
+    }
+    if (k == "pdl") {
+        h->pdl = value != 0;
+        return RB_OK;
+    }
+    if (k == "small_rounds") {
+        h->use_mk = value != 0 && h->mk_blocks_per_sm > 0;
+        return RB_OK;
+    }
+    if (k == "mk_bps") {
+        h->mk_bps = (int)std::max<int64_t>(1, value);
+        return RB_OK;
+    }
+    if (k == "mk_cap") {
+        h->mk_cap = value;
         return RB_OK;
     }
     if (k == "hs_cond") {

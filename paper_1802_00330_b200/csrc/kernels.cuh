@@ -13,6 +13,7 @@
 //   lo[j * cap + row], hi[j * cap + row] (float64), cert[row], unsplit[row] (u8).
 // Consecutive threads touch consecutive rows -> fully coalesced 8-byte lanes.
 #pragma once
+#include <climits>
 #include <cstdint>
 #include "interval.cuh"
 
@@ -220,13 +221,24 @@ struct Counters {
     unsigned long long dups;
     unsigned long long hs_on;
     unsigned long long n_compact;
-    unsigned long long pad[3];
+    unsigned long long tail_done;    // k_round_tail: blocks finished (last one runs the round end)
+    unsigned long long pad[2];
     // per-equation filter statistics (evaluations, rejections): the next round
     // evaluates the equations in descending rejections-per-op order.  Any order
     // gives the same survivor set -- a child is kept iff every equation encloses 0.
     unsigned long long f_eval[16];
     unsigned long long f_rej[16];
 };
+
+// Programmatic dependent launch: round-path kernels are launched with programmatic
+// stream serialization, so a kernel's blocks may start while its predecessor drains.
+// Every such kernel releases its successor at once and then waits for the full
+// completion (and memory visibility) of its predecessor before touching global
+// data; because every kernel of the chain waits, completion stays transitive.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
@@ -281,6 +293,8 @@ struct DevState {
     int done, bail, status, nrounds;
     int n_small_log2;           // bail when n_cur << n exceeds S capacity
     unsigned long long t_round_ns;
+    int cur;                    // k_small_rounds: frontier in F[cur] (0 whenever it exits)
+    int pad_;
 };
 
 struct DevRoundStats {
@@ -301,7 +315,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // their flags (degenerate -> cert 0, unsplit 1); the rest become parents.
 // Parent entries carry the filter guard verdict in bit 31 (1 = exact path).
 template <int N>
-__global__ void __launch_bounds__(256) k_classify(TabMeta meta, Front cur, int64_t n_cur_arg, Front next,
+__device__ __forceinline__ void k_classify_body(TabMeta meta, Front cur, int64_t n_cur_arg, Front next,
                                                   uint32_t* parents, Counters* ctr, double target_arg,
                                                   const DevState* st) {
     const int64_t n_cur = st ? (int64_t)st->n_cur : n_cur_arg;
@@ -368,9 +382,18 @@ __global__ void __launch_bounds__(256) k_classify(TabMeta meta, Front cur, int64
     }
 }
 
+template <int N>
+__global__ void __launch_bounds__(256) k_classify(TabMeta meta, Front cur, int64_t n_cur_arg, Front next,
+                                                  uint32_t* parents, Counters* ctr, double target_arg,
+                                                  const DevState* st) {
+    pdl_enter();
+    k_classify_body<N>(meta, cur, n_cur_arg, next, parents, ctr, target_arg, st);
+}
+
 // Parents for the rb_filter test hook: every row is a parent (no degeneracy split).
 template <int N>
 __global__ void k_all_parents(TabMeta meta, Front cur, int64_t n_cur, uint32_t* parents, Counters* ctr) {
+    pdl_enter();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_cur;
          i += (int64_t)gridDim.x * blockDim.x) {
         ExpRange r;
@@ -487,7 +510,7 @@ __host__ __device__ inline int filter_off_xs(const TabMeta& m) { return filter_o
 // warp ballot + one atomic per warp into S.  `tags` (test hook) receives the
 // child's global index p*2^n + c so the host can restore reference order.
 template <int N>
-__global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
+__device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                 const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
                                                 int64_t* tags, const int* __restrict__ eq_order) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -564,6 +587,14 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
         if (s_eval[threadIdx.x]) atomicAdd(&ctr->f_eval[threadIdx.x], (unsigned long long)s_eval[threadIdx.x]);
         if (s_rej[threadIdx.x]) atomicAdd(&ctr->f_rej[threadIdx.x], (unsigned long long)s_rej[threadIdx.x]);
     }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
+                                                const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
+                                                int64_t* tags, const int* __restrict__ eq_order) {
+    pdl_enter();
+    k_filter_body<N>(meta, gtab, cur, parents, ctr, S, tags, eq_order);
 }
 
 // Next round's equation order: descending rejections per algorithmic op, from
@@ -652,6 +683,7 @@ template <int N>
 __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                     const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
                                                     int64_t* tags, const int* __restrict__ eq_order) {
+    pdl_enter();
     using Sh = FtabShape<N>;
     __shared__ int s_order[16];
     __shared__ unsigned s_eval[16], s_rej[16];
@@ -897,6 +929,7 @@ template <int N>
 __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
                                                  int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
                                                  Front out, Counters* ctr, int64_t* tags, int R) {
+    pdl_enter();
     extern __shared__ __align__(16) uint8_t smem[];
     bool hs_on;
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
@@ -1180,6 +1213,7 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
 template <int N>
 __global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
                                                 Counters* ctr) {
+    pdl_enter();
     using L = LinLayout<N>;
     constexpr int G = L::G;
     extern __shared__ __align__(16) uint8_t smem[];
@@ -1214,6 +1248,7 @@ __global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_
 template <int N>
 __global__ void __launch_bounds__(128) k_krawczyk(SBuf S, int64_t b_end, int64_t b0, HsScratch W, Front out,
                                                   uint8_t* ok) {
+    pdl_enter();
     for (int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < b_end;
          b += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = b - b0;
@@ -1277,6 +1312,7 @@ __device__ __forceinline__ int div_extended_fast(ival p, ival y, ival& q0, ival&
 template <int N>
 __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm,
                                                   HsScratch W, Front out, Counters* ctr, int64_t* tags) {
+    pdl_enter();
     extern __shared__ __align__(16) uint8_t smem[];
     bool hs_on;
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
@@ -1475,7 +1511,7 @@ struct FusedLayout {
 __host__ __device__ inline int fused_off_tiles(const TabMeta& m) { return align16(stab_bytes(m, false)); }
 
 template <int N>
-__global__ void __launch_bounds__(128) k_hs_fused(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
+__device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
                                                   int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
                                                   int64_t* tags) {
     using L = FusedLayout<N>;
@@ -1695,6 +1731,14 @@ __global__ void __launch_bounds__(128) k_hs_fused(TabMeta meta, const uint8_t* _
     }
 }
 
+template <int N>
+__global__ void __launch_bounds__(128) k_hs_fused(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
+                                                  int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
+                                                  int64_t* tags) {
+    pdl_enter();
+    k_hs_fused_body<N>(meta, gtab, S, n_in_arg, prm, out, ctr, tags);
+}
+
 // ------------------------------------------------------------------ dedup
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
@@ -1744,7 +1788,7 @@ __device__ __forceinline__ bool round_ok(const Counters* c, int64_t s_cap, int64
 // is marked dead and ORs its flags into the keeper (dedup_sorted, _batch.py:253-266).
 // slot_of[i] records the occupied slot so k_dedup_finish can leave the table clean.
 template <int N>
-__global__ void k_dedup_insert(Front f, unsigned* table, unsigned long long mask, unsigned* slot_of, uint8_t* dead,
+__device__ __forceinline__ void k_dedup_insert_body(Front f, unsigned* table, unsigned long long mask, unsigned* slot_of, uint8_t* dead,
                                Counters* ctr, int64_t s_cap) {
     if (!round_ok(ctr, s_cap, f.cap)) return;
     const int64_t n = (int64_t)ctr->n_next;
@@ -1769,10 +1813,17 @@ __global__ void k_dedup_insert(Front f, unsigned* table, unsigned long long mask
     }
 }
 
+template <int N>
+__global__ void k_dedup_insert(Front f, unsigned* table, unsigned long long mask, unsigned* slot_of, uint8_t* dead,
+                               Counters* ctr, int64_t s_cap) {
+    pdl_enter();
+    k_dedup_insert_body<N>(f, table, mask, slot_of, dead, ctr, s_cap);
+}
+
 // Clear the used table slots; when duplicates were found, compact the live rows
 // into dst (counter ctr->n_compact).
 template <int N>
-__global__ void k_dedup_finish(Front src, Front dst, unsigned* table, const unsigned* slot_of, const uint8_t* dead,
+__device__ __forceinline__ void k_dedup_finish_body(Front src, Front dst, unsigned* table, const unsigned* slot_of, const uint8_t* dead,
                                Counters* ctr, int64_t s_cap) {
     if (!round_ok(ctr, s_cap, src.cap)) return;
     const int64_t n = (int64_t)ctr->n_next;
@@ -1795,12 +1846,20 @@ __global__ void k_dedup_finish(Front src, Front dst, unsigned* table, const unsi
     }
 }
 
+template <int N>
+__global__ void k_dedup_finish(Front src, Front dst, unsigned* table, const unsigned* slot_of, const uint8_t* dead,
+                               Counters* ctr, int64_t s_cap) {
+    pdl_enter();
+    k_dedup_finish_body<N>(src, dst, table, slot_of, dead, ctr, s_cap);
+}
+
 // ------------------------------------------------------------------ graph-mode round end
 
 // Bring the round's frontier back into F[0]: k_dedup_finish already compacted
 // into F[0] when duplicates were removed; otherwise copy F[1] -> F[0].
 template <int N>
 __global__ void k_settle(Front f1, Front f0, const Counters* ctr) {
+    pdl_enter();
     if (ctr->dups != 0) return;
     const int64_t n = (int64_t)ctr->n_next;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1816,9 +1875,9 @@ __global__ void k_settle(Front f1, Front f0, const Counters* ctr) {
 
 // Round statistics, termination (bnb.py:339-352) and the WHILE condition of the
 // device round loop; also clears the counters for the next round.
-__global__ void k_round_end(DevState* st, Counters* ctr, DevRoundStats* stats, int n, int64_t s_cap,
-                            cudaGraphConditionalHandle h_while, int* eq_order, TabMeta meta) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// One thread.  Returns true when the device loop should run another round.
+__device__ __noinline__ bool round_end_body(DevState* st, Counters* ctr, DevRoundStats* stats, int n, int64_t s_cap,
+                                            int* eq_order, const TabMeta& meta) {
     const Counters c = *ctr;
     filter_order(c.f_eval, c.f_rej, meta.cost_eq, n, eq_order);
     const unsigned long long after = c.n_next - c.dups;
@@ -1856,7 +1915,248 @@ __global__ void k_round_end(DevState* st, Counters* ctr, DevRoundStats* stats, i
     }
     unsigned long long* w = reinterpret_cast<unsigned long long*>(ctr);
     for (int i = 0; i < (int)(sizeof(Counters) / 8); i++) w[i] = 0ull;
-    cudaGraphSetConditional(h_while, (st->done || st->bail) ? 0u : 1u);
+    return !(st->done || st->bail);
+}
+
+__global__ void k_round_end(DevState* st, Counters* ctr, DevRoundStats* stats, int n, int64_t s_cap,
+                            cudaGraphConditionalHandle h_while, int* eq_order, TabMeta meta) {
+    pdl_enter();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const bool cont = round_end_body(st, ctr, stats, n, s_cap, eq_order, meta);
+    cudaGraphSetConditional(h_while, cont ? 1u : 0u);
+}
+
+// round_end_body by one warp (lane 0 of a warp, all 32 lanes present): the counters
+// are staged in shared memory with one coalesced load, the equation order is ranked
+// in parallel (the same stable descending sort as filter_order) and the counters
+// are cleared by all lanes.  Returns the WHILE condition (every lane).
+__device__ __noinline__ bool round_end_warp(DevState* st, Counters* ctr, DevRoundStats* stats, int n,
+                                            int64_t s_cap, int* eq_order, const TabMeta& meta) {
+    constexpr int W = (int)(sizeof(Counters) / 8);
+    __shared__ unsigned long long sc[W];
+    const int lane = threadIdx.x & 31;
+    unsigned long long* w = reinterpret_cast<unsigned long long*>(ctr);
+    for (int i = lane; i < W; i += 32) sc[i] = w[i];
+    const int cur_e = lane < n ? eq_order[lane] : 0;
+    const DevState s0 = *st;
+    __syncwarp();
+    const Counters& c = *reinterpret_cast<const Counters*>(sc);
+    // filter_order: key of the equation at position `lane`, rank = #greater + #equal before
+    double key = -1.0;
+    if (lane < n) {
+        const unsigned long long ev = c.f_eval[cur_e], rj = c.f_rej[cur_e];
+        const int ops = meta.cost_eq[cur_e];
+        key = ev ? ((double)rj / (double)ev) / (double)(ops > 0 ? ops : 1) : -1.0;
+    }
+    int rank = 0;
+    for (int b = 0; b < n; b++) {
+        const double kb = __shfl_sync(0xffffffffu, key, b);
+        rank += (kb > key) || (b < lane && kb == key);
+    }
+    if (lane < n) eq_order[rank] = cur_e;
+    for (int i = lane; i < W; i += 32) w[i] = 0ull;
+    int cont = 0;
+    if (lane == 0) {
+        const unsigned long long after = c.n_next - c.dups;
+        const double width = after ? __longlong_as_double((long long)c.wmax) : 0.0;
+        const unsigned long long now = gtimer();
+        DevRoundStats r;
+        r.round = s0.round_no;
+        r.boxes_in = (long long)s0.n_cur;
+        r.after_filter = (long long)(c.n_carried + c.n_surv);
+        r.after_hs = (long long)after;
+        r.children = (long long)(c.n_par << n);
+        r.hs_calls = (long long)c.hs_calls;
+        r.filter_ops = (long long)c.filter_ops;
+        r.hs_ops = (long long)c.hs_ops;
+        r.dups = (long long)c.dups;
+        r.exact = (long long)c.exact_boxes;
+        r.hs_on = (long long)c.hs_on;
+        r.width = width;
+        r.elapsed = (double)(now - s0.t_round_ns) * 1e-9;
+        stats[s0.round_no - 1] = r;
+        DevState s = s0;
+        s.t_round_ns = now;
+        s.n_cur = after;
+        s.nrounds = s0.round_no;
+        if (after == 0) {
+            s.done = 1;
+            s.status = 0;  // no_real_solution
+        } else if (width <= s0.target) {
+            s.done = 1;
+            s.status = 1;  // width_reached
+        } else if ((long long)after > s0.max_boxes || s0.round_no >= s0.max_rounds) {
+            s.done = 1;
+            s.status = 2;  // budget_exhausted
+        } else {
+            s.round_no += 1;
+            if ((after << n) > (unsigned long long)s_cap) s.bail = 1;  // next round needs the host
+        }
+        *st = s;
+        cont = !(s.done || s.bail);
+    }
+    return __shfl_sync(0xffffffffu, cont, 0) != 0;
+}
+
+// Graph-mode round tail: exact-dedup compaction (when k_dedup_insert found
+// duplicates) or plain copy of the round's frontier F[1] -> F[0], hash-table
+// cleanup, and -- in the last block to finish -- the round end.  One kernel
+// instead of dedup-finish + settle + round-end.
+template <int N>
+__global__ void __launch_bounds__(256) k_round_tail(Front f1, Front f0, unsigned* table, const unsigned* slot_of,
+                                                    const uint8_t* dead, int dedup, DevState* st, Counters* ctr,
+                                                    DevRoundStats* stats, int64_t s_cap,
+                                                    cudaGraphConditionalHandle h_while, int* eq_order,
+                                                    TabMeta meta) {
+    pdl_enter();
+    __shared__ int s_last;
+    const int64_t n = (int64_t)ctr->n_next;
+    const bool compact = dedup && ctr->dups != 0;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        if (dedup && i < n && slot_of[i] != 0xffffffffu) table[slot_of[i]] = 0u;
+        const bool live = i < n && !(compact && dead[i]);
+        const unsigned long long slot = compact ? warp_append(live, &ctr->n_compact) : (unsigned long long)i;
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                f0.lo[j * f0.cap + slot] = f1.lo[j * f1.cap + i];
+                f0.hi[j * f0.cap + slot] = f1.hi[j * f1.cap + i];
+            }
+            f0.cert[slot] = f1.cert[i];
+            f0.unsplit[slot] = f1.unsplit[i];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&ctr->tail_done, 1ull) == (unsigned long long)(gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x >= 32) return;
+    __threadfence();
+    const bool cont = round_end_warp(st, ctr, stats, N, s_cap, eq_order, meta);
+    if (threadIdx.x == 0) cudaGraphSetConditional(h_while, cont ? 1u : 0u);
+}
+
+// ------------------------------------------------------------------ persistent small rounds
+//
+// k_small_rounds runs whole rounds inside ONE resident grid while they are small
+// (n_cur * 2^n children <= mk_cap): classify, filter, fused HS, dedup and the round
+// end are the bodies of the per-phase kernels, separated by grid barriers instead
+// of kernel boundaries, and the frontier ping-pongs between F[0] and F[1] with no
+// copy.  Rounds are latency-bound at these sizes; a kernel boundary (~2 us launch
+// + drain, plus table reloads) costs more than the phase itself.  Launched
+// cooperatively, so every block is resident and the barrier cannot deadlock.
+
+struct SmallArgs {
+    TabMeta meta;
+    const uint8_t* gtab;
+    Front f0, f1;
+    SBuf S;
+    uint32_t* parents;
+    Counters* ctr;
+    DevState* st;
+    DevRoundStats* rstats;
+    int* order;
+    unsigned* table;
+    unsigned long long table_mask;
+    unsigned* slot_of;
+    uint8_t* dead;
+    HsParams prm;
+    unsigned* bar;               // {arrivals, generation}
+    long long mk_cap;            // run rounds here while n_cur << n <= mk_cap
+    long long graph_cap;         // then the WHILE loop while n_cur << n <= graph_cap
+    cudaGraphConditionalHandle h_while;
+    int dedup;                   // SolverConfig exact round dedup
+    unsigned long long* trace;   // RB_TRACE: phase timestamps [round][phase] (block 0)
+};
+
+__device__ __forceinline__ void mk_stamp(const SmallArgs& a, int round, int phase) {
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && round >= 0 && round < 256) a.trace[round * 8 + phase] = gtimer();
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) k_small_rounds(SmallArgs a) {
+    const volatile DevState* vs = a.st;
+    for (;;) {
+        if (vs->done || (((unsigned long long)vs->n_cur) << N) > (unsigned long long)a.mk_cap) break;
+        const int cur = vs->cur;
+        const int rno = vs->round_no;
+        const Front fc = cur ? a.f1 : a.f0, fn = cur ? a.f0 : a.f1;
+        mk_stamp(a, rno, 0);
+        k_classify_body<N>(a.meta, fc, 0, fn, a.parents, a.ctr, 0.0, a.st);
+        grid_barrier(a.bar);
+        mk_stamp(a, rno, 1);
+        k_filter_body<N>(a.meta, a.gtab, fc, a.parents, a.ctr, a.S, nullptr, a.order);
+        grid_barrier(a.bar);
+        mk_stamp(a, rno, 2);
+        HsParams p = a.prm;
+        p.count_from_ctr = 1;
+        p.st = a.st;
+        p.fused_max = LLONG_MAX;
+        p.has_cond = 0;
+        k_hs_fused_body<N>(a.meta, a.gtab, a.S, 0, p, fn, a.ctr, nullptr);
+        grid_barrier(a.bar);
+        mk_stamp(a, rno, 3);
+        if (a.dedup) {
+            k_dedup_insert_body<N>(fn, a.table, a.table_mask, a.slot_of, a.dead, a.ctr, a.S.cap);
+            grid_barrier(a.bar);
+            k_dedup_finish_body<N>(fn, fc, a.table, a.slot_of, a.dead, a.ctr, a.S.cap);
+            grid_barrier(a.bar);
+        }
+        mk_stamp(a, rno, 4);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            const bool dups = a.ctr->dups != 0;  // k_dedup_finish compacted back into fc
+            round_end_body(a.st, a.ctr, a.rstats, N, a.mk_cap, a.order, a.meta);
+            a.st->cur = dups ? cur : cur ^ 1;
+            a.st->bail = 0;  // the size test is at the loop head
+        }
+        mk_stamp(a, rno, 5);
+        grid_barrier(a.bar);
+        mk_stamp(a, rno, 6);
+    }
+    // leave the frontier in F[0] (the WHILE loop and the host expect it there)
+    if (vs->cur) {
+        const long long n = (long long)vs->n_cur;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                a.f0.lo[j * a.f0.cap + i] = a.f1.lo[j * a.f1.cap + i];
+                a.f0.hi[j * a.f0.cap + i] = a.f1.hi[j * a.f1.cap + i];
+            }
+            a.f0.cert[i] = a.f1.cert[i];
+            a.f0.unsplit[i] = a.f1.unsplit[i];
+        }
+        grid_barrier(a.bar);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        DevState* st = a.st;
+        st->cur = 0;
+        const bool cont = !st->done && ((st->n_cur << N) <= (unsigned long long)a.graph_cap);
+        st->bail = (!st->done && !cont) ? 1 : 0;
+        cudaGraphSetConditional(a.h_while, cont ? 1u : 0u);
+    }
 }
 
 // ------------------------------------------------------------------ sharding
@@ -1940,6 +2240,74 @@ __global__ void k_gather_rows(Front f, int n, int64_t N, const unsigned* perm, d
         }
         ocert[i] = f.cert[r];
         ouns[i] = f.unsplit[r];
+    }
+}
+
+// ------------------------------------------------------------------ graph prologue / epilogue
+//
+// A small solve is one graph launch: k_solve_start -> WHILE(rounds) -> k_solve_finish,
+// with the host reading everything back from mapped pinned memory after one sync.
+
+struct InitBox {
+    double lo[MAX_N], hi[MAX_N];
+};
+
+struct HostX {                  // pinned, mapped host memory shared with the graph
+    DevState start;             // host -> device: the state the solve starts from
+    DevState state;             // device -> host: state after the device rounds
+    int order[16];              // device -> host: filter equation order
+    long long rows;             // device -> host: rows gathered (-1: none)
+};
+
+// initial frontier = the initial box (bnb.py:229-232), device state, counters, filter order
+__global__ void k_solve_start(DevState* st, const HostX* hx, Front f0, Counters* ctr, int* order, InitBox box,
+                              int n) {
+    pdl_enter();
+    const int t = threadIdx.x;
+    if (t == 0) {
+        DevState s = hx->start;
+        s.t_round_ns = gtimer();
+        *st = s;
+    }
+    if (t < n) {
+        f0.lo[t * f0.cap] = box.lo[t];
+        f0.hi[t * f0.cap] = box.hi[t];
+    }
+    if (t == 0) {
+        f0.cert[0] = 0;
+        f0.unsplit[0] = 0;
+    }
+    if (t < 16) order[t] = t;
+    unsigned long long* w = reinterpret_cast<unsigned long long*>(ctr);
+    for (int i = t; i < (int)(sizeof(Counters) / 8); i += blockDim.x) w[i] = 0ull;
+}
+
+// final state, round statistics and order to the host; when the solve finished on the
+// device with at most max_rows boxes, also the boxes (row-major, unsorted)
+__global__ void k_solve_finish(const DevState* st, const DevRoundStats* rs, const int* order, HostX* hx,
+                               DevRoundStats* hstats, Front f0, int n, long long max_rows, double* hlo, double* hhi,
+                               uint8_t* hc, uint8_t* hu) {
+    pdl_enter();
+    const DevState s = *st;
+    const long long N = (long long)s.n_cur;
+    const bool gather = s.done && N <= max_rows;
+    if (blockIdx.x == 0) {
+        const int first = hx->start.round_no - 1;
+        for (int r = first + (int)threadIdx.x; r < s.nrounds; r += blockDim.x) hstats[r] = rs[r];
+        if (threadIdx.x < 16) hx->order[threadIdx.x] = order[threadIdx.x];
+        if (threadIdx.x == 0) {
+            hx->state = s;
+            hx->rows = gather ? N : -1;
+        }
+    }
+    if (!gather) return;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        for (int j = 0; j < n; j++) {
+            hlo[i * n + j] = canon0(f0.lo[j * f0.cap + i]);
+            hhi[i * n + j] = canon0(f0.hi[j * f0.cap + i]);
+        }
+        hc[i] = f0.cert[i];
+        hu[i] = f0.unsplit[i];
     }
 }
 
