@@ -11,179 +11,17 @@
 //   -> exact dedup (hash insert; compaction only when duplicates exist)
 //
 // so a round costs 3 kernel launches + 1-2 tiny syncs, independent of frontier size.
-#include <cub/cub.cuh>
-#include <nvtx3/nvToolsExt.h>
-
-#include <algorithm>
-#include <atomic>
-#include <chrono>
-#include <climits>
-#include <cmath>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <limits>
-#include <mutex>
-#include <numeric>
-#include <string>
-#include <vector>
-
-#include "../../include/rootbox_b200.h"
-#include "kernels.cuh"
-
-using namespace rb;
-
-#define RB_VERSION "rootbox_b200 0.1.0 (sm_100a)"
+#include "engine.cuh"
 
 namespace {
-
 std::string g_create_error;
-
-// Stream-ordered allocations from the handle's memory pool (memory is retained
-// across rounds and solves, so growth never stalls the device); set per API call.
-thread_local cudaMemPool_t t_pool = nullptr;
-thread_local cudaStream_t t_stream = nullptr;
-
-inline void dfree(void* p) {
-    if (!p) return;
-    if (t_pool) cudaFreeAsync(p, t_stream);
-    else cudaFree(p);
-}
-
-
-struct DevFront {
-    Front f{};
-    int n = 0;
-    void release() {
-        dfree(f.lo);
-        dfree(f.hi);
-        dfree(f.cert);
-        dfree(f.unsplit);
-        f = Front{};
-    }
-};
-
-struct CudaError {
-    cudaError_t e;
-    const char* what;
-};
-
-inline void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw CudaError{e, what};
-}
-
-struct ArgError {
-    int code;
-    std::string msg;
-};
-
 }  // namespace
 
-struct rb_handle {
-    std::mutex mu;
-    int dev = 0;
-    int n = 0;
-    int sms = 148;
-    cudaStream_t st = nullptr;
-    cudaMemPool_t pool = nullptr;
-    cudaEvent_t ev[8] = {};
-    int64_t launches = 0;
-    TabMeta meta{};
-    uint8_t* d_tab = nullptr;
-    std::vector<double> init_lo, init_hi;
-
-    DevFront F[2];
-    int cur = 0;
-    int64_t n_cur = 0;       // rows in F[cur]
-    uint32_t* parents = nullptr;
-    int64_t cap_par = 0;
-    SBuf S{};
-    Counters* d_ctr = nullptr;
-    Counters* h_ctr = nullptr;  // pinned
-    int64_t* d_tags = nullptr;
-    int64_t cap_tags = 0;
-    // dedup scratch (table kept all-zero between rounds)
-    unsigned* d_table = nullptr;
-    size_t table_slots = 0;
-    unsigned* d_slot = nullptr;
-    uint8_t* d_dead = nullptr;
-    int64_t cap_dead = 0;
-    // capacity prediction from the previous round
-    size_t mem_budget = 0;     // bytes the engine may hold
-    // sort scratch
-    void* d_cub = nullptr;
-    size_t cub_bytes = 0;
-    unsigned long long* d_keys[2] = {nullptr, nullptr};
-    unsigned* d_perm[2] = {nullptr, nullptr};
-    int64_t cap_sort = 0;
-    // result (device, row-major, canonical order)
-    double* r_lo = nullptr;
-    double* r_hi = nullptr;
-    uint8_t* r_cert = nullptr;
-    uint8_t* r_uns = nullptr;
-    int64_t r_n = 0;
-    bool r_on_host = false;  // small results are ordered on the host
-    bool r_ready = false;    // the result buffers already hold this solve's result
-    int64_t cap_r = 0;
-    // mapped pinned memory the round graph reads its start state from and writes back to
-    HostX* hx = nullptr;
-    HostX* hx_dev = nullptr;
-    DevRoundStats* hx_stats = nullptr;
-    DevRoundStats* hx_stats_dev = nullptr;
-    int cap_hx_stats = 0;
-    double *hx_lo = nullptr, *hx_hi = nullptr, *hx_lo_dev = nullptr, *hx_hi_dev = nullptr;
-    uint8_t *hx_c = nullptr, *hx_u = nullptr, *hx_c_dev = nullptr, *hx_u_dev = nullptr;
-    std::vector<double> hr_lo, hr_hi;
-    std::vector<uint8_t> hr_cert, hr_uns;
-    bool have_result = false;
-    std::vector<rb_round_stats> stats;
-    // adaptive filter equation order (device copy; host mirror for host-driven rounds)
-    int* d_order = nullptr;
-    int h_order[16] = {};
-    // device-resident round loop (CUDA graph with a WHILE node)
-    bool use_graph = true;
-    DevState* d_state = nullptr;
-    DevState* h_state = nullptr;  // pinned
-    DevRoundStats* d_rstats = nullptr;
-    int cap_rstats = 0;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t graph_exec = nullptr;
-    std::vector<uintptr_t> graph_key;
-    int64_t graph_launches_per_round = 0;
-    // sharded protocol state
-    double shard_target = 0.0;
-    int64_t shard_carried = 0;
-    int shard_round = 0;
-    int64_t shard_need_f = 0;
-    std::string err;
-    // launch shapes
-    int filter_threads = 256;
-    int hs_threads = 128;
-    int filter_blocks_per_sm = 1;
-    int eval_blocks_per_sm = 1, lin_blocks_per_sm = 1, sweep_blocks_per_sm = 1;
-    size_t filter_smem = 0, eval_smem = 0, lin_smem = 0, sweep_smem = 0, ftab_smem = 0;
-    int ftab_blocks_per_sm = 1;
-    bool use_ftab = true;
-    bool hs_fused = true;        // k_hs_fused (tile in shared memory) for small HS batches
-    int64_t fused_rows = 0;      // largest HS batch k_hs_fused takes (set from the SM count)
-    cudaStream_t st_side = nullptr;  // captures the IF branch of the round graph
-    bool hs_cond = true;
-    bool pdl = false;            // programmatic dependent launch between round kernels
-    bool use_mk = false;         // k_small_rounds (persistent grid) for the smallest rounds (experimental)
-    int64_t mk_cap = 1 << 16;    // ... while n_cur * 2^n <= mk_cap
-    size_t mk_smem = 0;
-    int mk_blocks_per_sm = 0;
-    int mk_bps = 1;              // blocks per SM of k_small_rounds
-    unsigned* d_bar = nullptr;         // graph: IF node around eval/lin/sweep (else they early-exit)
-    // RB_TRACE=1: device timestamps (%globaltimer) at the phase boundaries of every
-    // round, printed to stderr after each solve (a profiling aid; adds one tiny launch per phase)
-    bool trace = false;
-    unsigned long long* d_trace = nullptr;
-    size_t fused_smem = 0;
-    int fused_blocks_per_sm = 1;
-    HsScratch W{};
-    int smem_optin = 48 * 1024;
-};
+// launchers are instantiated in kinst.cu (one TU per few dimensions, built in parallel)
+#define RB_EXTERN(K) RB_LAUNCHERS(extern template struct, K)
+RB_EXTERN(1) RB_EXTERN(2) RB_EXTERN(3) RB_EXTERN(4) RB_EXTERN(5) RB_EXTERN(6) RB_EXTERN(7) RB_EXTERN(8)
+RB_EXTERN(9) RB_EXTERN(10) RB_EXTERN(11) RB_EXTERN(12) RB_EXTERN(13) RB_EXTERN(14) RB_EXTERN(15) RB_EXTERN(16)
+#undef RB_EXTERN
 
 // One stream-ordered memory pool per device for the whole process, retaining
 // its memory (release threshold = max): a new handle for the next system reuses
@@ -205,319 +43,7 @@ static cudaMemPool_t device_pool(int device) {
     return pools[device];
 }
 
-struct PoolScope {
-    explicit PoolScope(rb_handle* h) {
-        t_pool = h->pool;
-        t_stream = h->st;
-    }
-    ~PoolScope() {
-        t_pool = nullptr;
-        t_stream = nullptr;
-    }
-};
-
-// ---------------------------------------------------------------- dispatch on n
-
-template <template <int> class F, typename... Args>
-static void dispatch_n(int n, Args&&... args) {
-    switch (n) {
-#define RB_CASE(k) \
-    case k: F<k>::run(std::forward<Args>(args)...); break;
-        RB_CASE(1) RB_CASE(2) RB_CASE(3) RB_CASE(4) RB_CASE(5) RB_CASE(6) RB_CASE(7) RB_CASE(8)
-        RB_CASE(9) RB_CASE(10) RB_CASE(11) RB_CASE(12) RB_CASE(13) RB_CASE(14) RB_CASE(15) RB_CASE(16)
-#undef RB_CASE
-        default: throw ArgError{RB_ERR_LIMIT, "dimension out of range"};
-    }
-}
-
-static int grid_for(int64_t work, int threads, int max_blocks) {
-    int64_t b = (work + threads - 1) / threads;
-    if (b < 1) b = 1;
-    if (b > max_blocks) b = max_blocks;
-    return (int)b;
-}
-
-// dynamic shared memory limit = opt-in maximum minus the kernel's static shared memory
-template <typename K>
-static void set_max_dyn_smem(K kernel, int optin) {
-    cudaFuncAttributes fa;
-    ck(cudaFuncGetAttributes(&fa, kernel), "func attrs");
-    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes),
-       "attr");
-}
-
-template <int N>
-struct SetupK {
-    static void run(rb_handle* h) {
-        const int T = h->hs_threads;
-        h->filter_smem = filter_off_xs(h->meta) + (size_t)2 * N * h->filter_threads * sizeof(double);
-        h->eval_smem = stab_bytes(h->meta, false) + (size_t)3 * N * T * sizeof(double);
-        h->lin_smem = (size_t)(T / 32) * LinLayout<N>::BPW * LinLayout<N>::doubles * sizeof(double);
-        h->sweep_smem = (size_t)2 * N * T * sizeof(double);
-        if (h->meta.ftab) {
-            h->ftab_smem = ftab_smem_bytes<N>(h->meta);
-            if (h->ftab_smem > 160 * 1024) h->meta.ftab = 0;  // tables too large: direct evaluation
-        }
-        // the attribute is per kernel (shared by every handle of this n): set it to the opt-in maximum
-        const size_t mx = std::max({h->filter_smem, h->eval_smem, h->lin_smem, h->sweep_smem});
-        h->fused_smem = fused_off_tiles(h->meta) +
-                        (size_t)(T / 32) * FusedLayout<N>::BPW * FusedLayout<N>::doubles * sizeof(double);
-        if ((int)mx > h->smem_optin) throw ArgError{RB_ERR_LIMIT, "system tables exceed the shared-memory budget"};
-        set_max_dyn_smem(k_filter<N>, h->smem_optin);
-        set_max_dyn_smem(k_filter_tab<N>, h->smem_optin);
-        set_max_dyn_smem(k_hs_eval<N>, h->smem_optin);
-        set_max_dyn_smem(k_hs_lin<N>, h->smem_optin);
-        set_max_dyn_smem(k_hs_sweep<N>, h->smem_optin);
-        set_max_dyn_smem(k_hs_fused<N>, h->smem_optin);
-        if ((int)h->fused_smem > h->smem_optin) h->hs_fused = false;
-        int nb = 0;
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter<N>, h->filter_threads, h->filter_smem), "occ");
-        h->filter_blocks_per_sm = std::max(1, nb);
-        if (h->meta.ftab) {
-            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter_tab<N>, 256, h->ftab_smem), "occ");
-            h->ftab_blocks_per_sm = std::max(1, nb);
-        }
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_eval<N>, T, h->eval_smem), "occ");
-        h->eval_blocks_per_sm = std::max(1, nb);
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_lin<N>, T, h->lin_smem), "occ");
-        h->lin_blocks_per_sm = std::max(1, nb);
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_sweep<N>, T, h->sweep_smem), "occ");
-        h->sweep_blocks_per_sm = std::max(1, nb);
-        if (h->hs_fused) {
-            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_fused<N>, T, h->fused_smem), "occ");
-            h->fused_blocks_per_sm = std::max(1, nb);
-        }
-        // persistent small-round kernel: 256 threads, shared memory for its largest phase
-        h->mk_smem = std::max<size_t>(filter_off_xs(h->meta) + (size_t)2 * N * 256 * sizeof(double),
-                                      fused_off_tiles(h->meta) + (size_t)(256 / 32) * FusedLayout<N>::BPW *
-                                                                     FusedLayout<N>::doubles * sizeof(double));
-        h->mk_blocks_per_sm = 0;
-        if ((int)h->mk_smem <= h->smem_optin) {
-            set_max_dyn_smem(k_small_rounds<N>, h->smem_optin);
-            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_small_rounds<N>, 256, h->mk_smem), "occ");
-            h->mk_blocks_per_sm = nb;
-        }
-        if (h->mk_blocks_per_sm < 1) h->use_mk = false;
-    }
-};
-
-// Kernel launch on the handle's stream; with h->pdl the launch allows programmatic
-// dependent launch (the kernel's blocks start while the previous kernel drains and
-// wait in pdl_enter() for its completion).
-template <typename... KArgs, typename... Args>
-static void klaunch(rb_handle* h, void (*k)(KArgs...), int grid, int block, size_t smem, Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3((unsigned)block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = h->st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = h->pdl ? 1 : 0;
-    ck(cudaLaunchKernelEx(&cfg, k, args...), "kernel launch");
-}
-
-template <int N>
-struct ClassifyK {
-    static void run(rb_handle* h, double target, const DevState* st = nullptr, int64_t bound = -1) {
-        Front cur = h->F[h->cur].f, next = h->F[h->cur ^ 1].f;
-        const int blocks = grid_for(bound >= 0 ? bound : h->n_cur, 256, h->sms * 8);
-        h->launches++;
-        klaunch(h, k_classify<N>, blocks, 256, 0, h->meta, cur, h->n_cur, next, h->parents, h->d_ctr, target, st);
-        ck(cudaGetLastError(), "classify launch");
-    }
-};
-
-template <int N>
-struct AllParentsK {
-    static void run(rb_handle* h) {
-        const int blocks = grid_for(h->n_cur, 256, h->sms * 8);
-        h->launches++;
-        klaunch(h, k_all_parents<N>, blocks, 256, 0, h->meta, h->F[h->cur].f, h->n_cur, h->parents, h->d_ctr);
-        ck(cudaGetLastError(), "parents launch");
-    }
-};
-
-template <int N>
-struct FilterK {
-    static void run(rb_handle* h, int64_t max_parents, int64_t* tags) {
-        if (h->meta.ftab && h->use_ftab) {
-            using Sh = FtabShape<N>;
-            const int64_t units = N >= 8 ? (max_parents << Sh::CHLOG) : ((max_parents + Sh::PPB - 1) >> Sh::LOGPPB);
-            const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)h->sms * h->ftab_blocks_per_sm));
-            h->launches++;
-            klaunch(h, k_filter_tab<N>, blocks, 256, h->ftab_smem, h->meta, h->d_tab, h->F[h->cur].f, h->parents,
-                                                                 h->d_ctr, h->S, tags, h->d_order);
-            ck(cudaGetLastError(), "filter_tab launch");
-            return;
-        }
-        const int64_t work = max_parents << N;
-        const int blocks = grid_for(work, h->filter_threads, h->sms * h->filter_blocks_per_sm);
-        h->launches++;
-        klaunch(h, k_filter<N>, blocks, h->filter_threads, h->filter_smem, h->meta, h->d_tab, h->F[h->cur].f,
-                                                                         h->parents, h->d_ctr, h->S, tags, h->d_order);
-        ck(cudaGetLastError(), "filter launch");
-    }
-};
-
-// K2a + K2b + K2c over rows [b0, b0 + W.B) of S (n_in read on the device when prm.count_from_ctr)
-template <int N>
-struct HsK {
-    static void run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* tags, int64_t batch_bound) {
-        const int T = h->hs_threads;
-        const int64_t B = h->W.B;
-        Front out = h->F[h->cur ^ 1].f;
-        h->launches += 3;
-        // split each box's n^2 + n polynomials over R threads when the batch is small
-        const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(B, batch_bound));
-        const int64_t target = (int64_t)h->sms * 1024;
-        const int R = (int)std::max<int64_t>(1, std::min<int64_t>(N * N + N, (target + bound - 1) / bound));
-        klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
-            h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags, R);
-        klaunch(h, k_hs_lin<N>, grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem, h->S, n_in, b0, prm, h->W, h->d_ctr);
-        klaunch(h, k_hs_sweep<N>, grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem,
-            h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
-        ck(cudaGetLastError(), "hs launch");
-    }
-};
-
-// fused K2 over all n_in rows of S (n_in read on the device when prm.count_from_ctr); `bound`
-// is the most rows it can see, which sizes the grid
-template <int N>
-struct HsFusedK {
-    static void run(rb_handle* h, int64_t n_in, HsParams prm, int64_t* tags, int64_t bound) {
-        const int T = h->hs_threads;
-        h->launches++;
-        const int64_t lanes = std::max<int64_t>(1, bound) * FusedLayout<N>::G;
-        klaunch(h, k_hs_fused<N>, grid_for(lanes, T, h->sms * h->fused_blocks_per_sm), T, h->fused_smem,
-            h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
-        ck(cudaGetLastError(), "hs fused launch");
-    }
-};
-
-// K2a + K2b + Krawczyk over rows [b0, b_end) of S; results at the same rows of `out`
-template <int N>
-struct KrawczykK {
-    static void run(rb_handle* h, int64_t b0, int64_t b_end, Front out, uint8_t* ok) {
-        const int T = h->hs_threads;
-        const int64_t B = h->W.B;
-        HsParams prm{};
-        prm.hs_mode = 1;
-        h->launches += 3;
-        const int64_t bound = b_end - b0;
-        const int64_t target = (int64_t)h->sms * 1024;
-        const int R = (int)std::max<int64_t>(1, std::min<int64_t>(N * N + N, (target + bound - 1) / bound));
-        klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
-            h->meta, h->d_tab, h->S, b_end, b0, prm, h->W, out, h->d_ctr, nullptr, R);
-        klaunch(h, k_hs_lin<N>, grid_for(std::min(B, bound), (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem, h->S, b_end, b0, prm, h->W, h->d_ctr);
-        klaunch(h, k_krawczyk<N>, grid_for(bound, 128, h->sms * 16), 128, 0, h->S, b_end, b0, h->W, out, ok);
-        ck(cudaGetLastError(), "krawczyk launch");
-    }
-};
-
-// persistent small rounds (cooperative: every block resident for the grid barrier)
-template <int N>
-struct SmallRoundsK {
-    static void run(rb_handle* h, const HsParams& prm, bool dedup, int64_t scap, cudaGraphConditionalHandle hw) {
-        SmallArgs a{};
-        a.dedup = dedup ? 1 : 0;
-        a.trace = h->trace ? h->d_trace : nullptr;
-        a.meta = h->meta;
-        a.gtab = h->d_tab;
-        a.f0 = h->F[0].f;
-        a.f1 = h->F[1].f;
-        a.S = h->S;
-        a.parents = h->parents;
-        a.ctr = h->d_ctr;
-        a.st = h->d_state;
-        a.rstats = h->d_rstats;
-        a.order = h->d_order;
-        a.table = h->d_table;
-        a.table_mask = (unsigned long long)(h->table_slots - 1);
-        a.slot_of = h->d_slot;
-        a.dead = h->d_dead;
-        a.prm = prm;
-        a.bar = h->d_bar;
-        a.mk_cap = std::min<int64_t>(h->mk_cap, scap);
-        a.graph_cap = scap;
-        a.h_while = hw;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(h->sms * std::min(h->mk_blocks_per_sm, h->mk_bps)));
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = h->mk_smem;
-        cfg.stream = h->st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeCooperative;
-        at[0].val.cooperative = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        h->launches++;
-        ck(cudaLaunchKernelEx(&cfg, k_small_rounds<N>, a), "small rounds launch");
-    }
-};
-
-template <int N>
-struct DedupInsertK {
-    static void run(rb_handle* h, Front next) {
-        const int blocks = grid_for(next.cap, 256, h->sms * 8);
-        h->launches++;
-        klaunch(h, k_dedup_insert<N>, blocks, 256, 0, next, h->d_table, (unsigned long long)(h->table_slots - 1),
-                h->d_slot, h->d_dead, h->d_ctr, h->S.cap);
-    }
-};
-
-// dedup finish + F[1] -> F[0] + round end (graph mode)
-template <int N>
-struct TailK {
-    static void run(rb_handle* h, bool dedup, int64_t bound, int64_t scap, cudaGraphConditionalHandle hw) {
-        const int blocks = grid_for(bound, 256, h->sms * 2);
-        h->launches++;
-        klaunch(h, k_round_tail<N>, blocks, 256, 0, h->F[1].f, h->F[0].f, h->d_table, (const unsigned*)h->d_slot,
-                (const uint8_t*)h->d_dead, dedup ? 1 : 0, h->d_state, h->d_ctr, h->d_rstats, scap, hw, h->d_order,
-                h->meta);
-    }
-};
-
-template <int N>
-struct SettleK {
-    static void run(rb_handle* h, int64_t bound) {
-        klaunch(h, k_settle<N>, grid_for(bound, 256, h->sms * 8), 256, 0, h->F[1].f, h->F[0].f, h->d_ctr);
-        ck(cudaGetLastError(), "settle launch");
-    }
-};
-
-template <int N>
-struct DedupK {
-    static void run(rb_handle* h, Front next, Front other) {
-        // persistent grids: the row count is read on the device
-        const int blocks = grid_for(next.cap, 256, h->sms * 8);
-        h->launches += 2;
-        klaunch(h, k_dedup_insert<N>, blocks, 256, 0, next, h->d_table, (unsigned long long)(h->table_slots - 1),
-                                                     h->d_slot, h->d_dead, h->d_ctr, h->S.cap);
-        klaunch(h, k_dedup_finish<N>, blocks, 256, 0, next, other, h->d_table, h->d_slot, h->d_dead, h->d_ctr,
-                                                     h->S.cap);
-        ck(cudaGetLastError(), "dedup launch");
-    }
-};
-
 // ---------------------------------------------------------------- memory helpers
-
-template <typename T>
-static void dalloc(T** p, size_t count) {
-    if (*p) dfree(*p);
-    *p = nullptr;
-    if (count == 0) count = 1;
-    cudaError_t e = t_pool ? cudaMallocFromPoolAsync((void**)p, count * sizeof(T), t_pool, t_stream)
-                           : cudaMalloc((void**)p, count * sizeof(T));
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        *p = nullptr;
-        throw ArgError{RB_ERR_NOMEM, "device memory exhausted allocating " + std::to_string(count * sizeof(T)) +
-                                         " bytes"};
-    }
-}
 
 static int64_t grow_cap(int64_t need) {
     int64_t c = 4096;
@@ -1519,48 +1045,6 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
         (h)->err = ex.what();                                                              \
         return RB_ERR_CUDA;                                                                \
     }
-
-template <int N>
-struct PartitionK {
-    static void run(rb_handle* h, int world, int64_t* counts) {
-        const int64_t n = h->n_cur;
-        unsigned* owner = nullptr;
-        unsigned long long* cnt = nullptr;
-        dalloc(&owner, (size_t)std::max<int64_t>(n, 1));
-        dalloc(&cnt, (size_t)2 * world);
-        ck(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2 * world, h->st), "memset");
-        const int blocks = grid_for(n, 256, h->sms * 8);
-        h->launches += 2;
-        if (n > 0) k_owner_count<N><<<blocks, 256, 0, h->st>>>(h->F[h->cur].f, n, world, owner, cnt);
-        std::vector<unsigned long long> hc(2 * world);
-        ck(cudaMemcpyAsync(hc.data(), cnt, sizeof(unsigned long long) * world, cudaMemcpyDeviceToHost, h->st), "d2h");
-        ck(cudaStreamSynchronize(h->st), "sync");
-        unsigned long long off = 0;
-        for (int r = 0; r < world; r++) {
-            counts[r] = (int64_t)hc[r];
-            hc[world + r] = off;
-            off += hc[r];
-        }
-        ck(cudaMemcpyAsync(cnt + world, hc.data() + world, sizeof(unsigned long long) * world, cudaMemcpyHostToDevice,
-                           h->st), "h2d");
-        if (n > 0) k_owner_scatter<N><<<blocks, 256, 0, h->st>>>(h->F[h->cur].f, n, owner, cnt + world,
-                                                                h->F[h->cur ^ 1].f);
-        ck(cudaGetLastError(), "partition");
-        h->cur ^= 1;
-        dfree(owner);
-        dfree(cnt);
-        ck(cudaStreamSynchronize(h->st), "sync");
-    }
-};
-
-template <int N>
-struct WidthK {
-    static void run(rb_handle* h) {
-        h->launches++;
-        k_width<N><<<grid_for(h->n_cur, 256, h->sms * 8), 256, 0, h->st>>>(h->F[h->cur].f, h->n_cur, h->d_ctr);
-        ck(cudaGetLastError(), "width");
-    }
-};
 
 extern "C" {
 

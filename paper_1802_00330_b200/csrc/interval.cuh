@@ -132,7 +132,7 @@ struct Fast {
 
 // interval.py:98-108: Dekker product error by FMA-free Veltkamp splitting,
 // exactly as the reference computes it (NaN = "untrusted").
-__device__ __noinline__ double prod_err_ref(double a, double b, double p) {
+static __device__ __noinline__ double prod_err_ref(double a, double b, double p) {
     if (fabs(a) > RB_BIG || fabs(b) > RB_BIG || fabs(p) < RB_TINY) return CUDART_NAN;
     const double S = 134217729.0;
     double ah = __dmul_rn(S, a);
@@ -230,7 +230,7 @@ struct Exact {
 // ------------------------------------------------------------------ division (always exact)
 // interval.py:139-154
 
-__device__ __noinline__ double div_err_sign(double a, double b, double q) {
+static __device__ __noinline__ double div_err_sign(double a, double b, double q) {
     if (isinf(a) || isinf(b) || isinf(q)) return CUDART_NAN;
     double p = __dmul_rn(q, b);
     if (fabs(q) > RB_BIG || fabs(b) > RB_BIG || (p != 0.0 && fabs(p) < RB_TINY)) return CUDART_NAN;
@@ -242,7 +242,7 @@ __device__ __noinline__ double div_err_sign(double a, double b, double q) {
 }
 
 // interval.py:157-172
-__device__ __noinline__ double div_rd(double a, double b) {
+static __device__ __noinline__ double div_rd(double a, double b) {
     if (a == 0.0) return 0.0;
     if (isinf(a) && !isinf(b)) return ((a < 0) == (b < 0) || a > 0) ? a : -CUDART_INF;
     double q = __ddiv_rn(a, b);
@@ -255,7 +255,7 @@ __device__ __noinline__ double div_rd(double a, double b) {
 }
 
 // interval.py:175-190
-__device__ __noinline__ double div_ru(double a, double b) {
+static __device__ __noinline__ double div_ru(double a, double b) {
     if (a == 0.0) return 0.0;
     if (isinf(a) && !isinf(b)) return (a > 0 || (a < 0) == (b < 0)) ? a : CUDART_INF;
     double q = __ddiv_rn(a, b);

@@ -127,7 +127,7 @@ __device__ __forceinline__ ival eval_poly(const STab& t, int p, const double* xl
     return acc;
 }
 
-__device__ __noinline__ ival eval_poly_exact(const STab& t, int p, const double* xlo, const double* xhi,
+static __device__ __noinline__ ival eval_poly_exact(const STab& t, int p, const double* xlo, const double* xhi,
                                              int stride) {
     return eval_poly<Exact>(t, p, xlo, xhi, stride);
 }
@@ -164,7 +164,7 @@ __device__ __forceinline__ ival gmul(ival x, ival y) {
 enum { DIV_EMPTY = 0, DIV_SINGLE = 1, DIV_SPLIT = 2, DIV_WHOLE = 3 };
 
 // interval.py:394-432 (div_extended), Hanson/Kahan case table.
-__device__ __noinline__ int div_extended(ival x, ival y, ival& p0, ival& p1) {
+static __device__ __noinline__ int div_extended(ival x, ival y, ival& p0, ival& p1) {
     if (!contains_zero(y)) {
         ival r = mk(div_rd(1.0, y.hi), div_ru(1.0, y.lo));  // recip, interval.py:347-351
         p0 = gmul(x, r);  // guarded product: Fast when provably trusted
@@ -455,7 +455,7 @@ __device__ __forceinline__ ival eval_poly_packed(const TermP* tp, const STab& t,
     return acc;
 }
 
-__device__ __noinline__ ival eval_poly_packed_exact(const TermP* tp, const STab& t, int p, const double2* xs2,
+static __device__ __noinline__ ival eval_poly_packed_exact(const TermP* tp, const STab& t, int p, const double2* xs2,
                                                     int stride) {
     return eval_poly_packed<Exact>(tp, t, p, xs2, stride);
 }
@@ -674,7 +674,7 @@ __device__ __forceinline__ ival term_value(const STab& t, int q, int combo, cons
     return term;
 }
 
-__device__ __noinline__ ival term_value_exact(const STab& t, int q, int combo, const double* plo, const double* phi,
+static __device__ __noinline__ ival term_value_exact(const STab& t, int q, int combo, const double* plo, const double* phi,
                                               const double* pmid) {
     return term_value<Exact>(t, q, combo, plo, phi, pmid);
 }
@@ -1096,7 +1096,7 @@ __device__ __forceinline__ void lin_products(const double* Am, const ival* jcol,
 }
 
 template <int N>
-__device__ __noinline__ void lin_products_exact(const double* Am, const ival* jcol, int l, const LinSink& K,
+static __device__ __noinline__ void lin_products_exact(const double* Am, const ival* jcol, int l, const LinSink& K,
                                                 unsigned gmask) {
     lin_products<N, Exact>(Am, jcol, l, K, gmask);
 }
@@ -1876,7 +1876,7 @@ __global__ void k_settle(Front f1, Front f0, const Counters* ctr) {
 // Round statistics, termination (bnb.py:339-352) and the WHILE condition of the
 // device round loop; also clears the counters for the next round.
 // One thread.  Returns true when the device loop should run another round.
-__device__ __noinline__ bool round_end_body(DevState* st, Counters* ctr, DevRoundStats* stats, int n, int64_t s_cap,
+static __device__ __noinline__ bool round_end_body(DevState* st, Counters* ctr, DevRoundStats* stats, int n, int64_t s_cap,
                                             int* eq_order, const TabMeta& meta) {
     const Counters c = *ctr;
     filter_order(c.f_eval, c.f_rej, meta.cost_eq, n, eq_order);
@@ -1918,6 +1918,7 @@ __device__ __noinline__ bool round_end_body(DevState* st, Counters* ctr, DevRoun
     return !(st->done || st->bail);
 }
 
+#ifndef RB_KINST_TU
 __global__ void k_round_end(DevState* st, Counters* ctr, DevRoundStats* stats, int n, int64_t s_cap,
                             cudaGraphConditionalHandle h_while, int* eq_order, TabMeta meta) {
     pdl_enter();
@@ -1925,12 +1926,13 @@ __global__ void k_round_end(DevState* st, Counters* ctr, DevRoundStats* stats, i
     const bool cont = round_end_body(st, ctr, stats, n, s_cap, eq_order, meta);
     cudaGraphSetConditional(h_while, cont ? 1u : 0u);
 }
+#endif
 
 // round_end_body by one warp (lane 0 of a warp, all 32 lanes present): the counters
 // are staged in shared memory with one coalesced load, the equation order is ranked
 // in parallel (the same stable descending sort as filter_order) and the counters
 // are cleared by all lanes.  Returns the WHILE condition (every lane).
-__device__ __noinline__ bool round_end_warp(DevState* st, Counters* ctr, DevRoundStats* stats, int n,
+static __device__ __noinline__ bool round_end_warp(DevState* st, Counters* ctr, DevRoundStats* stats, int n,
                                             int64_t s_cap, int* eq_order, const TabMeta& meta) {
     constexpr int W = (int)(sizeof(Counters) / 8);
     __shared__ unsigned long long sc[W];
@@ -2216,6 +2218,7 @@ __device__ __forceinline__ unsigned long long order_key(double v) {
 }
 
 // key k of row perm[i]: k < n -> lo_k, else hi_{k-n}  (np.lexsort key order, _batch.py:247-249)
+#ifndef RB_KINST_TU
 __global__ void k_sort_keys(Front f, int n, int64_t N, int k, const unsigned* perm, unsigned long long* keys) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = perm ? perm[i] : i;
@@ -2223,13 +2226,17 @@ __global__ void k_sort_keys(Front f, int n, int64_t N, int k, const unsigned* pe
         keys[i] = order_key(v);
     }
 }
+#endif
 
+#ifndef RB_KINST_TU
 __global__ void k_iota(unsigned* p, int64_t N) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
         p[i] = (unsigned)i;
 }
+#endif
 
 // gather rows in perm order into row-major outputs
+#ifndef RB_KINST_TU
 __global__ void k_gather_rows(Front f, int n, int64_t N, const unsigned* perm, double* olo, double* ohi,
                               uint8_t* ocert, uint8_t* ouns) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
@@ -2242,6 +2249,7 @@ __global__ void k_gather_rows(Front f, int n, int64_t N, const unsigned* perm, d
         ouns[i] = f.unsplit[r];
     }
 }
+#endif
 
 // ------------------------------------------------------------------ graph prologue / epilogue
 //
@@ -2260,6 +2268,7 @@ struct HostX {                  // pinned, mapped host memory shared with the gr
 };
 
 // initial frontier = the initial box (bnb.py:229-232), device state, counters, filter order
+#ifndef RB_KINST_TU
 __global__ void k_solve_start(DevState* st, const HostX* hx, Front f0, Counters* ctr, int* order, InitBox box,
                               int n) {
     pdl_enter();
@@ -2281,9 +2290,11 @@ __global__ void k_solve_start(DevState* st, const HostX* hx, Front f0, Counters*
     unsigned long long* w = reinterpret_cast<unsigned long long*>(ctr);
     for (int i = t; i < (int)(sizeof(Counters) / 8); i += blockDim.x) w[i] = 0ull;
 }
+#endif
 
 // final state, round statistics and order to the host; when the solve finished on the
 // device with at most max_rows boxes, also the boxes (row-major, unsorted)
+#ifndef RB_KINST_TU
 __global__ void k_solve_finish(const DevState* st, const DevRoundStats* rs, const int* order, HostX* hx,
                                DevRoundStats* hstats, Front f0, int n, long long max_rows, double* hlo, double* hhi,
                                uint8_t* hc, uint8_t* hu) {
@@ -2310,8 +2321,10 @@ __global__ void k_solve_finish(const DevState* st, const DevRoundStats* rs, cons
         hu[i] = f0.unsplit[i];
     }
 }
+#endif
 
 // row-major (host layout) -> SoA frontier rows [off, off+N)
+#ifndef RB_KINST_TU
 __global__ void k_rows_to_soa(const double* rlo, const double* rhi, const uint8_t* rc, const uint8_t* ru, int n,
                               int64_t N, Front f, int64_t off) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
@@ -2323,5 +2336,6 @@ __global__ void k_rows_to_soa(const double* rlo, const double* rhi, const uint8_
         if (f.unsplit) f.unsplit[off + i] = ru ? ru[i] : 0;
     }
 }
+#endif
 
 }  // namespace rb

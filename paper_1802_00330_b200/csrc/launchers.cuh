@@ -1,0 +1,250 @@
+// launchers.cuh -- definitions of the per-dimension launchers declared in
+// engine.cuh.  Included only by kinst.cu, which instantiates them explicitly.
+#pragma once
+#include "engine.cuh"
+
+template <int N>
+void SetupK<N>::run(rb_handle* h) {
+    const int T = h->hs_threads;
+    h->filter_smem = filter_off_xs(h->meta) + (size_t)2 * N * h->filter_threads * sizeof(double);
+    h->eval_smem = stab_bytes(h->meta, false) + (size_t)3 * N * T * sizeof(double);
+    h->lin_smem = (size_t)(T / 32) * LinLayout<N>::BPW * LinLayout<N>::doubles * sizeof(double);
+    h->sweep_smem = (size_t)2 * N * T * sizeof(double);
+    if (h->meta.ftab) {
+        h->ftab_smem = ftab_smem_bytes<N>(h->meta);
+        if (h->ftab_smem > 160 * 1024) h->meta.ftab = 0;  // tables too large: direct evaluation
+    }
+    // the attribute is per kernel (shared by every handle of this n): set it to the opt-in maximum
+    const size_t mx = std::max({h->filter_smem, h->eval_smem, h->lin_smem, h->sweep_smem});
+    h->fused_smem = fused_off_tiles(h->meta) +
+                    (size_t)(T / 32) * FusedLayout<N>::BPW * FusedLayout<N>::doubles * sizeof(double);
+    if ((int)mx > h->smem_optin) throw ArgError{RB_ERR_LIMIT, "system tables exceed the shared-memory budget"};
+    set_max_dyn_smem(k_filter<N>, h->smem_optin);
+    set_max_dyn_smem(k_filter_tab<N>, h->smem_optin);
+    set_max_dyn_smem(k_hs_eval<N>, h->smem_optin);
+    set_max_dyn_smem(k_hs_lin<N>, h->smem_optin);
+    set_max_dyn_smem(k_hs_sweep<N>, h->smem_optin);
+    set_max_dyn_smem(k_hs_fused<N>, h->smem_optin);
+    if ((int)h->fused_smem > h->smem_optin) h->hs_fused = false;
+    int nb = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter<N>, h->filter_threads, h->filter_smem), "occ");
+    h->filter_blocks_per_sm = std::max(1, nb);
+    if (h->meta.ftab) {
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter_tab<N>, 256, h->ftab_smem), "occ");
+        h->ftab_blocks_per_sm = std::max(1, nb);
+    }
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_eval<N>, T, h->eval_smem), "occ");
+    h->eval_blocks_per_sm = std::max(1, nb);
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_lin<N>, T, h->lin_smem), "occ");
+    h->lin_blocks_per_sm = std::max(1, nb);
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_sweep<N>, T, h->sweep_smem), "occ");
+    h->sweep_blocks_per_sm = std::max(1, nb);
+    if (h->hs_fused) {
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_fused<N>, T, h->fused_smem), "occ");
+        h->fused_blocks_per_sm = std::max(1, nb);
+    }
+    // persistent small-round kernel: 256 threads, shared memory for its largest phase
+    h->mk_smem = std::max<size_t>(filter_off_xs(h->meta) + (size_t)2 * N * 256 * sizeof(double),
+                                  fused_off_tiles(h->meta) + (size_t)(256 / 32) * FusedLayout<N>::BPW *
+                                                                 FusedLayout<N>::doubles * sizeof(double));
+    h->mk_blocks_per_sm = 0;
+    if ((int)h->mk_smem <= h->smem_optin) {
+        set_max_dyn_smem(k_small_rounds<N>, h->smem_optin);
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_small_rounds<N>, 256, h->mk_smem), "occ");
+        h->mk_blocks_per_sm = nb;
+    }
+    if (h->mk_blocks_per_sm < 1) h->use_mk = false;
+}
+
+template <int N>
+void ClassifyK<N>::run(rb_handle* h, double target, const DevState* st, int64_t bound) {
+    Front cur = h->F[h->cur].f, next = h->F[h->cur ^ 1].f;
+    const int blocks = grid_for(bound >= 0 ? bound : h->n_cur, 256, h->sms * 8);
+    h->launches++;
+    klaunch(h, k_classify<N>, blocks, 256, 0, h->meta, cur, h->n_cur, next, h->parents, h->d_ctr, target, st);
+    ck(cudaGetLastError(), "classify launch");
+}
+
+template <int N>
+void AllParentsK<N>::run(rb_handle* h) {
+    const int blocks = grid_for(h->n_cur, 256, h->sms * 8);
+    h->launches++;
+    klaunch(h, k_all_parents<N>, blocks, 256, 0, h->meta, h->F[h->cur].f, h->n_cur, h->parents, h->d_ctr);
+    ck(cudaGetLastError(), "parents launch");
+}
+
+template <int N>
+void FilterK<N>::run(rb_handle* h, int64_t max_parents, int64_t* tags) {
+    if (h->meta.ftab && h->use_ftab) {
+        using Sh = FtabShape<N>;
+        const int64_t units = N >= 8 ? (max_parents << Sh::CHLOG) : ((max_parents + Sh::PPB - 1) >> Sh::LOGPPB);
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)h->sms * h->ftab_blocks_per_sm));
+        h->launches++;
+        klaunch(h, k_filter_tab<N>, blocks, 256, h->ftab_smem, h->meta, h->d_tab, h->F[h->cur].f, h->parents,
+                                                             h->d_ctr, h->S, tags, h->d_order);
+        ck(cudaGetLastError(), "filter_tab launch");
+        return;
+    }
+    const int64_t work = max_parents << N;
+    const int blocks = grid_for(work, h->filter_threads, h->sms * h->filter_blocks_per_sm);
+    h->launches++;
+    klaunch(h, k_filter<N>, blocks, h->filter_threads, h->filter_smem, h->meta, h->d_tab, h->F[h->cur].f,
+                                                                     h->parents, h->d_ctr, h->S, tags, h->d_order);
+    ck(cudaGetLastError(), "filter launch");
+}
+
+template <int N>
+void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* tags, int64_t batch_bound) {
+    const int T = h->hs_threads;
+    const int64_t B = h->W.B;
+    Front out = h->F[h->cur ^ 1].f;
+    h->launches += 3;
+    // split each box's n^2 + n polynomials over R threads when the batch is small
+    const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(B, batch_bound));
+    const int64_t target = (int64_t)h->sms * 1024;
+    const int R = (int)std::max<int64_t>(1, std::min<int64_t>(N * N + N, (target + bound - 1) / bound));
+    klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
+        h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags, R);
+    klaunch(h, k_hs_lin<N>, grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem, h->S, n_in, b0, prm, h->W, h->d_ctr);
+    klaunch(h, k_hs_sweep<N>, grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem,
+        h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
+    ck(cudaGetLastError(), "hs launch");
+}
+
+template <int N>
+void HsFusedK<N>::run(rb_handle* h, int64_t n_in, HsParams prm, int64_t* tags, int64_t bound) {
+    const int T = h->hs_threads;
+    h->launches++;
+    const int64_t lanes = std::max<int64_t>(1, bound) * FusedLayout<N>::G;
+    klaunch(h, k_hs_fused<N>, grid_for(lanes, T, h->sms * h->fused_blocks_per_sm), T, h->fused_smem,
+        h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
+    ck(cudaGetLastError(), "hs fused launch");
+}
+
+template <int N>
+void KrawczykK<N>::run(rb_handle* h, int64_t b0, int64_t b_end, Front out, uint8_t* ok) {
+    const int T = h->hs_threads;
+    const int64_t B = h->W.B;
+    HsParams prm{};
+    prm.hs_mode = 1;
+    h->launches += 3;
+    const int64_t bound = b_end - b0;
+    const int64_t target = (int64_t)h->sms * 1024;
+    const int R = (int)std::max<int64_t>(1, std::min<int64_t>(N * N + N, (target + bound - 1) / bound));
+    klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
+        h->meta, h->d_tab, h->S, b_end, b0, prm, h->W, out, h->d_ctr, nullptr, R);
+    klaunch(h, k_hs_lin<N>, grid_for(std::min(B, bound), (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem, h->S, b_end, b0, prm, h->W, h->d_ctr);
+    klaunch(h, k_krawczyk<N>, grid_for(bound, 128, h->sms * 16), 128, 0, h->S, b_end, b0, h->W, out, ok);
+    ck(cudaGetLastError(), "krawczyk launch");
+}
+
+template <int N>
+void SmallRoundsK<N>::run(rb_handle* h, const HsParams& prm, bool dedup, int64_t scap, cudaGraphConditionalHandle hw) {
+    SmallArgs a{};
+    a.dedup = dedup ? 1 : 0;
+    a.trace = h->trace ? h->d_trace : nullptr;
+    a.meta = h->meta;
+    a.gtab = h->d_tab;
+    a.f0 = h->F[0].f;
+    a.f1 = h->F[1].f;
+    a.S = h->S;
+    a.parents = h->parents;
+    a.ctr = h->d_ctr;
+    a.st = h->d_state;
+    a.rstats = h->d_rstats;
+    a.order = h->d_order;
+    a.table = h->d_table;
+    a.table_mask = (unsigned long long)(h->table_slots - 1);
+    a.slot_of = h->d_slot;
+    a.dead = h->d_dead;
+    a.prm = prm;
+    a.bar = h->d_bar;
+    a.mk_cap = std::min<int64_t>(h->mk_cap, scap);
+    a.graph_cap = scap;
+    a.h_while = hw;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(h->sms * std::min(h->mk_blocks_per_sm, h->mk_bps)));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = h->mk_smem;
+    cfg.stream = h->st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    h->launches++;
+    ck(cudaLaunchKernelEx(&cfg, k_small_rounds<N>, a), "small rounds launch");
+}
+
+template <int N>
+void DedupInsertK<N>::run(rb_handle* h, Front next) {
+    const int blocks = grid_for(next.cap, 256, h->sms * 8);
+    h->launches++;
+    klaunch(h, k_dedup_insert<N>, blocks, 256, 0, next, h->d_table, (unsigned long long)(h->table_slots - 1),
+            h->d_slot, h->d_dead, h->d_ctr, h->S.cap);
+}
+
+template <int N>
+void TailK<N>::run(rb_handle* h, bool dedup, int64_t bound, int64_t scap, cudaGraphConditionalHandle hw) {
+    const int blocks = grid_for(bound, 256, h->sms * 2);
+    h->launches++;
+    klaunch(h, k_round_tail<N>, blocks, 256, 0, h->F[1].f, h->F[0].f, h->d_table, (const unsigned*)h->d_slot,
+            (const uint8_t*)h->d_dead, dedup ? 1 : 0, h->d_state, h->d_ctr, h->d_rstats, scap, hw, h->d_order,
+            h->meta);
+}
+
+template <int N>
+void SettleK<N>::run(rb_handle* h, int64_t bound) {
+    klaunch(h, k_settle<N>, grid_for(bound, 256, h->sms * 8), 256, 0, h->F[1].f, h->F[0].f, h->d_ctr);
+    ck(cudaGetLastError(), "settle launch");
+}
+
+template <int N>
+void DedupK<N>::run(rb_handle* h, Front next, Front other) {
+    // persistent grids: the row count is read on the device
+    const int blocks = grid_for(next.cap, 256, h->sms * 8);
+    h->launches += 2;
+    klaunch(h, k_dedup_insert<N>, blocks, 256, 0, next, h->d_table, (unsigned long long)(h->table_slots - 1),
+                                                 h->d_slot, h->d_dead, h->d_ctr, h->S.cap);
+    klaunch(h, k_dedup_finish<N>, blocks, 256, 0, next, other, h->d_table, h->d_slot, h->d_dead, h->d_ctr,
+                                                 h->S.cap);
+    ck(cudaGetLastError(), "dedup launch");
+}
+
+template <int N>
+void PartitionK<N>::run(rb_handle* h, int world, int64_t* counts) {
+    const int64_t n = h->n_cur;
+    unsigned* owner = nullptr;
+    unsigned long long* cnt = nullptr;
+    dalloc(&owner, (size_t)std::max<int64_t>(n, 1));
+    dalloc(&cnt, (size_t)2 * world);
+    ck(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2 * world, h->st), "memset");
+    const int blocks = grid_for(n, 256, h->sms * 8);
+    h->launches += 2;
+    if (n > 0) k_owner_count<N><<<blocks, 256, 0, h->st>>>(h->F[h->cur].f, n, world, owner, cnt);
+    std::vector<unsigned long long> hc(2 * world);
+    ck(cudaMemcpyAsync(hc.data(), cnt, sizeof(unsigned long long) * world, cudaMemcpyDeviceToHost, h->st), "d2h");
+    ck(cudaStreamSynchronize(h->st), "sync");
+    unsigned long long off = 0;
+    for (int r = 0; r < world; r++) {
+        counts[r] = (int64_t)hc[r];
+        hc[world + r] = off;
+        off += hc[r];
+    }
+    ck(cudaMemcpyAsync(cnt + world, hc.data() + world, sizeof(unsigned long long) * world, cudaMemcpyHostToDevice,
+                       h->st), "h2d");
+    if (n > 0) k_owner_scatter<N><<<blocks, 256, 0, h->st>>>(h->F[h->cur].f, n, owner, cnt + world,
+                                                            h->F[h->cur ^ 1].f);
+    ck(cudaGetLastError(), "partition");
+    h->cur ^= 1;
+    dfree(owner);
+    dfree(cnt);
+    ck(cudaStreamSynchronize(h->st), "sync");
+}
+
+template <int N>
+void WidthK<N>::run(rb_handle* h) {
+    h->launches++;
+    k_width<N><<<grid_for(h->n_cur, 256, h->sms * 8), 256, 0, h->st>>>(h->F[h->cur].f, h->n_cur, h->d_ctr);
+    ck(cudaGetLastError(), "width");
+}
