@@ -446,7 +446,7 @@ static void stamp(rb_handle* h, const DevState* st, int round_host, int phase, i
 }
 static void trace_report(rb_handle* h, int rounds) {
     if (!h->trace) return;
-    std::vector<unsigned long long> t((size_t)kTraceRounds * kTracePhases);
+    std::vector<unsigned long long> t((size_t)kTraceRounds * kTracePhases + 16);
     ck(cudaMemcpy(t.data(), h->d_trace, t.size() * 8, cudaMemcpyDeviceToHost), "trace d2h");
     static const char* names[] = {"classify", "filter", "hs", "dedup", "settle", "round_end", "loop"};
     for (int r = 1; r <= std::min(rounds, kTraceRounds - 1); r++) {
@@ -460,6 +460,15 @@ static void trace_report(rb_handle* h, int rounds) {
         }
         std::fprintf(stderr, " us");
         std::fprintf(stderr, "\n");
+    }
+    const unsigned long long* q = &t[(size_t)kTraceRounds * kTracePhases];
+    if (q[1]) {
+        std::fprintf(stderr, "[rb trace] last k_hs_fused, block 0 (cycles): ctr %llu, tables %llu, box load %llu, eval %llu, "
+                             "lin %llu, sweep %llu, output %llu, rest %llu; kernel %.1f us\n",
+                     q[2] - q[1], q[3] - q[2], q[4] - q[3], q[5] - q[4], q[6] - q[5], q[7] - q[6], q[8] - q[7],
+                     q[9] - q[8], (q[10] - q[0]) * 1e-3);
+        std::fprintf(stderr, "[rb trace]   lin: loads %llu, scale %llu, gauss-jordan %llu, guards %llu, products %llu\n",
+                     q[11] - q[5], q[12] - q[11], q[13] - q[12], q[14] - q[13], q[6] - q[14]);
     }
     ck(cudaMemset(h->d_trace, 0, t.size() * 8), "trace clear");
 }
@@ -1091,8 +1100,8 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         dalloc(&h->d_bar, 2);
         ck(cudaMemsetAsync(h->d_bar, 0, 2 * sizeof(unsigned), h->st), "barrier clear");
         if (h->trace) {
-            dalloc(&h->d_trace, (size_t)kTraceRounds * kTracePhases);
-            ck(cudaMemsetAsync(h->d_trace, 0, (size_t)kTraceRounds * kTracePhases * 8, h->st), "trace clear");
+            dalloc(&h->d_trace, (size_t)kTraceRounds * kTracePhases + 16);
+            ck(cudaMemsetAsync(h->d_trace, 0, ((size_t)kTraceRounds * kTracePhases + 16) * 8, h->st), "trace clear");
         }
         dalloc(&h->d_order, 16);
         reset_order(h);

@@ -77,31 +77,16 @@ struct Fast {
         double b = (c >= 0.0) ? y.hi : y.lo;
         return mk(__dmul_rd(c, a), __dmul_ru(c, b));
     }
-    // case-split interval product; equals min/max of the four directed products
+    // interval.py:322-326 / _batch.i_mul (_batch.py:94-105): min of the four RD products,
+    // max of the four RU products, as the pairwise tree of _batch.i_mul.  Eight
+    // independent DMULs and two select trees: a short dependency chain (the
+    // sign-case split it replaces waited on four compares and a branch first).
     __device__ __forceinline__ static ival mul(ival x, ival y) {
-        const double a = x.lo, b = x.hi, c = y.lo, d = y.hi;
-        const bool xp = a >= 0.0, xn = b <= 0.0;
-        const bool yp = c >= 0.0, yn = d <= 0.0;
-        if (!xp && !xn && !yp && !yn) {  // both straddle zero
-            double lo = fmin(__dmul_rd(a, d), __dmul_rd(b, c));
-            double hi = fmax(__dmul_ru(a, c), __dmul_ru(b, d));
-            return mk(lo, hi);
-        }
-        double l1, l2, h1, h2;
-        if (xp) {
-            // x>=0: y>=0 -> [ac, bd]; y<=0 -> [bc, ad]; y straddles -> [bc, bd]
-            l1 = yp ? a : b;  l2 = c;
-            h1 = yn ? a : b;  h2 = d;
-        } else if (xn) {
-            // x<=0: y>=0 -> [ad, bc]; y<=0 -> [bd, ac]; y straddles -> [ad, ac]
-            l1 = yn ? b : a;  l2 = d;
-            h1 = yp ? b : a;  h2 = c;
-        } else {
-            // x straddles: y>=0 -> [ad, bd]; y<=0 -> [bc, ac]
-            l1 = yp ? a : b;  l2 = yp ? d : c;
-            h1 = yp ? b : a;  h2 = yp ? d : c;
-        }
-        return mk(__dmul_rd(l1, l2), __dmul_ru(h1, h2));
+        const double p0 = __dmul_rd(x.lo, y.lo), p1 = __dmul_rd(x.lo, y.hi);
+        const double p2 = __dmul_rd(x.hi, y.lo), p3 = __dmul_rd(x.hi, y.hi);
+        const double q0 = __dmul_ru(x.lo, y.lo), q1 = __dmul_ru(x.lo, y.hi);
+        const double q2 = __dmul_ru(x.hi, y.lo), q3 = __dmul_ru(x.hi, y.hi);
+        return mk(py_min(py_min(p0, p1), py_min(p2, p3)), py_max(py_max(q0, q1), py_max(q2, q3)));
     }
     // interval.py:328-345 / _batch.py:122-138.  Odd powers use the identity
     // -chain_ru(-l) == chain of RD multiplications by |l| started at l (and

@@ -155,9 +155,31 @@ __device__ __forceinline__ bool mul_guard_ok(ival x, ival y) {
     return prod_guard_ok(a, b);
 }
 
-// interval product, guarded per call (rarely taken slow path)
+// |v| <= 2^989 (operand side of the trusted band), a bit test on the high word
+__device__ __forceinline__ bool op_small(double v) {
+    return ((unsigned)__double2hiint(v) & 0x7fffffffu) < (2013u << 20);
+}
+// v == 0 or 2^-965 <= |v| <= 2^988 (result side of the trusted band)
+__device__ __forceinline__ bool prod_in_band(double v) {
+    const unsigned hi = (unsigned)__double2hiint(v) & 0x7fffffffu;
+    return (hi - (58u << 20)) < ((2012u - 58u) << 20) || (hi | (unsigned)__double2loint(v)) == 0u;
+}
+
+// interval product, guarded per call (rarely taken slow path).  The guard is
+// checked on the IEEE results themselves: every operand at most 2^989 and every
+// directed product zero or in [2^-965, 2^988] -- then no product of nonzero
+// operands reached the reference's untrusted band (a nonzero exact product below
+// it has its away-from-zero rounding nonzero and below 2^-965), so the Dekker
+// error is exact and IEEE RD/RU equal _mul_rd/_mul_ru (interval.py:98-136).
 __device__ __forceinline__ ival gmul(ival x, ival y) {
-    if (mul_guard_ok(x, y)) return Fast::mul(x, y);
+    const double p0 = __dmul_rd(x.lo, y.lo), p1 = __dmul_rd(x.lo, y.hi);
+    const double p2 = __dmul_rd(x.hi, y.lo), p3 = __dmul_rd(x.hi, y.hi);
+    const double q0 = __dmul_ru(x.lo, y.lo), q1 = __dmul_ru(x.lo, y.hi);
+    const double q2 = __dmul_ru(x.hi, y.lo), q3 = __dmul_ru(x.hi, y.hi);
+    const bool ok = op_small(x.lo) & op_small(x.hi) & op_small(y.lo) & op_small(y.hi) & prod_in_band(p0) &
+                    prod_in_band(p1) & prod_in_band(p2) & prod_in_band(p3) & prod_in_band(q0) & prod_in_band(q1) &
+                    prod_in_band(q2) & prod_in_band(q3);
+    if (ok) return mk(py_min(py_min(p0, p1), py_min(p2, p3)), py_max(py_max(q0, q1), py_max(q2, q3)));
     return Exact::mul(x, y);
 }
 
@@ -849,6 +871,7 @@ struct HsParams {
     long long fused_max;   // k_hs_fused takes n_in <= fused_max rows, eval/lin/sweep take larger counts
     int has_cond;          // graph mode: k_hs_fused selects the eval/lin/sweep branch (IF node)
     cudaGraphConditionalHandle big_cond;
+    unsigned long long* prof;  // RB_TRACE: k_hs_fused phase clocks of block 0's first box (dev aid)
 };
 
 struct HsScratch {         // SoA with stride B (batch capacity)
@@ -1045,7 +1068,7 @@ struct LinLayout {
 // the minimum is RD(a l), for a < 0 it is RD(a h) -- the 4-product min/max of
 // interval.py:322-326 for a point left operand.
 __device__ __forceinline__ ival pmul_minmax(double a, ival y) {
-    return mk(fmin(__dmul_rd(a, y.lo), __dmul_rd(a, y.hi)), fmax(__dmul_ru(a, y.lo), __dmul_ru(a, y.hi)));
+    return mk(py_min(__dmul_rd(a, y.lo), __dmul_rd(a, y.hi)), py_max(__dmul_ru(a, y.lo), __dmul_ru(a, y.hi)));
 }
 template <class A>
 __device__ __forceinline__ ival pmul(double a, ival y) {
@@ -1106,7 +1129,7 @@ static __device__ __noinline__ void lin_products_exact(const double* Am, const i
 // M = A J and g = A F(x) over J / F(x) in place.  Returns true when singular.
 template <int N, int G>
 __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* sCol, int l, unsigned gmask,
-                                          bool& exact_lin) {
+                                          bool& exact_lin, unsigned long long* pr = nullptr) {
     // J column (l % N), kept in registers for M
     ival jcol[N];
     double c[N];
@@ -1132,8 +1155,10 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
 #pragma unroll
         for (int i = 0; i < N; i++) c[i] = (l - N == i) ? 1.0 : 0.0;
     }
+    if (pr) pr[0] = clock64() + (unsigned long long)(c[0] + colmax) * 0ull;
     // Gauss-Jordan inverse (linalg.py:137-172), lane = column of [jc | I]
     const double scale = group_max<G>(gmask, l < N ? colmax : 0.0);
+    if (pr) pr[1] = clock64() + (unsigned long long)scale * 0ull;
     bool singular = scale == 0.0;
     const double threshold = __dmul_rn(1e-12, scale);
 #pragma unroll
@@ -1180,6 +1205,7 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
         }
         __syncwarp(gmask);
     }
+    if (pr) pr[2] = clock64() + (unsigned long long)c[N - 1] * 0ull;
     exact_lin = false;
     if (singular) return true;
     ExpRange ra, rf;
@@ -1202,6 +1228,7 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
     rj.emin = min(rj.emin, rf.emin);
     rj.emax = max(rj.emax, rf.emax);
     const bool fastM = prod_guard_ok(ra, rj);
+    if (pr) pr[3] = clock64() + (unsigned long long)fastM * 0ull;
     __syncwarp(gmask);
     if (fastM) lin_products<N, Fast>(Am, jcol, l, K, gmask);
     else lin_products_exact<N>(Am, jcol, l, K, gmask);
@@ -1293,13 +1320,28 @@ __global__ void __launch_bounds__(128) k_krawczyk(SBuf S, int64_t b_end, int64_t
     }
 }
 
+// 1/y rounded down or up (up != 0) for a normal y whose reciprocal is normal: one
+// round-to-nearest reciprocal r, whose FMA residual 1 - y r is exact; the residual's
+// sign times y's tells on which side of 1/y r lies (the directed-rounding division
+// sequences are ~3x longer on sm_100).
+__device__ __forceinline__ double recip_dir(double y, bool up) {
+    const double r = __drcp_rn(y);
+    const double e = __fma_rn(-y, r, 1.0);
+    if (e == 0.0) return r;
+    const bool r_below = (e > 0.0) == (y > 0.0);  // r < 1/y
+    const long long b = __double_as_longlong(r);
+    // one ulp toward +inf (up, r below) or -inf (down, r above); r != 0
+    if (up == r_below) return __longlong_as_double(b + (((r > 0.0) == up) ? 1 : -1));
+    return r;
+}
+
 // fast reciprocal-based single case of div_extended; exact emulation elsewhere
 __device__ __forceinline__ int div_extended_fast(ival p, ival y, ival& q0, ival& q1) {
     if (!contains_zero(y)) {
         const double al = fabs(y.lo), ah = fabs(y.hi);
         if (al > 0x1p-990 && ah < 0x1p990) {
             // _div_rd/_div_ru (interval.py:157-190) == IEEE directed division inside the trusted band
-            const ival r = mk(__ddiv_rd(1.0, y.hi), __ddiv_ru(1.0, y.lo));
+            const ival r = mk(recip_dir(y.hi, false), recip_dir(y.lo, true));
             q0 = gmul(p, r);
             return DIV_SINGLE;
         }
@@ -1519,7 +1561,10 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     constexpr int P = N * N + N;
     extern __shared__ __align__(16) uint8_t smem[];
     bool hs_on;
+    const bool prof = prm.prof && blockIdx.x == 0 && threadIdx.x == 0;
+    if (prof) prm.prof[0] = gtimer(), prm.prof[1] = clock64();
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
+    if (prof) prm.prof[2] = clock64();
     if (prm.has_cond && blockIdx.x == 0 && threadIdx.x == 0)
         cudaGraphSetConditional(prm.big_cond, n_in > prm.fused_max ? 1u : 0u);
     if (n_in < 0 || n_in > prm.fused_max) return;  // large counts: eval/lin/sweep
@@ -1536,6 +1581,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     double* s = reinterpret_cast<double*>(smem + fused_off_tiles(meta)) + (size_t)(warp * L::BPW + gi) * L::doubles;
     const LinSink K{s + L::oJl, s + L::oJh, s + L::oFl, s + L::oFh, 1};
     __syncthreads();
+    if (prof) prm.prof[3] = clock64();
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t wglob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     unsigned long long ops_acc = 0, calls_acc = 0, exact_acc = 0;
@@ -1558,6 +1604,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
             }
             __syncwarp(gmask);
             // ---- eval: J(X) (hansen.py:61-63) and F(x) (poly.py:205-207)
+            if (prof && wb0 == 0) prm.prof[4] = clock64();
             ExpRange rx, rm;
             rx.init();
             rm.init();
@@ -1586,10 +1633,13 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
             }
             if (l == 0 && !(fastJ && fastF)) exact_acc++;
             __syncwarp(gmask);
+            if (prof && wb0 == 0) prm.prof[5] = clock64();
             // ---- lin: A = mid(J)^-1, M = A J, g = A F(x)
             bool exact_lin;
-            const bool singular = lin_group<N, G>(K, s + L::oA, s + L::oCol, l, gmask, exact_lin);
+            const bool singular = lin_group<N, G>(K, s + L::oA, s + L::oCol, l, gmask, exact_lin,
+                                                  (prof && wb0 == 0) ? prm.prof + 11 : nullptr);
             __syncwarp(gmask);
+            if (prof && wb0 == 0) prm.prof[6] = clock64();
             if (singular) {
                 kind = HS_SKIP;
             } else {
@@ -1664,6 +1714,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
             }
         }
         // outputs (bnb.py:197-210): group leaders reserve slots for the warp
+        if (prof && wb0 == 0) prm.prof[7] = clock64();
         int cnt = 0;
         bool use_input = false;
         if (valid) {
@@ -1720,6 +1771,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
         wbits = warp_max(wbits);
         if (lane == 0 && wbits) atomicMax(&ctr->wmax, wbits);
         __syncwarp();  // the tile is reused by the next box of this group
+        if (prof && wb0 == 0) prm.prof[8] = clock64();
     }
     ops_acc = warp_sum(ops_acc);
     calls_acc = warp_sum(calls_acc);
@@ -1729,6 +1781,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
         if (calls_acc) atomicAdd(&ctr->hs_calls, calls_acc);
         if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
     }
+    if (prof) prm.prof[9] = clock64(), prm.prof[10] = gtimer();
 }
 
 template <int N>

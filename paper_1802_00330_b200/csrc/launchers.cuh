@@ -116,6 +116,7 @@ void HsFusedK<N>::run(rb_handle* h, int64_t n_in, HsParams prm, int64_t* tags, i
     const int T = h->hs_threads;
     h->launches++;
     const int64_t lanes = std::max<int64_t>(1, bound) * FusedLayout<N>::G;
+    if (h->trace) prm.prof = h->d_trace + 256 * 8;
     klaunch(h, k_hs_fused<N>, grid_for(lanes, T, h->sms * h->fused_blocks_per_sm), T, h->fused_smem,
         h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
     ck(cudaGetLastError(), "hs fused launch");
