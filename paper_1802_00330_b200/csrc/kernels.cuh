@@ -73,6 +73,24 @@ __host__ __device__ inline int stab_bytes(const TabMeta& m, bool f_only) {
     return align8(8 * T) + align8(2 * (P + 1)) + align8(2 * (T + 1)) + align8(2 * Fc);
 }
 
+// Asynchronous global -> shared copy (cp.async): every element copy of a table is
+// in flight at once instead of each load waiting for the previous shared store
+// (generic pointers may alias, so plain load/store loops serialise).  `bytes`
+// is rounded up to whole `W`-byte words; both sides must be W-aligned and the
+// destination region padded to the rounded size.  Completed by cp_async_wait().
+template <int W>
+__device__ __forceinline__ void copy_async(void* dst, const void* src, int bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const char* g = reinterpret_cast<const char*>(src);
+    for (int i = threadIdx.x * W; i < bytes; i += blockDim.x * W) {
+        if constexpr (W == 16)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + i), "l"(g + i) : "memory");
+        else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d + i), "l"(g + i), "n"(W) : "memory");
+    }
+}
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ inline STab load_stab(const TabMeta& m, const uint8_t* g, uint8_t* s, bool f_only) {
     const int T = f_only ? m.TF : m.T;
     const int P = f_only ? m.n : m.P;
@@ -82,14 +100,12 @@ __device__ inline STab load_stab(const TabMeta& m, const uint8_t* g, uint8_t* s,
     uint16_t* po = reinterpret_cast<uint16_t*>(s + align8(8 * T));
     uint16_t* fo = reinterpret_cast<uint16_t*>(s + align8(8 * T) + align8(2 * (P + 1)));
     uint16_t* fa = reinterpret_cast<uint16_t*>(s + align8(8 * T) + align8(2 * (P + 1)) + align8(2 * (T + 1)));
-    const double* gc = reinterpret_cast<const double*>(g);
-    const uint16_t* gpo = reinterpret_cast<const uint16_t*>(g + m.off_poly);
-    const uint16_t* gfo = reinterpret_cast<const uint16_t*>(g + m.off_fac_off);
-    const uint16_t* gfa = reinterpret_cast<const uint16_t*>(g + m.off_fac);
-    for (int i = threadIdx.x; i < T; i += blockDim.x) c[i] = gc[i];
-    for (int i = threadIdx.x; i <= P; i += blockDim.x) po[i] = gpo[i];
-    for (int i = threadIdx.x; i <= T; i += blockDim.x) fo[i] = gfo[i];
-    for (int i = threadIdx.x; i < Fc; i += blockDim.x) fa[i] = gfa[i];
+    // the global arrays are 8-aligned and zero-padded to 8 bytes, so whole 4-byte words stay in bounds
+    copy_async<8>(c, g, 8 * T);
+    copy_async<4>(po, g + m.off_poly, 2 * (P + 1));
+    copy_async<4>(fo, g + m.off_fac_off, 2 * (T + 1));
+    copy_async<4>(fa, g + m.off_fac, 2 * Fc);
+    cp_async_wait();
     t.coeff = c;
     t.poly_off = po;
     t.fac_off = fo;
@@ -543,12 +559,9 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
         s_eval[threadIdx.x] = 0;
         s_rej[threadIdx.x] = 0;
     }
-    const STab tab = load_stab(meta, gtab, smem, true);
     TermP* tp = reinterpret_cast<TermP*>(smem + filter_off_termp(meta));
-    {
-        const TermP* g = reinterpret_cast<const TermP*>(gtab + meta.off_termp);
-        for (int i = threadIdx.x; i < meta.TF; i += blockDim.x) tp[i] = g[i];
-    }
+    copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
+    const STab tab = load_stab(meta, gtab, smem, true);
     const int stride = blockDim.x;
     double2* xs2 = reinterpret_cast<double2*>(smem + filter_off_xs(meta)) + threadIdx.x;
     __syncthreads();
@@ -722,14 +735,10 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
     uint32_t* ent = reinterpret_cast<uint32_t*>(p8 + align8(2 * meta.TF) + align8(2 * (N + 1)));
     double* sp = reinterpret_cast<double*>(smem + ftab_off_sp<N>(meta));  // [PPB][3N + 1]: lo, hi, mid, exact
     double2* table = reinterpret_cast<double2*>(smem + ftab_off_table<N>(meta));
-    {
-        const uint16_t* g16 = reinterpret_cast<const uint16_t*>(gtab + meta.off_tbase);
-        for (int i = threadIdx.x; i < meta.TF; i += blockDim.x) tbase[i] = g16[i];
-        const uint16_t* g16b = reinterpret_cast<const uint16_t*>(gtab + meta.off_ent_off);
-        for (int i = threadIdx.x; i <= N; i += blockDim.x) ent_off[i] = g16b[i];
-        const uint32_t* g32 = reinterpret_cast<const uint32_t*>(gtab + meta.off_ent);
-        for (int i = threadIdx.x; i < meta.ent_total; i += blockDim.x) ent[i] = g32[i];
-    }
+    copy_async<4>(tbase, gtab + meta.off_tbase, 2 * meta.TF);
+    copy_async<4>(ent_off, gtab + meta.off_ent_off, 2 * (N + 1));
+    copy_async<4>(ent, gtab + meta.off_ent, 4 * meta.ent_total);
+    cp_async_wait();
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const unsigned long long n_par = ctr->n_par;
@@ -1161,49 +1170,90 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
     if (pr) pr[1] = clock64() + (unsigned long long)scale * 0ull;
     bool singular = scale == 0.0;
     const double threshold = __dmul_rn(1e-12, scale);
+    if constexpr (N <= 8) {
+        // column k broadcast by shuffles; every lane repeats the pivot search on it
 #pragma unroll
-    for (int k = 0; k < N; k++) {
-        if (singular) break;  // group-uniform
-        if (l == k) {
+        for (int k = 0; k < N; k++) {
+            if (singular) break;  // group-uniform
+            double col[N];
+#pragma unroll
+            for (int i = 0; i < N; i++) col[i] = gshfl<G>(gmask, c[i], k);
             int pr = k;  // first row r >= k with max |c[r][k]|
-            double best = fabs(c[k]);
+            double best = fabs(col[k]), pivot = col[k];
 #pragma unroll
             for (int r = k + 1; r < N; r++)
-                if (fabs(c[r]) > best) {
-                    best = fabs(c[r]);
+                if (fabs(col[r]) > best) {
+                    best = fabs(col[r]);
                     pr = r;
+                    pivot = col[r];
                 }
+            if (fabs(pivot) < threshold) {
+                singular = true;
+            } else {
 #pragma unroll
-            for (int i = 0; i < N; i++) sCol[i] = c[i];
-            sCol[N] = (double)pr;
-        }
-        __syncwarp(gmask);
-        const int pr = (int)sCol[N];
-        const double pivot = sCol[pr];
-        if (fabs(pivot) < threshold) {
-            singular = true;
-        } else {
+                for (int r = k + 1; r < N; r++)
+                    if (r == pr) {
+                        const double tmp = c[k];
+                        c[k] = c[r];
+                        c[r] = tmp;
+                    }
+                const double inv = __ddiv_rn(1.0, pivot);
+                if (l >= k && l < 2 * N) {
+                    c[k] = __dmul_rn(c[k], inv);
 #pragma unroll
-            for (int r = k + 1; r < N; r++)
-                if (r == pr) {
-                    const double tmp = c[k];
-                    c[k] = c[r];
-                    c[r] = tmp;
-                }
-            const double inv = __ddiv_rn(1.0, pivot);
-            if (l >= k && l < 2 * N) {
-                c[k] = __dmul_rn(c[k], inv);
-#pragma unroll
-                for (int i = 0; i < N; i++) {
-                    if (i == k) continue;
-                    const double f = sCol[i == pr ? k : i];  // column k after the row swap
-                    // the reference skips f == 0 (linalg.py:168); c - 0*c[k] == c for the finite
-                    // values here (only a zero's sign could differ), so no test is needed
-                    c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
+                    for (int i = 0; i < N; i++) {
+                        if (i == k) continue;
+                        const double f = i == pr ? col[k] : col[i];  // column k after the row swap
+                        c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
+                    }
                 }
             }
         }
-        __syncwarp(gmask);
+    } else {
+    #pragma unroll
+        for (int k = 0; k < N; k++) {
+            if (singular) break;  // group-uniform
+            if (l == k) {
+                int pr = k;  // first row r >= k with max |c[r][k]|
+                double best = fabs(c[k]);
+    #pragma unroll
+                for (int r = k + 1; r < N; r++)
+                    if (fabs(c[r]) > best) {
+                        best = fabs(c[r]);
+                        pr = r;
+                    }
+    #pragma unroll
+                for (int i = 0; i < N; i++) sCol[i] = c[i];
+                sCol[N] = (double)pr;
+            }
+            __syncwarp(gmask);
+            const int pr = (int)sCol[N];
+            const double pivot = sCol[pr];
+            if (fabs(pivot) < threshold) {
+                singular = true;
+            } else {
+    #pragma unroll
+                for (int r = k + 1; r < N; r++)
+                    if (r == pr) {
+                        const double tmp = c[k];
+                        c[k] = c[r];
+                        c[r] = tmp;
+                    }
+                const double inv = __ddiv_rn(1.0, pivot);
+                if (l >= k && l < 2 * N) {
+                    c[k] = __dmul_rn(c[k], inv);
+    #pragma unroll
+                    for (int i = 0; i < N; i++) {
+                        if (i == k) continue;
+                        const double f = sCol[i == pr ? k : i];  // column k after the row swap
+                        // the reference skips f == 0 (linalg.py:168); c - 0*c[k] == c for the finite
+                        // values here (only a zero's sign could differ), so no test is needed
+                        c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
+                    }
+                }
+            }
+            __syncwarp(gmask);
+        }
     }
     if (pr) pr[2] = clock64() + (unsigned long long)c[N - 1] * 0ull;
     exact_lin = false;
