@@ -887,8 +887,14 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     X.start = st;
     X.rows = -1;
     std::atomic_thread_fence(std::memory_order_seq_cst);
+    const double tg0 = now_s();
     ck(cudaGraphLaunch(h->graph_exec, h->st), "graph launch");
+    const double tg1 = now_s();
     ck(cudaStreamSynchronize(h->st), "graph sync");
+    const double tg2 = now_s();
+    if (h->trace)
+        std::fprintf(stderr, "[rb trace] host: solve start -> graph launch %.1f us, launch call %.1f us, sync %.1f us\n",
+                     (tg0 - h->t_solve0) * 1e6, (tg1 - tg0) * 1e6, (tg2 - tg1) * 1e6);
     const DevState r = X.state;
     const int first = (int)h->stats.size();
     const int nr = r.nrounds - first;
@@ -924,6 +930,7 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
 static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info) {
     const int n = h->n;
     const double t_start = now_s();
+    h->t_solve0 = t_start;
     h->launches = 0;
     ck(cudaEventRecord(h->ev[5], h->st), "ev start");
     h->stats.clear();
@@ -1021,6 +1028,7 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
         }
     }
     if (!h->r_ready) finalize_sorted(h);
+    if (h->trace) std::fprintf(stderr, "[rb trace] host: solve total %.1f us\n", (now_s() - t_start) * 1e6);
     trace_report(h, (int)h->stats.size());
     ck(cudaEventRecord(h->ev[6], h->st), "ev end");
     ck(cudaEventSynchronize(h->ev[6]), "ev sync");

@@ -171,6 +171,7 @@ struct rb_handle {
     // RB_TRACE=1: device timestamps (%globaltimer) at the phase boundaries of every
     // round, printed to stderr after each solve (a profiling aid; adds one tiny launch per phase)
     bool trace = false;
+    double t_solve0 = 0.0;
     unsigned long long* d_trace = nullptr;
     size_t fused_smem = 0;
     int fused_blocks_per_sm = 1;
