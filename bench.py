@@ -334,8 +334,16 @@ def run_ours(args, world, rank, local):
     else:
         dom, ops, ms = "k_filter (bisect+inclusion filter+compaction)", filt_ops, filt_ms
     achieved = ops / (ms * 1e-3) if ms > 0 else 0.0
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    traffic = None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        kname = (f"k_hs_fused<{spec.n}>" if dom.startswith("k_hs") else f"k_filter<{spec.n}>")
+        t = json.load(open(tpath)).get(kname)
+        if t:
+            traffic = {"kernel": kname, "dram_bytes_per_launch": t["dram_bytes_per_launch"], "source": t["source"]}
     roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved / 1e12, "peak": peak / 1e12,
-                "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
                 "note": "1 directed FP64 op (DMUL/DADD.RM/RP) = 1 FLOP; peak = measured directed-op throughput "
                         "of this B200 (rb_fp64_peak microbenchmark); algorithmic ops per SURVEY §8(d)",
                 "share_of_step": {"filter_ms": filt_ms / prof_steps, "hs_ms": hs_ms / prof_steps,
