@@ -178,8 +178,11 @@ def default_device() -> int:
 
 def _key(spec: SystemSpec):
     t = compile_tables(spec)
-    h = (t.n, t.poly_off.tobytes(), t.coeff.tobytes(), t.fac_off.tobytes(), t.fac_var.tobytes(),
-         t.fac_exp.tobytes(), t.init_lo.tobytes(), t.init_hi.tobytes())
+    h = t.__dict__.get("_key")
+    if h is None:
+        h = (t.n, t.poly_off.tobytes(), t.coeff.tobytes(), t.fac_off.tobytes(), t.fac_var.tobytes(),
+             t.fac_exp.tobytes(), t.init_lo.tobytes(), t.init_hi.tobytes())
+        t.__dict__["_key"] = h
     return h, t
 
 

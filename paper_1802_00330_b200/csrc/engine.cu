@@ -578,6 +578,31 @@ static void graph_release(rb_handle* h) {
     h->graph_key.clear();
 }
 
+// Mapped pinned host blocks, kept by the process and reused across handles
+// (pinning host memory costs milliseconds; a new engine for the next system reuses one).
+constexpr int64_t kHostSortRows = 16384;  // final sets up to this size are ordered on the host
+constexpr int kPinnedRounds = 256;        // round statistics held in the pinned block
+static std::mutex g_pin_mu;
+static std::vector<std::pair<void*, size_t>> g_pin_free;
+static void* pinned_acquire(size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        for (size_t i = 0; i < g_pin_free.size(); i++)
+            if (g_pin_free[i].second >= bytes) {
+                void* p = g_pin_free[i].first;
+                g_pin_free.erase(g_pin_free.begin() + (long)i);
+                return p;
+            }
+    }
+    void* p = nullptr;
+    ck(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable), "pinned block");
+    return p;
+}
+static void pinned_release(void* p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.emplace_back(p, bytes);
+}
+
 static void release_all(rb_handle* h) {
     h->F[0].release();
     h->F[1].release();
@@ -614,11 +639,12 @@ static void release_all(rb_handle* h) {
     if (h->st) cudaStreamSynchronize(h->st);  // frees are stream-ordered; the pool is shared
     h->pool = nullptr;
     graph_release(h);
-    if (h->h_ctr) cudaFreeHost(h->h_ctr);
-    if (h->h_state) cudaFreeHost(h->h_state);
+    if (h->hx_stats_own) cudaFreeHost(h->hx_stats_own);
+    h->hx_stats_own = nullptr;
+    if (h->pin) pinned_release(h->pin, h->pin_bytes);
+    h->pin = nullptr;
+    h->h_ctr = nullptr;
     h->h_state = nullptr;
-    for (void* p : {(void*)h->hx, (void*)h->hx_stats, (void*)h->hx_lo, (void*)h->hx_hi, (void*)h->hx_c, (void*)h->hx_u})
-        if (p) cudaFreeHost(p);
     h->hx = nullptr;
     h->hx_stats = nullptr;
     for (auto& e : h->ev)
@@ -628,7 +654,6 @@ static void release_all(rb_handle* h) {
 }
 
 // canonical order of F[cur] rows [0, N) -> result buffers (row-major)
-constexpr int64_t kHostSortRows = 16384;
 
 // canonical order of N row-major rows on the host -> hr_* result arrays
 static void sort_on_host(rb_handle* h, int64_t N, const double* lo, const double* hi, const uint8_t* c,
@@ -840,11 +865,12 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         dalloc(&h->d_rstats, (size_t)cfg->max_rounds);
         h->cap_rstats = cfg->max_rounds;
     }
-    if (h->cap_hx_stats < cfg->max_rounds) {
-        if (h->hx_stats) ck(cudaFreeHost(h->hx_stats), "free mapped stats");
-        h->hx_stats = nullptr;
-        ck(cudaHostAlloc((void**)&h->hx_stats, sizeof(DevRoundStats) * cfg->max_rounds, cudaHostAllocMapped),
+    if (h->cap_hx_stats < cfg->max_rounds) {  // beyond the pinned block's kPinnedRounds
+        if (h->hx_stats_own) ck(cudaFreeHost(h->hx_stats_own), "free mapped stats");
+        h->hx_stats_own = nullptr;
+        ck(cudaHostAlloc((void**)&h->hx_stats_own, sizeof(DevRoundStats) * cfg->max_rounds, cudaHostAllocMapped),
            "mapped stats");
+        h->hx_stats = h->hx_stats_own;
         ck(cudaHostGetDevicePointer((void**)&h->hx_stats_dev, h->hx_stats, 0), "mapped ptr");
         h->cap_hx_stats = cfg->max_rounds;
     }
@@ -1093,6 +1119,7 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         if (prop.major < 10) throw ArgError{RB_ERR_CUDA, "device is not sm_100 class (B200 required)"};
         h->sms = prop.multiProcessorCount;
         h->smem_optin = (int)prop.sharedMemPerBlockOptin;
+        const double tc0 = now_s();
         ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "stream");
         ck(cudaStreamCreateWithFlags(&h->st_side, cudaStreamNonBlocking), "stream");
         h->fused_rows = (int64_t)h->sms * 80;  // measured crossover, tools/hs_ab.py
@@ -1100,7 +1127,9 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         h->pool = device_pool(device);  // process-wide per device: memory outlives handles
         PoolScope ps(h);
         for (auto& e : h->ev) ck(cudaEventCreate(&e), "event");
+        const double tc1 = now_s();
         build_tables(h, sys);
+        const double tc2 = now_s();
         size_t free_b = 0, total_b = 0;
         ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
         h->mem_budget = (size_t)(0.80 * (double)free_b);
@@ -1113,19 +1142,47 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         }
         dalloc(&h->d_order, 16);
         reset_order(h);
-        ck(cudaMallocHost((void**)&h->h_ctr, sizeof(Counters)), "pinned ctr");
-        ck(cudaMallocHost((void**)&h->h_state, sizeof(DevState)), "pinned state");
-        ck(cudaHostAlloc((void**)&h->hx, sizeof(HostX), cudaHostAllocMapped), "mapped hx");
-        ck(cudaHostGetDevicePointer((void**)&h->hx_dev, h->hx, 0), "mapped hx ptr");
-        ck(cudaHostAlloc((void**)&h->hx_lo, sizeof(double) * kHostSortRows * h->n, cudaHostAllocMapped), "mapped lo");
-        ck(cudaHostAlloc((void**)&h->hx_hi, sizeof(double) * kHostSortRows * h->n, cudaHostAllocMapped), "mapped hi");
-        ck(cudaHostAlloc((void**)&h->hx_c, kHostSortRows, cudaHostAllocMapped), "mapped cert");
-        ck(cudaHostAlloc((void**)&h->hx_u, kHostSortRows, cudaHostAllocMapped), "mapped unsplit");
-        ck(cudaHostGetDevicePointer((void**)&h->hx_lo_dev, h->hx_lo, 0), "mapped ptr");
-        ck(cudaHostGetDevicePointer((void**)&h->hx_hi_dev, h->hx_hi, 0), "mapped ptr");
-        ck(cudaHostGetDevicePointer((void**)&h->hx_c_dev, h->hx_c, 0), "mapped ptr");
-        ck(cudaHostGetDevicePointer((void**)&h->hx_u_dev, h->hx_u, 0), "mapped ptr");
+        const double tc3 = now_s();
+        // one mapped pinned block (reused across handles): counters, state, the graph's
+        // start/readback area, kPinnedRounds of statistics and up to kHostSortRows result rows
+        {
+            size_t off = 0;
+            auto take = [&](size_t bytes) {
+                const size_t o = off;
+                off = (off + bytes + 63) & ~size_t(63);
+                return o;
+            };
+            const size_t o_ctr = take(sizeof(Counters)), o_state = take(sizeof(DevState)), o_hx = take(sizeof(HostX));
+            const size_t o_stats = take(sizeof(DevRoundStats) * kPinnedRounds);
+            const size_t o_lo = take(sizeof(double) * kHostSortRows * h->n);
+            const size_t o_hi = take(sizeof(double) * kHostSortRows * h->n);
+            const size_t o_c = take(kHostSortRows), o_u = take(kHostSortRows);
+            h->pin_bytes = off;
+            h->pin = static_cast<uint8_t*>(pinned_acquire(off));
+            uint8_t* dev = nullptr;
+            ck(cudaHostGetDevicePointer((void**)&dev, h->pin, 0), "mapped ptr");
+            h->h_ctr = reinterpret_cast<Counters*>(h->pin + o_ctr);
+            h->h_state = reinterpret_cast<DevState*>(h->pin + o_state);
+            h->hx = reinterpret_cast<HostX*>(h->pin + o_hx);
+            h->hx_dev = reinterpret_cast<HostX*>(dev + o_hx);
+            h->hx_stats = reinterpret_cast<DevRoundStats*>(h->pin + o_stats);
+            h->hx_stats_dev = reinterpret_cast<DevRoundStats*>(dev + o_stats);
+            h->cap_hx_stats = kPinnedRounds;
+            h->hx_lo = reinterpret_cast<double*>(h->pin + o_lo);
+            h->hx_lo_dev = reinterpret_cast<double*>(dev + o_lo);
+            h->hx_hi = reinterpret_cast<double*>(h->pin + o_hi);
+            h->hx_hi_dev = reinterpret_cast<double*>(dev + o_hi);
+            h->hx_c = h->pin + o_c;
+            h->hx_c_dev = dev + o_c;
+            h->hx_u = h->pin + o_u;
+            h->hx_u_dev = dev + o_u;
+        }
+        const double tc4 = now_s();
         dispatch_n<SetupK>(h->n, h);
+        if (h->trace)
+            std::fprintf(stderr, "[rb trace] create: streams/events %.2f ms, tables %.2f ms, buffers %.2f ms, pinned %.2f ms, "
+                                 "kernel setup %.2f ms\n", (tc1 - tc0) * 1e3, (tc2 - tc1) * 1e3, (tc3 - tc2) * 1e3,
+                         (tc4 - tc3) * 1e3, (now_s() - tc4) * 1e3);
         *out = h;
         return RB_OK;
     } catch (const CudaError& ce) {
@@ -1596,7 +1653,7 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
         return RB_OK;
     }
     if (k == "small_rounds") {
-        h->use_mk = value != 0 && h->mk_blocks_per_sm > 0;
+        h->use_mk = value != 0;
         return RB_OK;
     }
     if (k == "mk_bps") {

@@ -119,6 +119,9 @@ struct rb_handle {
     bool r_ready = false;    // the result buffers already hold this solve's result
     int64_t cap_r = 0;
     // mapped pinned memory the round graph reads its start state from and writes back to
+    uint8_t* pin = nullptr;      // mapped pinned block holding h_ctr, h_state, hx, stats and result rows
+    size_t pin_bytes = 0;
+    DevRoundStats* hx_stats_own = nullptr;
     HostX* hx = nullptr;
     HostX* hx_dev = nullptr;
     DevRoundStats* hx_stats = nullptr;

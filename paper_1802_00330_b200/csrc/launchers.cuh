@@ -43,17 +43,7 @@ void SetupK<N>::run(rb_handle* h) {
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_fused<N>, T, h->fused_smem), "occ");
         h->fused_blocks_per_sm = std::max(1, nb);
     }
-    // persistent small-round kernel: 256 threads, shared memory for its largest phase
-    h->mk_smem = std::max<size_t>(filter_off_xs(h->meta) + (size_t)2 * N * 256 * sizeof(double),
-                                  fused_off_tiles(h->meta) + (size_t)(256 / 32) * FusedLayout<N>::BPW *
-                                                                 FusedLayout<N>::doubles * sizeof(double));
-    h->mk_blocks_per_sm = 0;
-    if ((int)h->mk_smem <= h->smem_optin) {
-        set_max_dyn_smem(k_small_rounds<N>, h->smem_optin);
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_small_rounds<N>, 256, h->mk_smem), "occ");
-        h->mk_blocks_per_sm = nb;
-    }
-    if (h->mk_blocks_per_sm < 1) h->use_mk = false;
+
 }
 
 template <int N>
@@ -141,6 +131,19 @@ void KrawczykK<N>::run(rb_handle* h, int64_t b0, int64_t b_end, Front out, uint8
 
 template <int N>
 void SmallRoundsK<N>::run(rb_handle* h, const HsParams& prm, bool dedup, int64_t scap, cudaGraphConditionalHandle hw) {
+    if (h->mk_blocks_per_sm == 0) {  // set up on first use: 256 threads, shared memory of its largest phase
+        h->mk_smem = std::max<size_t>(filter_off_xs(h->meta) + (size_t)2 * N * 256 * sizeof(double),
+                                      fused_off_tiles(h->meta) + (size_t)(256 / 32) * FusedLayout<N>::BPW *
+                                                                     FusedLayout<N>::doubles * sizeof(double));
+        h->mk_blocks_per_sm = -1;
+        if ((int)h->mk_smem <= h->smem_optin) {
+            set_max_dyn_smem(k_small_rounds<N>, h->smem_optin);
+            int nb = 0;
+            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_small_rounds<N>, 256, h->mk_smem), "occ");
+            if (nb > 0) h->mk_blocks_per_sm = nb;
+        }
+    }
+    if (h->mk_blocks_per_sm < 1) return;  // not resident-capable: the WHILE loop runs every round
     SmallArgs a{};
     a.dedup = dedup ? 1 : 0;
     a.trace = h->trace ? h->d_trace : nullptr;

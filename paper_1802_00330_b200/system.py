@@ -18,6 +18,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import weakref
+
 import numpy as np
 
 Term = tuple  # (coeff: float, exps: tuple[int, ...])
@@ -141,7 +143,18 @@ class FlatTables:
 
 def compile_tables(spec: SystemSpec) -> FlatTables:
     """compile_system (_batch.py:156-164) for F and J: per term the coefficient
-    and its nonzero (var, exp) factors in ascending variable order."""
+    and its nonzero (var, exp) factors in ascending variable order.  Cached on the
+    spec (keyed by the identity of its term lists and the initial box bytes)."""
+    fp = (id(spec.eqs), id(spec.jac), spec.init_lo.tobytes(), spec.init_hi.tobytes())
+    cached = spec.__dict__.get("_flat_cache")
+    if cached is not None and cached[0] == fp:
+        return cached[1]
+    t = _compile_tables(spec)
+    spec.__dict__["_flat_cache"] = (fp, t)
+    return t
+
+
+def _compile_tables(spec: SystemSpec) -> FlatTables:
     n = spec.n
     polys = list(spec.eqs) + [spec.jac[i][j] for i in range(n) for j in range(n)]
     poly_off = [0]
@@ -169,9 +182,21 @@ def compile_tables(spec: SystemSpec) -> FlatTables:
     )
 
 
+_SPEC_CACHE: dict = {}  # id(PolySystem) -> (weakref, SystemSpec): solve() on the same system converts once
+
+
 def as_spec(s) -> SystemSpec:
     if isinstance(s, SystemSpec):
         return s
     if hasattr(s, "polynomials") and hasattr(s, "initial_box"):
-        return SystemSpec.from_polysystem(s)
+        hit = _SPEC_CACHE.get(id(s))
+        if hit is not None and hit[0]() is s:
+            return hit[1]
+        spec = SystemSpec.from_polysystem(s)
+        try:
+            ref = weakref.ref(s, lambda _r, k=id(s): _SPEC_CACHE.pop(k, None))
+        except TypeError:  # not weak-referenceable: no caching
+            return spec
+        _SPEC_CACHE[id(s)] = (ref, spec)
+        return spec
     raise TypeError(f"cannot interpret {type(s).__name__} as a polynomial system")

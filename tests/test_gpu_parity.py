@@ -255,6 +255,21 @@ def test_solve_vs_reference_golden(native, case, graph, fused):
     check_against_golden(case, out, meta)
 
 
+@pytest.mark.parametrize("case", solve_cases()[:12])
+def test_solve_persistent_small_rounds(native, case):
+    """The experimental persistent small-round kernel (grid barriers, ping-pong frontier)."""
+    from paper_1802_00330_b200 import bnb
+    meta = load_solve(case)
+    spec = golden_spec(meta["system"])
+    eng = bnb.engine_for(spec)
+    eng.set_option("small_rounds", 1)
+    try:
+        out = eng.solve(bnb.native_config(bnb.SolverConfig(**meta["config"])))
+    finally:
+        eng.set_option("small_rounds", 0)
+    check_against_golden(case, out, meta)
+
+
 def test_solve_returns_reference_shaped_objects(native):
     from paper_1802_00330_b200 import SolverConfig, solve
     spec = golden_spec("circle_line")
