@@ -436,7 +436,10 @@ static float elapsed(rb_handle* h, int a, int b) {
 
 // K3 classify + K1 filter (no sync)
 constexpr int kTraceRounds = 256, kTracePhases = 8;
+// + 16 words of k_hs_fused block-0 clocks, + (start, end, smid) of up to kTraceBlocks blocks
+constexpr size_t kTraceWords = (size_t)kTraceRounds * kTracePhases + 16 + 32 + 3 * kTraceBlocks;
 __global__ void k_stamp(unsigned long long* buf, const DevState* st, int round_host, int phase, int delta) {
+    if (st && (st->done || st->bail) && delta == 0) return;  // unrolled round after the end
     const int r = (st ? st->round_no : round_host) + delta;
     if (r >= 0 && r < kTraceRounds) buf[r * kTracePhases + phase] = gtimer();
 }
@@ -446,7 +449,7 @@ static void stamp(rb_handle* h, const DevState* st, int round_host, int phase, i
 }
 static void trace_report(rb_handle* h, int rounds) {
     if (!h->trace) return;
-    std::vector<unsigned long long> t((size_t)kTraceRounds * kTracePhases + 16);
+    std::vector<unsigned long long> t(kTraceWords);
     ck(cudaMemcpy(t.data(), h->d_trace, t.size() * 8, cudaMemcpyDeviceToHost), "trace d2h");
     static const char* names[] = {"classify", "filter", "hs", "dedup", "settle", "round_end", "loop"};
     for (int r = 1; r <= std::min(rounds, kTraceRounds - 1); r++) {
@@ -469,6 +472,29 @@ static void trace_report(rb_handle* h, int rounds) {
                      q[9] - q[8], (q[10] - q[0]) * 1e-3);
         std::fprintf(stderr, "[rb trace]   lin: loads %llu, scale %llu, gauss-jordan %llu, guards %llu, products %llu\n",
                      q[11] - q[5], q[12] - q[11], q[13] - q[12], q[14] - q[13], q[6] - q[14]);
+    }
+    {
+        const unsigned long long* bt = &t[(size_t)kTraceRounds * kTracePhases + 16 + 32];
+        unsigned long long t0 = ~0ull, t1 = 0;
+        int nb = 0;
+        for (int b = 0; b < kTraceBlocks; b++)
+            if (bt[3 * b] && bt[3 * b + 1]) {
+                nb++;
+                t0 = std::min(t0, bt[3 * b]);
+                t1 = std::max(t1, bt[3 * b + 1]);
+            }
+        if (nb) {
+            std::vector<double> st, en;
+            for (int b = 0; b < kTraceBlocks; b++)
+                if (bt[3 * b] && bt[3 * b + 1]) st.push_back((bt[3 * b] - t0) * 1e-3), en.push_back((bt[3 * b + 1] - t0) * 1e-3);
+            std::vector<double> s2 = st, e2 = en;
+            std::sort(s2.begin(), s2.end());
+            std::sort(e2.begin(), e2.end());
+            auto q = [](const std::vector<double>& v, double f) { return v[(size_t)(f * (v.size() - 1))]; };
+            std::fprintf(stderr, "[rb trace] last k_hs_fused blocks %d: start p0 %.1f p50 %.1f p100 %.1f, end p0 %.1f "
+                                 "p50 %.1f p90 %.1f p100 %.1f us (from first block start)\n",
+                         nb, q(s2, 0), q(s2, .5), q(s2, 1), q(e2, 0), q(e2, .5), q(e2, .9), q(e2, 1));
+        }
     }
     ck(cudaMemset(h->d_trace, 0, t.size() * 8), "trace clear");
 }
@@ -826,24 +852,35 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     const int64_t l0 = h->launches;
     h->cur = 0;
     const int64_t fcap = h->F[0].f.cap;
-    stamp(h, h->d_state, 0, 0);
-    dispatch_n<ClassifyK>(n, h, 0.0, (const DevState*)h->d_state, std::min<int64_t>(fcap, scap));
-    stamp(h, h->d_state, 0, 1);
-    dispatch_n<FilterK>(n, h, std::max<int64_t>(1, scap >> n), (int64_t*)nullptr);
-    stamp(h, h->d_state, 0, 2);
-    HsParams p = prm;
-    p.count_from_ctr = 1;
-    p.st = h->d_state;
-    launch_hs_batches(h, scap, 0, p, nullptr);
-    stamp(h, h->d_state, 0, 3);
-    if (dedup) dispatch_n<DedupInsertK>(n, h, h->F[1].f);
-    stamp(h, h->d_state, 0, 4);
-    dispatch_n<TailK>(n, h, dedup, std::min<int64_t>(fcap, 3 * scap), scap, hw);
-    stamp(h, h->d_state, 0, 6, -1);
+    // U rounds per WHILE iteration: an iteration costs ~5 us on B200 (tools/microbench/
+    // graph_nodes.cu) against ~0.8 us per kernel node, so rounds are unrolled; the
+    // rounds after the one that ends the solve find st->done / st->bail and exit at once.
+    for (int u = 0; u < h->graph_unroll; u++) {
+        stamp(h, h->d_state, 0, 0);
+        dispatch_n<ClassifyK>(n, h, 0.0, (const DevState*)h->d_state, std::min<int64_t>(fcap, scap));
+        stamp(h, h->d_state, 0, 1);
+        dispatch_n<FilterK>(n, h, std::max<int64_t>(1, scap >> n), (int64_t*)nullptr);
+        stamp(h, h->d_state, 0, 2);
+        HsParams p = prm;
+        p.count_from_ctr = 1;
+        p.st = h->d_state;
+        if (h->graph_fused_only && h->hs_fused) {  // no early-exit eval/lin/sweep nodes in the round
+            p.fused_max = LLONG_MAX;
+            p.has_cond = 0;
+            dispatch_n<HsFusedK>(n, h, (int64_t)0, p, (int64_t*)nullptr, scap);
+        } else {
+            launch_hs_batches(h, scap, 0, p, nullptr);
+        }
+        stamp(h, h->d_state, 0, 3);
+        if (dedup) dispatch_n<DedupInsertK>(n, h, h->F[1].f);
+        stamp(h, h->d_state, 0, 4);
+        dispatch_n<TailK>(n, h, dedup, std::min<int64_t>(fcap, 3 * scap), scap, hw);
+        stamp(h, h->d_state, 0, 6, -1);
+    }
     h->launches++;
     cudaGraph_t captured = nullptr;
     ck(cudaStreamEndCapture(h->st, &captured), "end capture");
-    h->graph_launches_per_round = h->launches - l0;
+    h->graph_launches_per_iter = h->launches - l0;
     h->launches = l0;
     ck(cudaGraphInstantiate(&h->graph_exec, g, 0), "graph instantiate");
     h->graph = g;
@@ -895,6 +932,8 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         (uintptr_t)prm.hs_possible, (uintptr_t)hw_bits, (uintptr_t)prm.contract_output,
         (uintptr_t)(h->use_ftab ? 1 : 0), (uintptr_t)(h->hs_fused ? 1 : 0), (uintptr_t)h->fused_rows};
     key.push_back((uintptr_t)h->hs_cond);
+    key.push_back((uintptr_t)h->graph_unroll);
+    key.push_back((uintptr_t)h->graph_fused_only);
     key.push_back((uintptr_t)h->use_mk);
     key.push_back((uintptr_t)h->mk_cap);
     key.push_back((uintptr_t)h->mk_bps);
@@ -944,7 +983,7 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         o.classify_bytes = x.boxes_in * (16 * n + 2);
         h->stats.push_back(o);
     }
-    h->launches += (int64_t)nr * h->graph_launches_per_round + 2;
+    h->launches += (int64_t)((nr + h->graph_unroll - 1) / h->graph_unroll) * h->graph_launches_per_iter + 2;
     h->cur = 0;
     h->n_cur = (int64_t)r.n_cur;
     for (int k = 0; k < 16; k++) h->h_order[k] = X.order[k];
@@ -1137,8 +1176,8 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         dalloc(&h->d_bar, 2);
         ck(cudaMemsetAsync(h->d_bar, 0, 2 * sizeof(unsigned), h->st), "barrier clear");
         if (h->trace) {
-            dalloc(&h->d_trace, (size_t)kTraceRounds * kTracePhases + 16);
-            ck(cudaMemsetAsync(h->d_trace, 0, ((size_t)kTraceRounds * kTracePhases + 16) * 8, h->st), "trace clear");
+            dalloc(&h->d_trace, kTraceWords);
+            ck(cudaMemsetAsync(h->d_trace, 0, kTraceWords * 8, h->st), "trace clear");
         }
         dalloc(&h->d_order, 16);
         reset_order(h);
@@ -1662,6 +1701,14 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     }
     if (k == "mk_cap") {
         h->mk_cap = value;
+        return RB_OK;
+    }
+    if (k == "graph_fused_only") {  // round graph: k_hs_fused for every survivor count
+        h->graph_fused_only = value != 0;
+        return RB_OK;
+    }
+    if (k == "graph_unroll") {  // rounds per WHILE iteration of the round graph
+        h->graph_unroll = (int)std::min<int64_t>(16, std::max<int64_t>(1, value));
         return RB_OK;
     }
     if (k == "hs_cond") {

@@ -145,7 +145,9 @@ struct rb_handle {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     std::vector<uintptr_t> graph_key;
-    int64_t graph_launches_per_round = 0;
+    int64_t graph_launches_per_iter = 0;
+    int graph_unroll = 3;        // rounds per WHILE iteration of the round graph
+    bool graph_fused_only = true;  // round graph: k_hs_fused for every count (no eval/lin/sweep nodes)
     // sharded protocol state
     double shard_target = 0.0;
     int64_t shard_carried = 0;

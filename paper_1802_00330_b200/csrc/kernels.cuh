@@ -20,6 +20,7 @@
 namespace rb {
 
 constexpr int MAX_N = 16;
+constexpr int kTraceBlocks = 4096;  // RB_TRACE per-block timeline capacity
 
 // ------------------------------------------------------------------ tables
 
@@ -91,7 +92,14 @@ __device__ __forceinline__ void copy_async(void* dst, const void* src, int bytes
 }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// issue the table copies (complete with cp_async_wait + a block barrier)
+__device__ inline STab issue_stab(const TabMeta& m, const uint8_t* g, uint8_t* s, bool f_only);
 __device__ inline STab load_stab(const TabMeta& m, const uint8_t* g, uint8_t* s, bool f_only) {
+    const STab t = issue_stab(m, g, s, f_only);
+    cp_async_wait();
+    return t;
+}
+__device__ inline STab issue_stab(const TabMeta& m, const uint8_t* g, uint8_t* s, bool f_only) {
     const int T = f_only ? m.TF : m.T;
     const int P = f_only ? m.n : m.P;
     const int Fc = f_only ? m.FcF : m.Fc;
@@ -105,7 +113,6 @@ __device__ inline STab load_stab(const TabMeta& m, const uint8_t* g, uint8_t* s,
     copy_async<4>(po, g + m.off_poly, 2 * (P + 1));
     copy_async<4>(fo, g + m.off_fac_off, 2 * (T + 1));
     copy_async<4>(fa, g + m.off_fac, 2 * Fc);
-    cp_async_wait();
     t.coeff = c;
     t.poly_off = po;
     t.fac_off = fo;
@@ -273,9 +280,12 @@ struct Counters {
 // Every such kernel releases its successor at once and then waits for the full
 // completion (and memory visibility) of its predecessor before touching global
 // data; because every kernel of the chain waits, completion stays transitive.
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// no-op unless the kernel was launched with a programmatic dependency
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    pdl_launch();
+    pdl_wait();
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -340,6 +350,11 @@ struct DevRoundStats {
     double width, elapsed;
 };
 
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -356,6 +371,7 @@ template <int N>
 __device__ __forceinline__ void k_classify_body(TabMeta meta, Front cur, int64_t n_cur_arg, Front next,
                                                   uint32_t* parents, Counters* ctr, double target_arg,
                                                   const DevState* st) {
+    if (st && (st->done || st->bail)) return;  // unrolled round after the end of the device loop
     const int64_t n_cur = st ? (int64_t)st->n_cur : n_cur_arg;
     const double target = st ? st->target : target_arg;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -554,18 +570,21 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_order[16];
     __shared__ unsigned s_eval[16], s_rej[16];
+    // the system tables are constant: copied before waiting on the previous kernel (PDL)
+    TermP* tp = reinterpret_cast<TermP*>(smem + filter_off_termp(meta));
+    copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
+    const STab tab = issue_stab(meta, gtab, smem, true);
+    pdl_wait();
     if (threadIdx.x < 16) {
         s_order[threadIdx.x] = (eq_order && threadIdx.x < N) ? eq_order[threadIdx.x] : (int)threadIdx.x;
         s_eval[threadIdx.x] = 0;
         s_rej[threadIdx.x] = 0;
     }
-    TermP* tp = reinterpret_cast<TermP*>(smem + filter_off_termp(meta));
-    copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
-    const STab tab = load_stab(meta, gtab, smem, true);
     const int stride = blockDim.x;
     double2* xs2 = reinterpret_cast<double2*>(smem + filter_off_xs(meta)) + threadIdx.x;
+    const unsigned long long total = ctr->n_par << N;  // read while the table copies are in flight
+    cp_async_wait();
     __syncthreads();
-    const unsigned long long total = ctr->n_par << N;
     const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
     unsigned long long ops_acc = 0, exact_acc = 0;
     for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < total; base += gstride) {
@@ -628,8 +647,8 @@ template <int N>
 __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                 const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
                                                 int64_t* tags, const int* __restrict__ eq_order) {
-    pdl_enter();
-    k_filter_body<N>(meta, gtab, cur, parents, ctr, S, tags, eq_order);
+    pdl_launch();
+    k_filter_body<N>(meta, gtab, cur, parents, ctr, S, tags, eq_order);  // waits after the table copies
 }
 
 // Next round's equation order: descending rejections per algorithmic op, from
@@ -1613,17 +1632,23 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     bool hs_on;
     const bool prof = prm.prof && blockIdx.x == 0 && threadIdx.x == 0;
     if (prof) prm.prof[0] = gtimer(), prm.prof[1] = clock64();
+    unsigned long long* btr = (prm.prof && threadIdx.x == 0 && blockIdx.x < kTraceBlocks) ? prm.prof + 48 + 3 * blockIdx.x : nullptr;
+    if (btr) btr[0] = gtimer();
+    // the system tables are constant: copied before waiting on the previous kernel (PDL),
+    // and in flight while the survivor count is read
+    const STab tab = issue_stab(meta, gtab, smem, false);
+    pdl_wait();
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
     if (prof) prm.prof[2] = clock64();
     if (prm.has_cond && blockIdx.x == 0 && threadIdx.x == 0)
         cudaGraphSetConditional(prm.big_cond, n_in > prm.fused_max ? 1u : 0u);
+    cp_async_wait();
     if (n_in < 0 || n_in > prm.fused_max) return;  // large counts: eval/lin/sweep
     if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
     if (!hs_on) {
         hs_passthrough<N>(S, n_in, out, ctr, tags);
         return;
     }
-    const STab tab = load_stab(meta, gtab, smem, false);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gi = lane / G, l = lane % G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
@@ -1832,14 +1857,19 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
         if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
     }
     if (prof) prm.prof[9] = clock64(), prm.prof[10] = gtimer();
+    if (prm.prof) __syncthreads();  // block-uniform
+    if (btr) {
+        btr[1] = gtimer();
+        btr[2] = smid();
+    }
 }
 
 template <int N>
 __global__ void __launch_bounds__(128) k_hs_fused(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
                                                   int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
                                                   int64_t* tags) {
-    pdl_enter();
-    k_hs_fused_body<N>(meta, gtab, S, n_in_arg, prm, out, ctr, tags);
+    pdl_launch();
+    k_hs_fused_body<N>(meta, gtab, S, n_in_arg, prm, out, ctr, tags);  // waits after the table copies
 }
 
 // ------------------------------------------------------------------ dedup
@@ -2115,6 +2145,7 @@ __global__ void __launch_bounds__(256) k_round_tail(Front f1, Front f0, unsigned
                                                     TabMeta meta) {
     pdl_enter();
     __shared__ int s_last;
+    if (st->done || st->bail) return;  // unrolled round after the end of the device loop
     const int64_t n = (int64_t)ctr->n_next;
     const bool compact = dedup && ctr->dups != 0;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
