@@ -435,9 +435,7 @@ static float elapsed(rb_handle* h, int a, int b) {
 }
 
 // K3 classify + K1 filter (no sync)
-constexpr int kTraceRounds = 256, kTracePhases = 8;
-// + 16 words of k_hs_fused block-0 clocks, + (start, end, smid) of up to kTraceBlocks blocks
-constexpr size_t kTraceWords = (size_t)kTraceRounds * kTracePhases + 16 + 32 + 3 * kTraceBlocks;
+
 __global__ void k_stamp(unsigned long long* buf, const DevState* st, int round_host, int phase, int delta) {
     if (st && (st->done || st->bail) && delta == 0) return;  // unrolled round after the end
     const int r = (st ? st->round_no : round_host) + delta;
@@ -474,7 +472,7 @@ static void trace_report(rb_handle* h, int rounds) {
                      q[11] - q[5], q[12] - q[11], q[13] - q[12], q[14] - q[13], q[6] - q[14]);
     }
     {
-        const unsigned long long* bt = &t[(size_t)kTraceRounds * kTracePhases + 16 + 32];
+        const unsigned long long* bt = &t[kTraceHsBlkOff];
         unsigned long long t0 = ~0ull, t1 = 0;
         int nb = 0;
         for (int b = 0; b < kTraceBlocks; b++)
@@ -494,6 +492,27 @@ static void trace_report(rb_handle* h, int rounds) {
             std::fprintf(stderr, "[rb trace] last k_hs_fused blocks %d: start p0 %.1f p50 %.1f p100 %.1f, end p0 %.1f "
                                  "p50 %.1f p90 %.1f p100 %.1f us (from first block start)\n",
                          nb, q(s2, 0), q(s2, .5), q(s2, 1), q(e2, 0), q(e2, .5), q(e2, .9), q(e2, 1));
+        }
+    }
+    {
+        const unsigned long long* bt = &t[kTraceCfOff];
+        std::vector<double> a, b, c, d;
+        unsigned long long t0 = ~0ull;
+        for (int k = 0; k < kTraceBlocks; k++)
+            if (bt[4 * k] && bt[4 * k + 3]) t0 = std::min(t0, bt[4 * k]);
+        for (int k = 0; k < kTraceBlocks; k++)
+            if (bt[4 * k] && bt[4 * k + 3]) {
+                a.push_back((bt[4 * k] - t0) * 1e-3);
+                b.push_back((bt[4 * k + 1] - t0) * 1e-3);
+                c.push_back((bt[4 * k + 2] - t0) * 1e-3);
+                d.push_back((bt[4 * k + 3] - t0) * 1e-3);
+            }
+        if (!a.empty()) {
+            for (auto* v : {&a, &b, &c, &d}) std::sort(v->begin(), v->end());
+            auto q = [](const std::vector<double>& v, double f) { return v[(size_t)(f * (v.size() - 1))]; };
+            std::fprintf(stderr, "[rb trace] last k_classify_filter blocks %zu (p50/p100 us from first start): start "
+                                 "%.1f/%.1f tables %.1f/%.1f loop %.1f/%.1f end %.1f/%.1f\n",
+                         a.size(), q(a, .5), q(a, 1), q(b, .5), q(b, 1), q(c, .5), q(c, 1), q(d, .5), q(d, 1));
         }
     }
     ck(cudaMemset(h->d_trace, 0, t.size() * 8), "trace clear");
@@ -855,16 +874,29 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     // U rounds per WHILE iteration: an iteration costs ~5 us on B200 (tools/microbench/
     // graph_nodes.cu) against ~0.8 us per kernel node, so rounds are unrolled; the
     // rounds after the one that ends the solve find st->done / st->bail and exit at once.
+    const bool fused_hs = h->graph_fused_only && h->hs_fused;
+    // exact dedup at append time needs every appender to insert: classify / k_classify_filter
+    // (carried rows) and k_hs_fused (HS outputs, pass-through)
+    const bool append_dedup = dedup && fused_hs && h->append_dedup;
+    DedupCtx dd{};
+    if (append_dedup) dd = DedupCtx{h->d_table, (unsigned long long)(h->table_slots - 1), h->d_slot, h->d_dead};
+    const bool cf = h->graph_cf && !(h->meta.ftab && h->use_ftab);
     for (int u = 0; u < h->graph_unroll; u++) {
         stamp(h, h->d_state, 0, 0);
-        dispatch_n<ClassifyK>(n, h, 0.0, (const DevState*)h->d_state, std::min<int64_t>(fcap, scap));
-        stamp(h, h->d_state, 0, 1);
-        dispatch_n<FilterK>(n, h, std::max<int64_t>(1, scap >> n), (int64_t*)nullptr);
+        if (cf) {
+            dispatch_n<ClassifyFilterK>(n, h, dd, scap);
+            stamp(h, h->d_state, 0, 1);
+        } else {
+            dispatch_n<ClassifyK>(n, h, 0.0, (const DevState*)h->d_state, std::min<int64_t>(fcap, scap), dd);
+            stamp(h, h->d_state, 0, 1);
+            dispatch_n<FilterK>(n, h, std::max<int64_t>(1, scap >> n), (int64_t*)nullptr);
+        }
         stamp(h, h->d_state, 0, 2);
         HsParams p = prm;
         p.count_from_ctr = 1;
         p.st = h->d_state;
-        if (h->graph_fused_only && h->hs_fused) {  // no early-exit eval/lin/sweep nodes in the round
+        p.dd = dd;
+        if (fused_hs) {  // no early-exit eval/lin/sweep nodes in the round
             p.fused_max = LLONG_MAX;
             p.has_cond = 0;
             dispatch_n<HsFusedK>(n, h, (int64_t)0, p, (int64_t*)nullptr, scap);
@@ -872,7 +904,7 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
             launch_hs_batches(h, scap, 0, p, nullptr);
         }
         stamp(h, h->d_state, 0, 3);
-        if (dedup) dispatch_n<DedupInsertK>(n, h, h->F[1].f);
+        if (dedup && !append_dedup) dispatch_n<DedupInsertK>(n, h, h->F[1].f);
         stamp(h, h->d_state, 0, 4);
         dispatch_n<TailK>(n, h, dedup, std::min<int64_t>(fcap, 3 * scap), scap, hw);
         stamp(h, h->d_state, 0, 6, -1);
@@ -934,6 +966,8 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     key.push_back((uintptr_t)h->hs_cond);
     key.push_back((uintptr_t)h->graph_unroll);
     key.push_back((uintptr_t)h->graph_fused_only);
+    key.push_back((uintptr_t)h->graph_cf);
+    key.push_back((uintptr_t)h->append_dedup);
     key.push_back((uintptr_t)h->use_mk);
     key.push_back((uintptr_t)h->mk_cap);
     key.push_back((uintptr_t)h->mk_bps);
@@ -1705,6 +1739,14 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     }
     if (k == "graph_fused_only") {  // round graph: k_hs_fused for every survivor count
         h->graph_fused_only = value != 0;
+        return RB_OK;
+    }
+    if (k == "graph_cf") {  // round graph: classify + filter in one kernel
+        h->graph_cf = value != 0;
+        return RB_OK;
+    }
+    if (k == "append_dedup") {  // round graph: exact dedup at append time
+        h->append_dedup = value != 0;
         return RB_OK;
     }
     if (k == "graph_unroll") {  // rounds per WHILE iteration of the round graph

@@ -148,6 +148,8 @@ struct rb_handle {
     int64_t graph_launches_per_iter = 0;
     int graph_unroll = 3;        // rounds per WHILE iteration of the round graph
     bool graph_fused_only = true;  // round graph: k_hs_fused for every count (no eval/lin/sweep nodes)
+    bool graph_cf = true;        // round graph: k_classify_filter instead of k_classify + k_filter
+    bool append_dedup = true;    // round graph: exact dedup at append time instead of k_dedup_insert
     // sharded protocol state
     double shard_target = 0.0;
     int64_t shard_carried = 0;
@@ -225,6 +227,13 @@ static void set_max_dyn_smem(K kernel, int optin) {
        "attr");
 }
 
+// RB_TRACE buffer layout (words): per-round phase stamps, k_hs_fused block-0 clocks and
+// per-block (start, end, smid), k_classify_filter per-block (start, tables, loop, end)
+constexpr int kTraceRounds = 256, kTracePhases = 8;
+constexpr size_t kTraceHsBlkOff = (size_t)kTraceRounds * kTracePhases + 16 + 32;
+constexpr size_t kTraceCfOff = kTraceHsBlkOff + 3 * (size_t)kTraceBlocks;
+constexpr size_t kTraceWords = kTraceCfOff + 4 * (size_t)kTraceBlocks;
+
 template <int N>
 struct SetupK {
     static void run(rb_handle* h);
@@ -250,7 +259,14 @@ static void klaunch(rb_handle* h, void (*k)(KArgs...), int grid, int block, size
 
 template <int N>
 struct ClassifyK {
-    static void run(rb_handle* h, double target, const DevState* st = nullptr, int64_t bound = -1);
+    static void run(rb_handle* h, double target, const DevState* st = nullptr, int64_t bound = -1,
+                    DedupCtx dd = DedupCtx{});
+};
+
+// classify + filter in one launch (round graph): at most `bound` children
+template <int N>
+struct ClassifyFilterK {
+    static void run(rb_handle* h, DedupCtx dd, int64_t bound);
 };
 
 template <int N>
@@ -337,5 +353,5 @@ struct WidthK {
 
 // every launcher template, for explicit instantiation (kinst.cu) and extern declarations (engine.cu)
 #define RB_LAUNCHERS(X, K)                                                                              \
-    X SetupK<K>; X ClassifyK<K>; X AllParentsK<K>; X FilterK<K>; X HsK<K>; X HsFusedK<K>; X KrawczykK<K>; \
+    X SetupK<K>; X ClassifyK<K>; X ClassifyFilterK<K>; X AllParentsK<K>; X FilterK<K>; X HsK<K>; X HsFusedK<K>; X KrawczykK<K>; \
     X SmallRoundsK<K>; X DedupInsertK<K>; X TailK<K>; X SettleK<K>; X DedupK<K>; X PartitionK<K>; X WidthK<K>;

@@ -296,6 +296,13 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 __device__ __forceinline__ double canon0(double v) { return __dadd_rn(v, 0.0); }  // -0 -> +0
 
+__device__ __forceinline__ void atomic_or_u8_(uint8_t* p, uint8_t v) {
+    if (!v) return;
+    const size_t a = reinterpret_cast<size_t>(p);
+    unsigned* w = reinterpret_cast<unsigned*>(a & ~size_t(3));
+    atomicOr(w, (unsigned)v << (8 * (a & 3)));
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_max(T v) {
 #pragma unroll
@@ -325,6 +332,60 @@ __device__ __forceinline__ unsigned long long warp_append(bool pred, unsigned lo
         base = __shfl_sync(0xffffffffu, base, leader);
     }
     return base + (unsigned long long)__popc(b & lanemask_lt()) * mult;
+}
+
+// ------------------------------------------------------------------ dedup at append time
+
+// Exact dedup (dedup_sorted, _batch.py:253-266) done by the thread that appends a
+// row, instead of a separate pass over the next frontier: the row is stored, made
+// visible (fence), then inserted into the open-addressing table; a thread that finds
+// an equal row already inserted marks its own row dead and ORs its flags into the
+// keeper.  The table, slot_of and dead have the layout k_dedup_insert uses, so the
+// round tail cleans up and compacts the same way.
+struct DedupCtx {
+    unsigned* table;            // nullptr: no dedup at append time
+    unsigned long long mask;
+    unsigned* slot_of;
+    uint8_t* dead;
+};
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x);
+
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// row `i` of f holds (lo[j], hi[j]) and the flags, already stored by this thread or
+// its lane group and fenced; one thread inserts it.
+template <int N>
+__device__ __forceinline__ void dedup_insert_regs(const Front& f, int64_t i, const double* lo, const double* hi,
+                                                  uint8_t cert, uint8_t uns, const DedupCtx& d, Counters* ctr) {
+    unsigned long long h = 0x9e3779b97f4a7c15ull;  // = row_hash over the stored (canonical) values
+#pragma unroll
+    for (int j = 0; j < N; j++) {
+        h = mix64(h ^ (unsigned long long)__double_as_longlong(__dadd_rn(lo[j], 0.0)));
+        h = mix64(h ^ (unsigned long long)__double_as_longlong(__dadd_rn(hi[j], 0.0)));
+    }
+    unsigned long long slot = h & d.mask;
+    bool dup = false;
+    while (true) {
+        const unsigned prev = atomicCAS(&d.table[slot], 0u, (unsigned)(i + 1));
+        if (prev == 0u) break;
+        __threadfence();  // acquire: the keeper stored and fenced its row before its CAS
+        const int64_t k = (int64_t)prev - 1;
+        bool eq = true;
+#pragma unroll
+        for (int j = 0; j < N; j++)
+            eq = eq && (ld_cg(&f.lo[j * f.cap + k]) == lo[j]) && (ld_cg(&f.hi[j * f.cap + k]) == hi[j]);
+        if (eq) {
+            dup = true;
+            atomic_or_u8_(&f.cert[k], cert);
+            atomic_or_u8_(&f.unsplit[k], uns);
+            break;
+        }
+        slot = (slot + 1) & d.mask;
+    }
+    d.dead[i] = dup ? 1 : 0;
+    d.slot_of[i] = dup ? 0xffffffffu : (unsigned)slot;
+    if (dup) atomicAdd(&ctr->dups, 1ull);
 }
 
 // ------------------------------------------------------------------ device-resident round loop state
@@ -370,7 +431,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 template <int N>
 __device__ __forceinline__ void k_classify_body(TabMeta meta, Front cur, int64_t n_cur_arg, Front next,
                                                   uint32_t* parents, Counters* ctr, double target_arg,
-                                                  const DevState* st) {
+                                                  const DevState* st, DedupCtx dd = DedupCtx{}) {
     if (st && (st->done || st->bail)) return;  // unrolled round after the end of the device loop
     const int64_t n_cur = st ? (int64_t)st->n_cur : n_cur_arg;
     const double target = st ? st->target : target_arg;
@@ -422,6 +483,10 @@ __device__ __forceinline__ void k_classify_body(TabMeta meta, Front cur, int64_t
             }
             next.cert[slot] = cert;
             next.unsplit[slot] = uns;
+            if (dd.table) {
+                __threadfence();
+                dedup_insert_regs<N>(next, (int64_t)slot, lo, hi, cert, uns, dd, ctr);
+            }
         }
         const unsigned long long ps = warp_append(valid && !carried, &ctr->n_par);
         if (valid && !carried) parents[ps] = (uint32_t)i | (exact ? 0x80000000u : 0u);
@@ -439,9 +504,9 @@ __device__ __forceinline__ void k_classify_body(TabMeta meta, Front cur, int64_t
 template <int N>
 __global__ void __launch_bounds__(256) k_classify(TabMeta meta, Front cur, int64_t n_cur_arg, Front next,
                                                   uint32_t* parents, Counters* ctr, double target_arg,
-                                                  const DevState* st) {
+                                                  const DevState* st, DedupCtx dd) {
     pdl_enter();
-    k_classify_body<N>(meta, cur, n_cur_arg, next, parents, ctr, target_arg, st);
+    k_classify_body<N>(meta, cur, n_cur_arg, next, parents, ctr, target_arg, st, dd);
 }
 
 // Parents for the rb_filter test hook: every row is a parent (no degeneracy split).
@@ -649,6 +714,156 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
                                                 int64_t* tags, const int* __restrict__ eq_order) {
     pdl_launch();
     k_filter_body<N>(meta, gtab, cur, parents, ctr, S, tags, eq_order);  // waits after the table copies
+}
+
+// K3 + K1 in one launch for the device round loop: thread per (frontier row, child).
+// Each thread classifies its row (the k_classify rules, bnb.py:249-269): a carried
+// row is appended to `next` by its child-0 thread (and inserted for exact dedup);
+// a parent's children are built and filtered as in k_filter_body.  Saves the
+// classify kernel and the parents list round trip; costs 2^n - 1 idle threads per
+// carried row, which is why only the small rounds of the round graph use it.
+template <int N>
+__global__ void __launch_bounds__(256) k_classify_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
+                                                         Front next, Counters* ctr, SBuf S, const DevState* st,
+                                                         const int* __restrict__ eq_order, DedupCtx dd,
+                                                         unsigned long long* prof) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int s_order[16];
+    __shared__ unsigned s_eval[16], s_rej[16];
+    // RB_TRACE: (start, tables ready, loop done, end) of each block
+    unsigned long long* btr = (prof && threadIdx.x == 0 && blockIdx.x < kTraceBlocks) ? prof + 4 * blockIdx.x : nullptr;
+    const unsigned long long t_start = btr ? gtimer() : 0ull;
+    TermP* tp = reinterpret_cast<TermP*>(smem + filter_off_termp(meta));
+    copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
+    const STab tab = issue_stab(meta, gtab, smem, true);
+    pdl_enter();
+    if (threadIdx.x < 16) {
+        s_order[threadIdx.x] = threadIdx.x < N ? eq_order[threadIdx.x] : (int)threadIdx.x;
+        s_eval[threadIdx.x] = 0;
+        s_rej[threadIdx.x] = 0;
+    }
+    const bool skip = st->done || st->bail;  // unrolled round after the end of the device loop
+    if (skip) btr = nullptr;
+    if (btr) btr[0] = t_start;
+    const int64_t n_cur = skip ? 0 : (int64_t)st->n_cur;
+    const double target = st->target;
+    const int stride = blockDim.x;
+    double2* xs2 = reinterpret_cast<double2*>(smem + filter_off_xs(meta)) + threadIdx.x;
+    cp_async_wait();
+    __syncthreads();
+    if (btr) btr[1] = gtimer();
+    const unsigned long long total = (unsigned long long)n_cur << N;
+    const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    unsigned long long ops_acc = 0, exact_acc = 0;
+    for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < total; base += gstride) {
+        const unsigned long long idx = base + threadIdx.x;
+        const bool valid = idx < total;
+        const int64_t p = (int64_t)(idx >> N);
+        const uint32_t c = (uint32_t)(idx & ((1ull << N) - 1));
+        bool keep = false, carried = false, parent = false;
+        double w = 0.0, wrow = 0.0;
+        double lo[N], hi[N];
+        uint8_t cert = 0, uns = 0;
+        unsigned ops = 0;
+        if (valid) {
+            ExpRange r;
+            r.init();
+            bool deg = false;
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                lo[j] = cur.lo[j * cur.cap + p];
+                hi[j] = cur.hi[j * cur.cap + p];
+                const double d = __dsub_rn(hi[j], lo[j]);
+                wrow = j == 0 ? d : (d > wrow ? d : wrow);
+            }
+            cert = cur.cert[p];
+            uns = cur.unsplit[p];
+            const bool done = (wrow <= target) || uns;
+            if (!done) {
+#pragma unroll
+                for (int j = 0; j < N; j++) {
+                    const double m = mid_of(lo[j], hi[j]);
+                    deg |= (m == lo[j]) || (m == hi[j]);
+                    r.add(lo[j]);
+                    r.add(hi[j]);
+                    r.add(m);
+                    const bool up = (c >> (N - 1 - j)) & 1u;
+                    const double cl = up ? m : lo[j], ch = up ? hi[j] : m;
+                    xs2[j * stride] = make_double2(cl, ch);
+                    const double d = __dsub_rn(ch, cl);
+                    w = j == 0 ? d : (d > w ? d : w);
+                }
+            }
+            carried = done || deg;
+            if (deg && !done) {
+                cert = 0;
+                uns = 1;
+            }
+            parent = !carried;
+            if (parent) {
+                const bool exact = !poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, r);
+                const bool sample = (blockIdx.x & 3) == 0;  // statistics from a quarter of the blocks
+                if (!exact) keep = feasible<N, Fast>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
+                else {
+                    keep = feasible<N, Exact>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
+                    exact_acc++;
+                }
+                ops_acc += ops;
+            }
+        }
+        // carried rows -> next frontier (child-0 thread of the row)
+        const bool app = valid && carried && c == 0;
+        const unsigned long long cs = warp_append(app, &ctr->n_next);
+        if (app && cs < (unsigned long long)next.cap) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                next.lo[j * next.cap + cs] = lo[j];
+                next.hi[j * next.cap + cs] = hi[j];
+            }
+            next.cert[cs] = cert;
+            next.unsplit[cs] = uns;
+            if (dd.table) {
+                __threadfence();
+                dedup_insert_regs<N>(next, (int64_t)cs, lo, hi, cert, uns, dd, ctr);
+            }
+        }
+        // survivors -> S
+        const unsigned long long slot = warp_append(keep, &ctr->n_surv);
+        if (keep && slot < (unsigned long long)S.cap) {
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                const double2 x = xs2[j * stride];
+                S.lo[j * S.cap + slot] = x.x;
+                S.hi[j * S.cap + slot] = x.y;
+            }
+        }
+        unsigned long long wb = keep ? (unsigned long long)__double_as_longlong(w) : 0ull;
+        unsigned long long wc = app ? (unsigned long long)__double_as_longlong(wrow) : 0ull;
+        wb = warp_max(wb);
+        wc = warp_max(wc);
+        const unsigned nc = __popc(__ballot_sync(0xffffffffu, app));
+        const unsigned np = __popc(__ballot_sync(0xffffffffu, valid && parent && c == 0));
+        if (lane == 0) {
+            if (wb) atomicMax(&ctr->child_wmax, wb);
+            if (wc) atomicMax(&ctr->wmax, wc);
+            if (nc) atomicAdd(&ctr->n_carried, (unsigned long long)nc);
+            if (np) atomicAdd(&ctr->n_par, (unsigned long long)np);
+        }
+    }
+    if (btr) btr[2] = gtimer();
+    ops_acc = warp_sum(ops_acc);
+    exact_acc = warp_sum(exact_acc);
+    if (lane == 0) {
+        if (ops_acc) atomicAdd(&ctr->filter_ops, ops_acc);
+        if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        if (s_eval[threadIdx.x]) atomicAdd(&ctr->f_eval[threadIdx.x], (unsigned long long)s_eval[threadIdx.x]);
+        if (s_rej[threadIdx.x]) atomicAdd(&ctr->f_rej[threadIdx.x], (unsigned long long)s_rej[threadIdx.x]);
+    }
+    if (btr) btr[3] = gtimer();
 }
 
 // Next round's equation order: descending rejections per algorithmic op, from
@@ -900,6 +1115,7 @@ struct HsParams {
     int has_cond;          // graph mode: k_hs_fused selects the eval/lin/sweep branch (IF node)
     cudaGraphConditionalHandle big_cond;
     unsigned long long* prof;  // RB_TRACE: k_hs_fused phase clocks of block 0's first box (dev aid)
+    DedupCtx dd;           // k_hs_fused / pass-through: dedup at append time (table null: off)
 };
 
 struct HsScratch {         // SoA with stride B (batch capacity)
@@ -943,7 +1159,8 @@ __device__ __forceinline__ int64_t hs_count(const HsParams& prm, const Counters*
 
 // HS off for this round: survivors join the frontier uncertified (bnb.py:580-581)
 template <int N>
-__device__ void hs_passthrough(const SBuf& S, int64_t n_in, const Front& out, Counters* ctr, int64_t* tags) {
+__device__ void hs_passthrough(const SBuf& S, int64_t n_in, const Front& out, Counters* ctr, int64_t* tags,
+                               const DedupCtx& dd = DedupCtx{}) {
     const int lane = threadIdx.x & 31;
     // pass-through: survivors join the frontier uncertified
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x < n_in;
@@ -966,6 +1183,13 @@ __device__ void hs_passthrough(const SBuf& S, int64_t n_in, const Front& out, Co
                 out.cert[slot] = 0;
                 out.unsplit[slot] = 0;
                 if (tags) tags[slot] = 2 * i;
+                if (dd.table) {
+                    double lo[N], hi[N];
+#pragma unroll
+                    for (int j = 0; j < N; j++) lo[j] = S.lo[j * S.cap + i], hi[j] = S.hi[j * S.cap + i];
+                    __threadfence();
+                    dedup_insert_regs<N>(out, (int64_t)slot, lo, hi, 0, 0, dd, ctr);
+                }
             }
         }
         unsigned long long wb = valid ? (unsigned long long)__double_as_longlong(w) : 0ull;
@@ -1607,9 +1831,12 @@ __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t 
 //          every lane folds the products left to right (the reference order) and
 //          runs the same extended division, so control flow stays group-uniform
 // The arithmetic is operation-for-operation that of the three-kernel pipeline.
+#ifndef RB_FUSED_G32
+#define RB_FUSED_G32 0
+#endif
 template <int N>
 struct FusedLayout {
-    static constexpr int G = LinLayout<N>::G;
+    static constexpr int G = (RB_FUSED_G32 && N >= 3) ? 32 : LinLayout<N>::G;
     static constexpr int BPW = 32 / G;
     static constexpr int oXl = 0, oXh = N, oXm = 2 * N;
     static constexpr int oJl = 3 * N, oJh = 3 * N + N * N;
@@ -1646,7 +1873,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     if (n_in < 0 || n_in > prm.fused_max) return;  // large counts: eval/lin/sweep
     if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
     if (!hs_on) {
-        hs_passthrough<N>(S, n_in, out, ctr, tags);
+        hs_passthrough<N>(S, n_in, out, ctr, tags, prm.dd);
         return;
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1816,7 +2043,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
         double wmax = 0.0;
         for (int q = 0; q < cnt; q++) {  // group-uniform
             const unsigned long long slot = wbase + off + q;
-            double w = 0.0;
+            double w = 0.0, w_lo = 0.0, w_hi = 0.0;
             if (l < N) {
                 double lo, hi;
                 if (use_input) {
@@ -1830,6 +2057,8 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                     hi = cur.hi;
                 }
                 w = __dsub_rn(hi, lo);
+                w_lo = lo;
+                w_hi = hi;
                 if (slot < (unsigned long long)out.cap) {
                     out.lo[l * out.cap + slot] = canon0(lo);
                     out.hi[l * out.cap + slot] = canon0(hi);
@@ -1840,6 +2069,19 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                 out.cert[slot] = cert ? 1 : 0;
                 out.unsplit[slot] = 0;
                 if (tags) tags[slot] = 2 * b + q;
+            }
+            if (prm.dd.table) {  // group-uniform: gather the row into lane 0 and insert it
+                double rlo[N], rhi[N];
+                const double mlo = canon0(w_lo), mhi = canon0(w_hi);
+#pragma unroll
+                for (int j = 0; j < N; j++) {
+                    rlo[j] = gshfl<G>(gmask, mlo, j);
+                    rhi[j] = gshfl<G>(gmask, mhi, j);
+                }
+                __threadfence();
+                __syncwarp(gmask);
+                if (l == 0 && slot < (unsigned long long)out.cap)
+                    dedup_insert_regs<N>(out, (int64_t)slot, rlo, rhi, cert ? 1 : 0, 0, prm.dd, ctr);
             }
         }
         unsigned long long wbits = (unsigned long long)__double_as_longlong(wmax);
@@ -1874,7 +2116,7 @@ __global__ void __launch_bounds__(128) k_hs_fused(TabMeta meta, const uint8_t* _
 
 // ------------------------------------------------------------------ dedup
 
-__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {  // declared above
     x ^= x >> 33;
     x *= 0xff51afd7ed558ccdull;
     x ^= x >> 33;
@@ -1903,12 +2145,7 @@ __device__ __forceinline__ bool rows_equal(const Front& f, int64_t a, int64_t b)
     return true;
 }
 
-__device__ __forceinline__ void atomic_or_u8(uint8_t* p, uint8_t v) {
-    if (!v) return;
-    const size_t a = reinterpret_cast<size_t>(p);
-    unsigned* w = reinterpret_cast<unsigned*>(a & ~size_t(3));
-    atomicOr(w, (unsigned)v << (8 * (a & 3)));
-}
+__device__ __forceinline__ void atomic_or_u8(uint8_t* p, uint8_t v) { atomic_or_u8_(p, v); }
 
 // The round's dedup runs without host knowledge of the frontier size: both
 // kernels read n_next from the counters and do nothing when the round

@@ -20,6 +20,7 @@ void SetupK<N>::run(rb_handle* h) {
                     (size_t)(T / 32) * FusedLayout<N>::BPW * FusedLayout<N>::doubles * sizeof(double);
     if ((int)mx > h->smem_optin) throw ArgError{RB_ERR_LIMIT, "system tables exceed the shared-memory budget"};
     set_max_dyn_smem(k_filter<N>, h->smem_optin);
+    set_max_dyn_smem(k_classify_filter<N>, h->smem_optin);
     set_max_dyn_smem(k_filter_tab<N>, h->smem_optin);
     set_max_dyn_smem(k_hs_eval<N>, h->smem_optin);
     set_max_dyn_smem(k_hs_lin<N>, h->smem_optin);
@@ -47,12 +48,23 @@ void SetupK<N>::run(rb_handle* h) {
 }
 
 template <int N>
-void ClassifyK<N>::run(rb_handle* h, double target, const DevState* st, int64_t bound) {
+void ClassifyK<N>::run(rb_handle* h, double target, const DevState* st, int64_t bound, DedupCtx dd) {
     Front cur = h->F[h->cur].f, next = h->F[h->cur ^ 1].f;
     const int blocks = grid_for(bound >= 0 ? bound : h->n_cur, 256, h->sms * 8);
     h->launches++;
-    klaunch(h, k_classify<N>, blocks, 256, 0, h->meta, cur, h->n_cur, next, h->parents, h->d_ctr, target, st);
+    klaunch(h, k_classify<N>, blocks, 256, 0, h->meta, cur, h->n_cur, next, h->parents, h->d_ctr, target, st, dd);
     ck(cudaGetLastError(), "classify launch");
+}
+
+template <int N>
+void ClassifyFilterK<N>::run(rb_handle* h, DedupCtx dd, int64_t bound) {
+    Front cur = h->F[h->cur].f, next = h->F[h->cur ^ 1].f;
+    const int blocks = grid_for(bound, 256, h->sms * h->filter_blocks_per_sm);
+    h->launches++;
+    klaunch(h, k_classify_filter<N>, blocks, 256, h->filter_smem, h->meta, h->d_tab, cur, next, h->d_ctr, h->S,
+            (const DevState*)h->d_state, (const int*)h->d_order, dd,
+            h->trace ? h->d_trace + kTraceCfOff : (unsigned long long*)nullptr);
+    ck(cudaGetLastError(), "classify_filter launch");
 }
 
 template <int N>
@@ -106,7 +118,7 @@ void HsFusedK<N>::run(rb_handle* h, int64_t n_in, HsParams prm, int64_t* tags, i
     const int T = h->hs_threads;
     h->launches++;
     const int64_t lanes = std::max<int64_t>(1, bound) * FusedLayout<N>::G;
-    if (h->trace) prm.prof = h->d_trace + 256 * 8;
+    if (h->trace) prm.prof = h->d_trace + (size_t)kTraceRounds * kTracePhases;
     klaunch(h, k_hs_fused<N>, grid_for(lanes, T, h->sms * h->fused_blocks_per_sm), T, h->fused_smem,
         h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
     ck(cudaGetLastError(), "hs fused launch");

@@ -396,3 +396,59 @@ def test_run_pipeline_report_equals_reference(native, case):
         st["elapsed_seconds"] = 0.0
     rep["wall_seconds"] = 0.0
     assert rep == meta["report"], case
+
+
+# ------------------------------------------------------------------ exact dedup with real duplicates
+
+def _dup_systems():
+    """Systems whose roots sit on bisection points, so that HS contracts
+    neighbouring boxes to the same box and the round's exact dedup
+    (dedup_sorted, _batch.py:253-266) removes rows and ORs flags."""
+    from paper_1802_00330_b200.system import SystemSpec, canonical
+
+    def mk(eqs, lo, hi):
+        n = len(lo)
+        return SystemSpec(n=n, eqs=[canonical([(c, tuple(e)) for c, e in eq], n) for eq in eqs],
+                          init_lo=lo, init_hi=hi)
+    return {
+        "lin2": mk([[(1.0, (1, 0)), (-1.0, (0, 1))], [(1.0, (1, 0)), (1.0, (0, 1))]], [-1, -1], [1, 1]),
+        "lin3": mk([[(1.0, (1, 0, 0)), (-1.0, (0, 1, 0))], [(1.0, (0, 1, 0)), (-1.0, (0, 0, 1))],
+                    [(1.0, (1, 0, 0)), (1.0, (0, 0, 1))]], [-1, -1, -1], [1, 1, 1]),
+        "lin2_r2": mk([[(1.0, (1, 0)), (-1.0, (0, 1))], [(1.0, (1, 0)), (1.0, (0, 1))]], [-1, -1], [3, 3]),
+        "lin2_skew": mk([[(1.0, (1, 0)), (-1.0, (0, 1))], [(1.0, (1, 0)), (1.0, (0, 1))]], [-1, -1], [1, 0.5]),
+        "lin4_r2": mk([[(1.0, (1, 0, 0, 0)), (-1.0, (0, 1, 0, 0))], [(1.0, (0, 1, 0, 0)), (-1.0, (0, 0, 1, 0))],
+                       [(1.0, (0, 0, 1, 0)), (-1.0, (0, 0, 0, 1))], [(1.0, (1, 0, 0, 0)), (1.0, (0, 0, 0, 1))]],
+                      [-1, -1, -1, -1], [3, 3, 3, 3]),
+    }
+
+
+@pytest.mark.parametrize("opts", [
+    dict(graph=1), dict(graph=1, append_dedup=0), dict(graph=1, graph_cf=0), dict(graph=1, graph_fused_only=0),
+    dict(graph=0)], ids=["device_loop", "device_loop_dedup_pass", "device_loop_classify_filter_split",
+                         "device_loop_three_kernel_hs", "host_loop"])
+@pytest.mark.parametrize("name", ["lin2", "lin3", "lin2_r2", "lin2_skew", "lin4_r2"])
+def test_solve_with_duplicates_vs_oracle(native, name, opts):
+    from paper_1802_00330_b200 import bnb
+    spec = _dup_systems()[name]
+    eng = bnb.engine_for(spec)
+    defaults = dict(graph=1, append_dedup=1, graph_cf=1, graph_fused_only=1)
+    for k, v in opts.items():
+        eng.set_option(k, v)
+    try:
+        out = eng.solve(bnb.native_config(bnb.SolverConfig(target_width=1e-6)))
+    finally:
+        for k, v in defaults.items():
+            eng.set_option(k, v)
+    ref = O.OSystem(spec.n, spec.eqs, spec.jac).solve(spec.init_lo, spec.init_hi, target_width=1e-6)
+    assert sum(int(o[8]) for o in ref["stats"]) > 0, "case must produce duplicates"
+    assert out["status"] == ref["status"]
+    assert len(out["stats"]) == len(ref["stats"])
+    for st, o in zip(out["stats"], ref["stats"]):
+        assert [st["round"], st["boxes_in"], st["boxes_after_filter"], st["boxes_after_hs"], st["dups"]] == \
+            [int(o[0]), int(o[1]), int(o[2]), int(o[3]), int(o[8])], name
+        assert bits(st["width"]) == bits(o[4])
+    order = canonical_sort(ref["lo"], ref["hi"])
+    assert_bits_equal(out["lo"], ref["lo"][order], f"{name} lo")
+    assert_bits_equal(out["hi"], ref["hi"][order], f"{name} hi")
+    assert np.array_equal(out["cert"], ref["cert"][order])
+    assert np.array_equal(out["unsplit"], ref["unsplit"][order])
