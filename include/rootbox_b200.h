@@ -214,6 +214,16 @@ int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const 
  *                 0: host-driven rounds (per-kernel CUDA-event timings in the stats). */
 int rb_set_option(rb_handle* h, const char* key, int64_t value);
 
+/* ---- system-specialised kernels ----------------------------------------------
+ * rb_create compiles the system's F equations into straight-line filter kernels
+ * (NVRTC, sm_100a; replaces the per-term walk over compile_system's tables,
+ * _batch.py:144-186, with identical operations) and caches the cubin on disk.
+ * rb_codegen_prepare fills that cache without a device (e.g. at build time).
+ * rb_codegen_active returns 1 when the handle runs the specialised kernels, 0
+ * when it runs the table kernels (reason in why).  RB_CODEGEN=0 disables it. */
+int rb_codegen_prepare(const rb_system* sys, char* err, int64_t err_len);
+int rb_codegen_active(rb_handle* h, char* why, int64_t why_len);
+
 /* ---- post-processing -----------------------------------
  * Backtracking merge of a solve result: snap_to_grid of every box, then
  * merge_to_width (rootbox/backtrack.py:118-242), in exact integer arithmetic on

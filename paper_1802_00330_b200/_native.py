@@ -118,6 +118,10 @@ def lib():
     L.rb_set_option.restype = i32
     L.rb_fp64_peak.argtypes = [i32, C.POINTER(C.c_double)]
     L.rb_fp64_peak.restype = i32
+    L.rb_codegen_prepare.argtypes = [C.POINTER(RbSystem), C.c_char_p, i64]
+    L.rb_codegen_prepare.restype = i32
+    L.rb_codegen_active.argtypes = [P, C.c_char_p, i64]
+    L.rb_codegen_active.restype = i32
     _lib = L
     return L
 
@@ -126,7 +130,7 @@ EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch"
             "rb_last_error", "rb_destroy", "rb_shard_load", "rb_round_filter", "rb_round_hs",
             "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak", "rb_set_option",
             "rb_shard_partition", "rb_shard_dedup", "rb_shard_export_device", "rb_shard_import_device",
-            "rb_merge", "rb_krawczyk"]
+            "rb_merge", "rb_krawczyk", "rb_codegen_prepare", "rb_codegen_active"]
 
 
 def _p(a):
@@ -144,6 +148,26 @@ def _check(rc, h, what):
         raise NativeError(f"{what} failed ({rc}): {msg}")
 
 
+def _rb_system(tables):
+    keep = (tables.poly_off, tables.coeff, tables.fac_off,
+            tables.fac_var if tables.fac_var.size else np.zeros(1, np.uint8),
+            tables.fac_exp if tables.fac_exp.size else np.zeros(1, np.uint8), tables.init_lo, tables.init_hi)
+    sysd = RbSystem(
+        n=tables.n, n_polys=len(tables.poly_off) - 1,
+        poly_off=_p(keep[0]), coeff=_p(keep[1]), fac_off=_p(keep[2]), fac_var=_p(keep[3]), fac_exp=_p(keep[4]),
+        init_lo=_p(keep[5]), init_hi=_p(keep[6]))
+    return sysd, keep
+
+
+def codegen_prepare(tables) -> None:
+    """Compile the system-specialised kernels into the on-disk cache (no device needed)."""
+    sysd, keep = _rb_system(tables)
+    err = C.create_string_buffer(4096)
+    rc = lib().rb_codegen_prepare(C.byref(sysd), err, len(err))
+    if rc != 0:
+        raise NativeError(f"rb_codegen_prepare failed ({rc}): {err.value.decode(errors='replace')}")
+
+
 class Engine:
     """One device-resident engine for one compiled system (rb_handle)."""
 
@@ -151,18 +175,17 @@ class Engine:
         L = lib()
         self.n = tables.n
         self.device = device
-        self._keep = (tables.poly_off, tables.coeff, tables.fac_off, tables.fac_var, tables.fac_exp,
-                      tables.init_lo, tables.init_hi)
-        sysd = RbSystem(
-            n=tables.n, n_polys=len(tables.poly_off) - 1,
-            poly_off=_p(tables.poly_off), coeff=_p(tables.coeff), fac_off=_p(tables.fac_off),
-            fac_var=_p(tables.fac_var if tables.fac_var.size else np.zeros(1, np.uint8)),
-            fac_exp=_p(tables.fac_exp if tables.fac_exp.size else np.zeros(1, np.uint8)),
-            init_lo=_p(tables.init_lo), init_hi=_p(tables.init_hi))
+        sysd, self._keep = _rb_system(tables)
         h = C.c_void_p()
         rc = L.rb_create(C.byref(sysd), int(device), C.byref(h))
         _check(rc, None, "rb_create")
         self.h = h
+
+    def codegen_active(self):
+        """(True, '') when the system-specialised kernels run, else (False, reason)."""
+        why = C.create_string_buffer(2048)
+        on = lib().rb_codegen_active(self.h, why, len(why))
+        return on == 1, why.value.decode(errors="replace")
 
     def set_option(self, key: str, value: int):
         _check(lib().rb_set_option(self.h, key.encode(), int(value)), self.h, "rb_set_option")

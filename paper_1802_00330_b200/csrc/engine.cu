@@ -967,6 +967,7 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     key.push_back((uintptr_t)h->graph_unroll);
     key.push_back((uintptr_t)h->graph_fused_only);
     key.push_back((uintptr_t)h->graph_cf);
+    key.push_back((uintptr_t)gen_on(h));
     key.push_back((uintptr_t)h->append_dedup);
     key.push_back((uintptr_t)h->use_mk);
     key.push_back((uintptr_t)h->mk_cap);
@@ -1176,6 +1177,102 @@ int rb_device_count(void) {
     return c;
 }
 
+static rbg::SystemTerms terms_of(const rb_system* sys) {
+    rbg::SystemTerms t;
+    t.n = sys->n;
+    const int P = sys->n + sys->n * sys->n;
+    t.poly_off.assign(sys->poly_off, sys->poly_off + P + 1);
+    const int T = sys->poly_off[P];
+    t.coeff.assign(sys->coeff, sys->coeff + T);
+    t.fac_off.assign(sys->fac_off, sys->fac_off + T + 1);
+    const int Fc = sys->fac_off[T];
+    t.fac_var.assign(sys->fac_var, sys->fac_var + Fc);
+    t.fac_exp.assign(sys->fac_exp, sys->fac_exp + Fc);
+    return t;
+}
+
+static int codegen_mode() {  // 0 off, 1 background compile on a cache miss, 2 synchronous
+    const char* e = std::getenv("RB_CODEGEN");
+    if (e && e[0] == '0') return 0;
+    if (e && (e[0] == 's' || e[0] == '2')) return 2;
+    return 1;
+}
+
+// Specialised kernels for this system (compiled once per machine, cached on disk).
+// A cached system loads at once; otherwise NVRTC compiles it on a background
+// thread while the table kernels run, and the specialised ones take over at the
+// next API call after it finishes (codegen_poll).  Both are device code with
+// identical results; rb_codegen_active reports which one is in use.
+static void codegen_setup(rb_handle* h, const rb_system* sys) {
+    h->terms = terms_of(sys);
+    const int mode = codegen_mode();
+    if (mode == 0) {
+        h->gen_err = "disabled (RB_CODEGEN=0)";
+        return;
+    }
+    rbg::Compiled c;
+    std::string err;
+    if (rbg::cached(h->terms, c) || (mode == 2 && rbg::compile(h->terms, c, err))) {
+        if (!rbg::load(c, h->dev, h->gen, err)) {
+            h->gen = rbg::Loaded{};
+            h->gen_err = err;
+        }
+        return;
+    }
+    if (mode == 2) {
+        h->gen_err = err;
+        return;
+    }
+    h->gen_err = "compiling";
+    h->gen_pending = true;
+    const rbg::SystemTerms t = h->terms;
+    h->gen_job = std::async(std::launch::async, [t]() {
+        std::pair<bool, rbg::Compiled> r;
+        std::string e;
+        r.first = rbg::compile(t, r.second, e);
+        if (!r.first) r.second.key = e;  // carries the reason
+        return r;
+    });
+}
+
+// take over the specialised kernels once the background compile is done (or wait for it)
+static void codegen_poll(rb_handle* h, bool wait = false) {
+    if (!h->gen_pending) return;
+    if (!wait && h->gen_job.wait_for(std::chrono::seconds(0)) != std::future_status::ready) return;
+    std::pair<bool, rbg::Compiled> r = h->gen_job.get();
+    h->gen_pending = false;
+    std::string err;
+    if (!r.first) {
+        h->gen_err = r.second.key;
+        return;
+    }
+    if (!rbg::load(r.second, h->dev, h->gen, err)) {
+        h->gen = rbg::Loaded{};
+        h->gen_err = err;
+        return;
+    }
+    h->gen_err.clear();
+    gen_configure(h);
+}
+
+int rb_codegen_prepare(const rb_system* sys, char* err, int64_t err_len) {
+    if (!sys) return RB_ERR_ARG;
+    if (sys->n < 1 || sys->n > RB_MAX_DIM) return RB_ERR_LIMIT;
+    rbg::Compiled c;
+    std::string e;
+    if (!rbg::compile(terms_of(sys), c, e)) {
+        if (err && err_len > 0) std::snprintf(err, (size_t)err_len, "%s", e.c_str());
+        return RB_ERR_CUDA;
+    }
+    return RB_OK;
+}
+
+int rb_codegen_active(rb_handle* h, char* why, int64_t why_len) {
+    if (!h) return RB_ERR_ARG;
+    if (why && why_len > 0) std::snprintf(why, (size_t)why_len, "%s", h->gen.ok ? "" : h->gen_err.c_str());
+    return gen_on(h) ? 1 : 0;
+}
+
 int rb_create(const rb_system* sys, int device, rb_handle** out) {
     if (!out || !sys) {
         g_create_error = "null argument";
@@ -1251,11 +1348,14 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
             h->hx_u_dev = dev + o_u;
         }
         const double tc4 = now_s();
+        codegen_setup(h, sys);
+        const double tc5 = now_s();
         dispatch_n<SetupK>(h->n, h);
         if (h->trace)
             std::fprintf(stderr, "[rb trace] create: streams/events %.2f ms, tables %.2f ms, buffers %.2f ms, pinned %.2f ms, "
-                                 "kernel setup %.2f ms\n", (tc1 - tc0) * 1e3, (tc2 - tc1) * 1e3, (tc3 - tc2) * 1e3,
-                         (tc4 - tc3) * 1e3, (now_s() - tc4) * 1e3);
+                                 "codegen %.2f ms (%s), kernel setup %.2f ms\n", (tc1 - tc0) * 1e3, (tc2 - tc1) * 1e3,
+                         (tc3 - tc2) * 1e3, (tc4 - tc3) * 1e3, (tc5 - tc4) * 1e3,
+                         h->gen.ok ? "specialised kernels" : h->gen_err.c_str(), (now_s() - tc5) * 1e3);
         *out = h;
         return RB_OK;
     } catch (const CudaError& ce) {
@@ -1283,6 +1383,7 @@ int rb_solve(rb_handle* h, const rb_config* cfg, rb_result_info* info) {
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         solve_impl(h, cfg, info);
     })
@@ -1297,6 +1398,7 @@ int rb_fetch(rb_handle* h, double* lo, double* hi, uint8_t* cert, uint8_t* unspl
     }
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         const int64_t N = h->r_n;
         if (N > 0 && h->r_on_host) {
@@ -1322,6 +1424,7 @@ int rb_filter(rb_handle* h, const double* plo, const double* phi, int64_t P, dou
     h->have_result = false;
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         const int n = h->n;
         *M = 0;
@@ -1373,6 +1476,7 @@ int rb_hs(rb_handle* h, const double* lo, const double* hi, int64_t M, int contr
     h->have_result = false;
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         const int n = h->n;
         *M2 = 0;
@@ -1429,6 +1533,7 @@ int rb_krawczyk(rb_handle* h, const double* lo, const double* hi, int64_t M, dou
     h->have_result = false;
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         const int n = h->n;
         if (M == 0) return RB_OK;
@@ -1488,6 +1593,7 @@ int rb_shard_load(rb_handle* h, const double* lo, const double* hi, const uint8_
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         h->cur = 0;
         h->n_cur = 0;
@@ -1506,6 +1612,7 @@ int rb_round_filter(rb_handle* h, int32_t round_no, int64_t* carried, int64_t* s
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         int64_t need_s, need_f;
         plan_capacity(h, need_s, need_f);
@@ -1538,6 +1645,7 @@ int rb_round_hs(rb_handle* h, int32_t hs_on, int32_t hs_contract, int64_t* n_out
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         HsParams prm{};
         prm.round_no = h->shard_round;
@@ -1573,6 +1681,7 @@ int rb_shard_export(rb_handle* h, int64_t start, int64_t count, double* lo, doub
     }
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         const int n = h->n;
         if (count == 0) return RB_OK;
@@ -1612,6 +1721,7 @@ int rb_shard_import(rb_handle* h, int64_t keep, const double* lo, const double* 
     }
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         h->n_cur = keep;
         fronts_reserve(h, keep + count);
@@ -1627,6 +1737,7 @@ int rb_shard_partition(rb_handle* h, int32_t world, int64_t* counts) {
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         fronts_reserve(h, std::max<int64_t>(h->n_cur, 1));
         dispatch_n<PartitionK>(h->n, h, (int)world, counts);
@@ -1638,6 +1749,7 @@ int rb_shard_dedup(rb_handle* h, int64_t* dups, double* width) {
     std::lock_guard<std::mutex> lk(h->mu);
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         fronts_reserve(h, std::max<int64_t>(h->n_cur, 1));
         // the dedup kernels read the row count from the counters (n_next) and skip
@@ -1669,6 +1781,7 @@ int rb_shard_export_device(rb_handle* h, int64_t start, int64_t count, double* d
     }
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         if (count == 0) return RB_OK;
         Front f = h->F[h->cur].f, sub = f;
@@ -1694,6 +1807,7 @@ int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const 
     }
     RB_GUARD(h, {
         ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
         PoolScope ps(h);
         h->n_cur = keep;
         fronts_reserve(h, keep + count);
@@ -1740,6 +1854,16 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     if (k == "graph_fused_only") {  // round graph: k_hs_fused for every survivor count
         h->graph_fused_only = value != 0;
         return RB_OK;
+    }
+    if (k == "codegen") {  // 1: system-specialised kernels when compiled, 0: table kernels
+        h->use_gen = value != 0;
+        return RB_OK;
+    }
+    if (k == "codegen_wait") {  // block until a background compile has finished and take it over
+        RB_GUARD(h, {
+            ck(cudaSetDevice(h->dev), "cudaSetDevice");
+            codegen_poll(h, true);
+        })
     }
     if (k == "graph_cf") {  // round graph: classify + filter in one kernel
         h->graph_cf = value != 0;

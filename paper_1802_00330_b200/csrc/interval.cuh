@@ -18,8 +18,24 @@
 // inside the trusted band.  The kernels prove that per box with exponent-range
 // guards (see guard_* in engine.cuh) and fall back to Exact otherwise.
 #pragma once
+#ifdef __CUDACC_RTC__
+// NVRTC (system-specialised kernels, codegen.cpp): no host C++ headers
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef short int16_t;
+typedef unsigned short uint16_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long int64_t;
+typedef unsigned long uint64_t;
+#define INT_MAX 2147483647
+#define INT_MIN (-INT_MAX - 1)
+#define LLONG_MAX 9223372036854775807LL
+#define RB_KINST_TU 1
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 #include <math_constants.h>
 
 namespace rb {

@@ -13,9 +13,18 @@
 //   lo[j * cap + row], hi[j * cap + row] (float64), cert[row], unsplit[row] (u8).
 // Consecutive threads touch consecutive rows -> fully coalesced 8-byte lanes.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <climits>
 #include <cstdint>
+#endif
 #include "interval.cuh"
+
+#ifdef __CUDACC_RTC__
+// system-specialised kernels (NVRTC) are never launched with graph conditionals
+#define RB_SET_COND(h, v) ((void)(h), (void)(v))
+#else
+#define RB_SET_COND(h, v) cudaGraphSetConditional((h), (v))
+#endif
 
 namespace rb {
 
@@ -579,7 +588,21 @@ static __device__ __noinline__ ival eval_poly_packed_exact(const TermP* tp, cons
     return eval_poly_packed<Exact>(tp, t, p, xs2, stride);
 }
 
-template <int N, class A>
+// Polynomial evaluators.  TabEval interprets the flat tables copied to shared
+// memory; a system-specialised evaluator (codegen.cpp, compiled by NVRTC) has the
+// same interface with every polynomial as straight-line code and needs no tables.
+// Both perform the same operations in the same order, so results are bit-identical.
+struct TabEval {
+    static constexpr bool tables = true;
+    static constexpr bool whole_box = false;  // HS evaluates J(X) and F(x) polynomial by polynomial
+    // F equation e over x = xs2[j * stride] = (lo, hi)
+    template <class A>
+    __device__ __forceinline__ static ival feq(const TermP* tp, const STab& t, int e, const double2* xs2, int stride) {
+        return A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride) : eval_poly_packed<A>(tp, t, e, xs2, stride);
+    }
+};
+
+template <int N, class A, class EV = TabEval>
 __device__ __forceinline__ bool feasible(const TabMeta& meta, const TermP* tp, const STab& t, const double2* xs2,
                                          int stride, const int* order, unsigned* s_eval, unsigned* s_rej,
                                          bool sample, unsigned& ops) {
@@ -587,8 +610,7 @@ __device__ __forceinline__ bool feasible(const TabMeta& meta, const TermP* tp, c
 #pragma unroll 1
         for (int k = 0; k < N; k++) {
             const int e = order[k];
-            const ival v = A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride)
-                                    : eval_poly_packed<A>(tp, t, e, xs2, stride);
+            const ival v = EV::template feq<A>(tp, t, e, xs2, stride);
             ops += meta.ops_eq[e];
             if (!(v.lo <= 0.0 && 0.0 <= v.hi)) return false;
         }
@@ -606,8 +628,7 @@ __device__ __forceinline__ bool feasible(const TabMeta& meta, const TermP* tp, c
         const int e = order[k];
         bool rej = false;
         if (alive) {
-            const ival v = A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride)
-                                    : eval_poly_packed<A>(tp, t, e, xs2, stride);
+            const ival v = EV::template feq<A>(tp, t, e, xs2, stride);
             ops += meta.ops_eq[e];
             rej = !(v.lo <= 0.0 && 0.0 <= v.hi);
         }
@@ -628,7 +649,7 @@ __host__ __device__ inline int filter_off_xs(const TabMeta& m) { return filter_o
 // iff bit (n-1-j) of c is 0 (_batch.py:226-238).  Survivors are compacted by
 // warp ballot + one atomic per warp into S.  `tags` (test hook) receives the
 // child's global index p*2^n + c so the host can restore reference order.
-template <int N>
+template <int N, class EV = TabEval>
 __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                 const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
                                                 int64_t* tags, const int* __restrict__ eq_order) {
@@ -637,8 +658,11 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
     __shared__ unsigned s_eval[16], s_rej[16];
     // the system tables are constant: copied before waiting on the previous kernel (PDL)
     TermP* tp = reinterpret_cast<TermP*>(smem + filter_off_termp(meta));
-    copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
-    const STab tab = issue_stab(meta, gtab, smem, true);
+    STab tab{};
+    if constexpr (EV::tables) {
+        copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
+        tab = issue_stab(meta, gtab, smem, true);
+    }
     pdl_wait();
     if (threadIdx.x < 16) {
         s_order[threadIdx.x] = (eq_order && threadIdx.x < N) ? eq_order[threadIdx.x] : (int)threadIdx.x;
@@ -674,9 +698,9 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
                 w = j == 0 ? d : (d > w ? d : w);
             }
             const bool sample = (blockIdx.x & 3) == 0;  // statistics from a quarter of the blocks
-            if (!exact) keep = feasible<N, Fast>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
+            if (!exact) keep = feasible<N, Fast, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
             else {
-                keep = feasible<N, Exact>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
+                keep = feasible<N, Exact, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
                 exact_acc++;
             }
             ops_acc += ops;
@@ -708,12 +732,12 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
     }
 }
 
-template <int N>
+template <int N, class EV = TabEval>
 __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                 const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
                                                 int64_t* tags, const int* __restrict__ eq_order) {
     pdl_launch();
-    k_filter_body<N>(meta, gtab, cur, parents, ctr, S, tags, eq_order);  // waits after the table copies
+    k_filter_body<N, EV>(meta, gtab, cur, parents, ctr, S, tags, eq_order);  // waits after the table copies
 }
 
 // K3 + K1 in one launch for the device round loop: thread per (frontier row, child).
@@ -722,7 +746,7 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
 // a parent's children are built and filtered as in k_filter_body.  Saves the
 // classify kernel and the parents list round trip; costs 2^n - 1 idle threads per
 // carried row, which is why only the small rounds of the round graph use it.
-template <int N>
+template <int N, class EV = TabEval>
 __global__ void __launch_bounds__(256) k_classify_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                          Front next, Counters* ctr, SBuf S, const DevState* st,
                                                          const int* __restrict__ eq_order, DedupCtx dd,
@@ -734,8 +758,11 @@ __global__ void __launch_bounds__(256) k_classify_filter(TabMeta meta, const uin
     unsigned long long* btr = (prof && threadIdx.x == 0 && blockIdx.x < kTraceBlocks) ? prof + 4 * blockIdx.x : nullptr;
     const unsigned long long t_start = btr ? gtimer() : 0ull;
     TermP* tp = reinterpret_cast<TermP*>(smem + filter_off_termp(meta));
-    copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
-    const STab tab = issue_stab(meta, gtab, smem, true);
+    STab tab{};
+    if constexpr (EV::tables) {
+        copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
+        tab = issue_stab(meta, gtab, smem, true);
+    }
     pdl_enter();
     if (threadIdx.x < 16) {
         s_order[threadIdx.x] = threadIdx.x < N ? eq_order[threadIdx.x] : (int)threadIdx.x;
@@ -804,9 +831,9 @@ __global__ void __launch_bounds__(256) k_classify_filter(TabMeta meta, const uin
             if (parent) {
                 const bool exact = !poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, r);
                 const bool sample = (blockIdx.x & 3) == 0;  // statistics from a quarter of the blocks
-                if (!exact) keep = feasible<N, Fast>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
+                if (!exact) keep = feasible<N, Fast, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
                 else {
-                    keep = feasible<N, Exact>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
+                    keep = feasible<N, Exact, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
                     exact_acc++;
                 }
                 ops_acc += ops;
@@ -1200,7 +1227,7 @@ __device__ void hs_passthrough(const SBuf& S, int64_t n_in, const Front& out, Co
 
 // K2a: thread per box.  Rows [b0, b0 + B) of S.  When HS is off for this round the
 // first batch launch copies S into F_next instead (bnb.py:580-581).
-template <int N>
+template <int N, class EV = TabEval>
 __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
                                                  int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
                                                  Front out, Counters* ctr, int64_t* tags, int R) {
@@ -1217,7 +1244,8 @@ __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __
     }
     const int64_t b_end = min(n_in, b0 + W.B);
     if (b0 >= b_end) return;
-    const STab tab = load_stab(meta, gtab, smem, false);
+    STab tab{};
+    if constexpr (EV::tables) tab = load_stab(meta, gtab, smem, false);
     double* xs = reinterpret_cast<double*>(smem + stab_bytes(meta, false));
     const int stride = blockDim.x;
     double* xlo = xs + threadIdx.x;
@@ -1251,7 +1279,13 @@ __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __
         }
         const bool fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
         const bool fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
-        const int p0 = (int)((int64_t)r * P / R), p1 = (int)((int64_t)(r + 1) * P / R);
+        if constexpr (EV::whole_box) {  // specialised evaluator: all of J(X) and F(x) by this thread (R = 1)
+            if (fastJ) EV::template J<Fast>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
+            else EV::template J<Exact>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
+            if (fastF) EV::template F<Fast>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
+            else EV::template F<Exact>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
+        }
+        const int p0 = EV::whole_box ? P : (int)((int64_t)r * P / R), p1 = (int)((int64_t)(r + 1) * P / R);
 #pragma unroll 1
         for (int q = p0; q < p1; q++) {
             if (q < N * N) {
@@ -1848,7 +1882,7 @@ struct FusedLayout {
 
 __host__ __device__ inline int fused_off_tiles(const TabMeta& m) { return align16(stab_bytes(m, false)); }
 
-template <int N>
+template <int N, class EV = TabEval>
 __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
                                                   int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
                                                   int64_t* tags) {
@@ -1863,12 +1897,13 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     if (btr) btr[0] = gtimer();
     // the system tables are constant: copied before waiting on the previous kernel (PDL),
     // and in flight while the survivor count is read
-    const STab tab = issue_stab(meta, gtab, smem, false);
+    STab tab{};
+    if constexpr (EV::tables) tab = issue_stab(meta, gtab, smem, false);
     pdl_wait();
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
     if (prof) prm.prof[2] = clock64();
     if (prm.has_cond && blockIdx.x == 0 && threadIdx.x == 0)
-        cudaGraphSetConditional(prm.big_cond, n_in > prm.fused_max ? 1u : 0u);
+        RB_SET_COND(prm.big_cond, n_in > prm.fused_max ? 1u : 0u);
     cp_async_wait();
     if (n_in < 0 || n_in > prm.fused_max) return;  // large counts: eval/lin/sweep
     if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
@@ -1918,8 +1953,16 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
             }
             const bool fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
             const bool fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
+            if constexpr (EV::whole_box) {  // specialised evaluator: lane 0 of the group, straight-line code
+                if (l == 0) {
+                    if (fastJ) EV::template J<Fast>(s + L::oXl, s + L::oXh, 1, s + L::oJl, s + L::oJh, 1);
+                    else EV::template J<Exact>(s + L::oXl, s + L::oXh, 1, s + L::oJl, s + L::oJh, 1);
+                    if (fastF) EV::template F<Fast>(s + L::oXm, s + L::oXm, 1, s + L::oFl, s + L::oFh, 1);
+                    else EV::template F<Exact>(s + L::oXm, s + L::oXm, 1, s + L::oFl, s + L::oFh, 1);
+                }
+            }
 #pragma unroll 1
-            for (int q = l; q < P; q += G) {
+            for (int q = EV::whole_box ? P : l; q < P; q += G) {
                 if (q < N * N) {
                     const ival v = fastJ ? eval_poly<Fast>(tab, N + q, s + L::oXl, s + L::oXh, 1)
                                          : eval_poly_exact(tab, N + q, s + L::oXl, s + L::oXh, 1);
@@ -2106,12 +2149,12 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     }
 }
 
-template <int N>
+template <int N, class EV = TabEval>
 __global__ void __launch_bounds__(128) k_hs_fused(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
                                                   int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
                                                   int64_t* tags) {
     pdl_launch();
-    k_hs_fused_body<N>(meta, gtab, S, n_in_arg, prm, out, ctr, tags);  // waits after the table copies
+    k_hs_fused_body<N, EV>(meta, gtab, S, n_in_arg, prm, out, ctr, tags);  // waits after the table copies
 }
 
 // ------------------------------------------------------------------ dedup
@@ -2409,7 +2452,7 @@ __global__ void __launch_bounds__(256) k_round_tail(Front f1, Front f0, unsigned
     if (!s_last || threadIdx.x >= 32) return;
     __threadfence();
     const bool cont = round_end_warp(st, ctr, stats, N, s_cap, eq_order, meta);
-    if (threadIdx.x == 0) cudaGraphSetConditional(h_while, cont ? 1u : 0u);
+    if (threadIdx.x == 0) RB_SET_COND(h_while, cont ? 1u : 0u);
 }
 
 // ------------------------------------------------------------------ persistent small rounds
@@ -2528,7 +2571,7 @@ __global__ void __launch_bounds__(256) k_small_rounds(SmallArgs a) {
         st->cur = 0;
         const bool cont = !st->done && ((st->n_cur << N) <= (unsigned long long)a.graph_cap);
         st->bail = (!st->done && !cont) ? 1 : 0;
-        cudaGraphSetConditional(a.h_while, cont ? 1u : 0u);
+        RB_SET_COND(a.h_while, cont ? 1u : 0u);
     }
 }
 

@@ -44,6 +44,7 @@ void SetupK<N>::run(rb_handle* h) {
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_fused<N>, T, h->fused_smem), "occ");
         h->fused_blocks_per_sm = std::max(1, nb);
     }
+    gen_configure(h);
 
 }
 
@@ -59,11 +60,17 @@ void ClassifyK<N>::run(rb_handle* h, double target, const DevState* st, int64_t 
 template <int N>
 void ClassifyFilterK<N>::run(rb_handle* h, DedupCtx dd, int64_t bound) {
     Front cur = h->F[h->cur].f, next = h->F[h->cur ^ 1].f;
-    const int blocks = grid_for(bound, 256, h->sms * h->filter_blocks_per_sm);
     h->launches++;
-    klaunch(h, k_classify_filter<N>, blocks, 256, h->filter_smem, h->meta, h->d_tab, cur, next, h->d_ctr, h->S,
-            (const DevState*)h->d_state, (const int*)h->d_order, dd,
-            h->trace ? h->d_trace + kTraceCfOff : (unsigned long long*)nullptr);
+    unsigned long long* prof = h->trace ? h->d_trace + kTraceCfOff : (unsigned long long*)nullptr;
+    if (gen_on(h)) {
+        const int blocks = grid_for(bound, 256, h->sms * h->gen_cf_bps);
+        klaunch_k(h, h->gen.cf, blocks, 256, h->filter_smem, h->meta, (const uint8_t*)h->d_tab, cur, next, h->d_ctr,
+                  h->S, (const DevState*)h->d_state, (const int*)h->d_order, dd, prof);
+    } else {
+        const int blocks = grid_for(bound, 256, h->sms * h->filter_blocks_per_sm);
+        klaunch(h, k_classify_filter<N>, blocks, 256, h->filter_smem, h->meta, h->d_tab, cur, next, h->d_ctr, h->S,
+                (const DevState*)h->d_state, (const int*)h->d_order, dd, prof);
+    }
     ck(cudaGetLastError(), "classify_filter launch");
 }
 
@@ -88,8 +95,15 @@ void FilterK<N>::run(rb_handle* h, int64_t max_parents, int64_t* tags) {
         return;
     }
     const int64_t work = max_parents << N;
-    const int blocks = grid_for(work, h->filter_threads, h->sms * h->filter_blocks_per_sm);
     h->launches++;
+    if (gen_on(h)) {
+        const int blocks = grid_for(work, h->filter_threads, h->sms * h->gen_filter_bps);
+        klaunch_k(h, h->gen.filter, blocks, h->filter_threads, h->filter_smem, h->meta, (const uint8_t*)h->d_tab,
+                  h->F[h->cur].f, (const uint32_t*)h->parents, h->d_ctr, h->S, tags, (const int*)h->d_order);
+        ck(cudaGetLastError(), "filter launch");
+        return;
+    }
+    const int blocks = grid_for(work, h->filter_threads, h->sms * h->filter_blocks_per_sm);
     klaunch(h, k_filter<N>, blocks, h->filter_threads, h->filter_smem, h->meta, h->d_tab, h->F[h->cur].f,
                                                                      h->parents, h->d_ctr, h->S, tags, h->d_order);
     ck(cudaGetLastError(), "filter launch");
@@ -105,8 +119,12 @@ void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* 
     const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(B, batch_bound));
     const int64_t target = (int64_t)h->sms * 1024;
     const int R = (int)std::max<int64_t>(1, std::min<int64_t>(N * N + N, (target + bound - 1) / bound));
-    klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
-        h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags, R);
+    if (gen_on(h))  // specialised J(X) / F(x): one thread evaluates a whole box
+        klaunch_k(h, h->gen.hs_eval, grid_for(bound, T, h->sms * h->gen_hse_bps), T, h->eval_smem, h->meta,
+                  (const uint8_t*)h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags, 1);
+    else
+        klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
+            h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags, R);
     klaunch(h, k_hs_lin<N>, grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem, h->S, n_in, b0, prm, h->W, h->d_ctr);
     klaunch(h, k_hs_sweep<N>, grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem,
         h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
@@ -119,8 +137,12 @@ void HsFusedK<N>::run(rb_handle* h, int64_t n_in, HsParams prm, int64_t* tags, i
     h->launches++;
     const int64_t lanes = std::max<int64_t>(1, bound) * FusedLayout<N>::G;
     if (h->trace) prm.prof = h->d_trace + (size_t)kTraceRounds * kTracePhases;
-    klaunch(h, k_hs_fused<N>, grid_for(lanes, T, h->sms * h->fused_blocks_per_sm), T, h->fused_smem,
-        h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
+    if (gen_on(h) && !prm.has_cond)  // the specialised build never sets graph conditionals
+        klaunch_k(h, h->gen.hs_fused, grid_for(lanes, T, h->sms * h->gen_hsf_bps), T, h->fused_smem, h->meta,
+                  (const uint8_t*)h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
+    else
+        klaunch(h, k_hs_fused<N>, grid_for(lanes, T, h->sms * h->fused_blocks_per_sm), T, h->fused_smem,
+            h->meta, h->d_tab, h->S, n_in, prm, h->F[h->cur ^ 1].f, h->d_ctr, tags);
     ck(cudaGetLastError(), "hs fused launch");
 }
 

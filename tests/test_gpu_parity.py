@@ -84,13 +84,24 @@ FILTER_SYSTEMS = ["circle_line", "broyden_tri6", "katsura6", "eco8", "brown8", "
                   "reimer5", "noon5", "kinema", "caprasse", "katsura4", "trinks1", "redeco8"]
 
 
-@pytest.mark.parametrize("mode", [1, 0], ids=["tabulated", "direct"])
+def _set_codegen(eng, on):
+    """Select the system-specialised (NVRTC) kernels or the table kernels."""
+    if on:
+        eng.set_option("codegen_wait", 1)
+        active, why = eng.codegen_active()
+        assert active, f"specialised kernels unavailable: {why}"
+    eng.set_option("codegen", int(on))
+
+
+@pytest.mark.parametrize("mode,codegen", [(1, 0), (0, 0), (0, 1)],
+                         ids=["tabulated", "direct_tables", "direct_specialised"])
 @pytest.mark.parametrize("name", FILTER_SYSTEMS)
-def test_filter_random_cells_vs_oracle(native, name, mode):
+def test_filter_random_cells_vs_oracle(native, name, mode, codegen):
     spec = golden_spec(name)
     from paper_1802_00330_b200 import _native
     from paper_1802_00330_b200.system import compile_tables
     eng = _native.Engine(compile_tables(spec), 0)
+    _set_codegen(eng, codegen)
     eng.set_option("filter_tab", mode)
     osys = oracle_sys(name)
     for depth, seed in ((1, 1), (3, 2), (7, 3), (30, 4)):
@@ -137,12 +148,14 @@ HS_SYSTEMS = ["circle_line", "broyden_tri6", "katsura6", "eco8", "brown8", "broy
               "noon5", "kinema", "caprasse", "reimer5", "katsura8", "cyclic9", "noon9"]
 
 
+@pytest.mark.parametrize("codegen", [1, 0], ids=["specialised", "tables"])
 @pytest.mark.parametrize("fused", [2, 0], ids=["fused", "three_kernel"])
 @pytest.mark.parametrize("name", HS_SYSTEMS)
-def test_hs_random_cells_vs_oracle(native, name, fused):
+def test_hs_random_cells_vs_oracle(native, name, fused, codegen):
     spec = golden_spec(name)
     from paper_1802_00330_b200.system import compile_tables
     eng = native.Engine(compile_tables(spec), 0)
+    _set_codegen(eng, codegen)
     eng.set_option("hs_fused", fused)
     osys = oracle_sys(name)
     for depth, seed in ((2, 5), (6, 6), (12, 7), (24, 8), (40, 9)):
@@ -235,16 +248,19 @@ def check_against_golden(case, out, meta):
     assert not np.any(np.signbit(lo) & (lo == 0)) and not np.any(np.signbit(hi) & (hi == 0))
 
 
-@pytest.mark.parametrize("graph,fused", [(1, 1), (0, 1), (0, 0), (1, 2)],
-                         ids=["device_loop", "host_loop", "host_loop_three_kernel_hs", "device_loop_fused_hs"])
+@pytest.mark.parametrize("graph,fused,codegen", [(1, 1, 1), (0, 1, 1), (0, 0, 1), (1, 2, 1), (1, 1, 0), (0, 0, 0)],
+                         ids=["device_loop", "host_loop", "host_loop_three_kernel_hs", "device_loop_fused_hs",
+                              "device_loop_tables", "host_loop_three_kernel_hs_tables"])
 @pytest.mark.parametrize("case", solve_cases())
-def test_solve_vs_reference_golden(native, case, graph, fused):
+def test_solve_vs_reference_golden(native, case, graph, fused, codegen):
     """Whole solves, with the round loop on the device (CUDA graph WHILE node)
-    and host-driven, against the reference's recorded results."""
+    and host-driven, with the system-specialised and the table kernels, against
+    the reference's recorded results."""
     from paper_1802_00330_b200 import bnb
     meta = load_solve(case)
     spec = golden_spec(meta["system"])
     eng = bnb.engine_for(spec)
+    _set_codegen(eng, codegen)
     eng.set_option("graph", graph)
     eng.set_option("hs_fused", fused)
     try:
@@ -252,6 +268,7 @@ def test_solve_vs_reference_golden(native, case, graph, fused):
     finally:
         eng.set_option("graph", 1)
         eng.set_option("hs_fused", 1)
+        eng.set_option("codegen", 1)
     check_against_golden(case, out, meta)
 
 
@@ -431,6 +448,8 @@ def test_solve_with_duplicates_vs_oracle(native, name, opts):
     from paper_1802_00330_b200 import bnb
     spec = _dup_systems()[name]
     eng = bnb.engine_for(spec)
+    eng.set_option("codegen_wait", 1)  # not in the build-time cache: compiled on first use
+    assert eng.codegen_active()[0]
     defaults = dict(graph=1, append_dedup=1, graph_cf=1, graph_fused_only=1)
     for k, v in opts.items():
         eng.set_option(k, v)
