@@ -218,7 +218,8 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value);
  * rb_create compiles the system's F equations into straight-line filter kernels
  * (NVRTC, sm_100a; replaces the per-term walk over compile_system's tables,
  * _batch.py:144-186, with identical operations) and caches the cubin on disk.
- * rb_codegen_prepare fills that cache without a device (e.g. at build time).
+ * rb_codegen_prepare fills that cache without a device (e.g. at build time);
+ * on success err receives the cache key.
  * rb_codegen_active returns 1 when the handle runs the specialised kernels, 0
  * when it runs the table kernels (reason in why).  RB_CODEGEN=0 disables it. */
 int rb_codegen_prepare(const rb_system* sys, char* err, int64_t err_len);

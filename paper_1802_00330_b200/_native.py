@@ -159,13 +159,15 @@ def _rb_system(tables):
     return sysd, keep
 
 
-def codegen_prepare(tables) -> None:
-    """Compile the system-specialised kernels into the on-disk cache (no device needed)."""
+def codegen_prepare(tables) -> str:
+    """Compile the system-specialised kernels into the on-disk cache (no device
+    needed); returns the cache key."""
     sysd, keep = _rb_system(tables)
     err = C.create_string_buffer(4096)
     rc = lib().rb_codegen_prepare(C.byref(sysd), err, len(err))
     if rc != 0:
         raise NativeError(f"rb_codegen_prepare failed ({rc}): {err.value.decode(errors='replace')}")
+    return err.value.decode()
 
 
 class Engine:

@@ -450,6 +450,14 @@ static void trace_report(rb_handle* h, int rounds) {
     std::vector<unsigned long long> t(kTraceWords);
     ck(cudaMemcpy(t.data(), h->d_trace, t.size() * 8, cudaMemcpyDeviceToHost), "trace d2h");
     static const char* names[] = {"classify", "filter", "hs", "dedup", "settle", "round_end", "loop"};
+    {
+        const unsigned long long* g = &t[(size_t)(kTraceRounds - 1) * kTracePhases];
+        const unsigned long long r1 = t[(size_t)1 * kTracePhases];
+        if (g[0] && g[3] && r1)
+            std::fprintf(stderr, "[rb trace] graph: start kernel %.1f us, to round 1 %.1f us, rounds (start -> finish) "
+                                 "%.1f us, finish kernel %.1f us, total %.1f us\n", (g[1] - g[0]) * 1e-3,
+                         (r1 - g[1]) * 1e-3, (g[2] - g[1]) * 1e-3, (g[3] - g[2]) * 1e-3, (g[3] - g[0]) * 1e-3);
+    }
     for (int r = 1; r <= std::min(rounds, kTraceRounds - 1); r++) {
         const unsigned long long* p = &t[(size_t)r * kTracePhases];
         if (!p[0]) continue;
@@ -513,6 +521,40 @@ static void trace_report(rb_handle* h, int rounds) {
             std::fprintf(stderr, "[rb trace] last k_classify_filter blocks %zu (p50/p100 us from first start): start "
                                  "%.1f/%.1f tables %.1f/%.1f loop %.1f/%.1f end %.1f/%.1f\n",
                          a.size(), q(a, .5), q(a, 1), q(b, .5), q(b, 1), q(c, .5), q(c, 1), q(d, .5), q(d, 1));
+        }
+    }
+    {  // per-box k_hs_fused records of the last round that ran HS
+        const unsigned long long* br = &t[kTraceBoxAbs];
+        unsigned long long rmax = 0;
+        for (int b = 0; b < kTraceBoxes; b++)
+            if (br[8 * b + 4]) rmax = std::max(rmax, br[8 * b + 6]);
+        std::vector<int> ids;
+        for (int b = 0; b < kTraceBoxes; b++)
+            if (br[8 * b + 4] && br[8 * b + 6] == rmax) ids.push_back(b);
+        if (!ids.empty()) {
+            unsigned long long t0 = ~0ull;
+            for (int b : ids) t0 = std::min(t0, br[8 * b]);
+            std::sort(ids.begin(), ids.end(), [&](int a, int b) { return br[8 * a + 4] < br[8 * b + 4]; });
+            double ph[4] = {0, 0, 0, 0};
+            int rows_hist[17] = {0};
+            for (int b : ids) {
+                for (int k = 0; k < 4; k++) ph[k] += (br[8 * b + k + 1] - br[8 * b + k]) * 1e-3;
+                rows_hist[std::min<int>(16, br[8 * b + 5] & 0xff)]++;
+            }
+            std::fprintf(stderr, "[rb trace] round %llu k_hs_fused boxes %zu: mean us eval %.2f lin %.2f sweep %.2f out %.2f; "
+                                 "rows:", (unsigned long long)rmax, ids.size(), ph[0] / ids.size(), ph[1] / ids.size(),
+                         ph[2] / ids.size(), ph[3] / ids.size());
+            for (int r = 0; r <= 16; r++)
+                if (rows_hist[r]) std::fprintf(stderr, " %d:%d", r, rows_hist[r]);
+            std::fprintf(stderr, "\n");
+            for (int q : {(int)ids.size() / 2, (int)(ids.size() * 9 / 10), (int)ids.size() - 1}) {
+                const unsigned long long* x = &br[8 * ids[q]];
+                std::fprintf(stderr, "[rb trace]   box %d (end rank %d): start %.2f eval %.2f lin %.2f sweep %.2f out %.2f "
+                                     "end %.2f us, rows %llu kind %llu sm %llu\n",
+                             ids[q], q, (x[0] - t0) * 1e-3, (x[1] - x[0]) * 1e-3, (x[2] - x[1]) * 1e-3,
+                             (x[3] - x[2]) * 1e-3, (x[4] - x[3]) * 1e-3, (x[4] - t0) * 1e-3, x[5] & 0xff,
+                             (x[5] >> 8) & 0xff, x[5] >> 16);
+            }
         }
     }
     ck(cudaMemset(h->d_trace, 0, t.size() * 8), "trace clear");
@@ -840,8 +882,10 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
             box.lo[j] = h->init_lo[j];
             box.hi[j] = h->init_hi[j];
         }
+        stamp(h, nullptr, kTraceRounds - 1, 0);
         k_solve_start<<<1, 32, 0, h->st>>>(h->d_state, h->hx_dev, h->F[0].f, h->d_ctr, h->d_order, box, n);
         ck(cudaGetLastError(), "start launch");
+        stamp(h, nullptr, kTraceRounds - 1, 1);
     }
     if (h->use_mk) dispatch_n<SmallRoundsK>(n, h, prm, dedup, scap, hw);
     cudaStreamCaptureStatus cs;
@@ -858,10 +902,12 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     ck(cudaGraphAddNode(&node, cg, deps, ndeps, &cp), "while node");
     ck(cudaStreamUpdateCaptureDependencies(h->st, &node, 1, cudaStreamSetCaptureDependencies), "capture deps");
     cudaGraph_t body = cp.conditional.phGraph_out[0];
+    stamp(h, nullptr, kTraceRounds - 1, 2);
     k_solve_finish<<<grid_for(kHostSortRows, 256, h->sms * 4), 256, 0, h->st>>>(
         h->d_state, h->d_rstats, h->d_order, h->hx_dev, h->hx_stats_dev, h->F[0].f, n, (long long)kHostSortRows,
         h->hx_lo_dev, h->hx_hi_dev, h->hx_c_dev, h->hx_u_dev);
     ck(cudaGetLastError(), "finish launch");
+    stamp(h, nullptr, kTraceRounds - 1, 3);
     {
         cudaGraph_t top = nullptr;
         ck(cudaStreamEndCapture(h->st, &top), "end capture");
@@ -1264,6 +1310,7 @@ int rb_codegen_prepare(const rb_system* sys, char* err, int64_t err_len) {
         if (err && err_len > 0) std::snprintf(err, (size_t)err_len, "%s", e.c_str());
         return RB_ERR_CUDA;
     }
+    if (err && err_len > 0) std::snprintf(err, (size_t)err_len, "%s", c.key.c_str());  // cache key on success
     return RB_OK;
 }
 

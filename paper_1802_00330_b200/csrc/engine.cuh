@@ -242,7 +242,9 @@ static void set_max_dyn_smem(K kernel, int optin) {
 constexpr int kTraceRounds = 256, kTracePhases = 8;
 constexpr size_t kTraceHsBlkOff = (size_t)kTraceRounds * kTracePhases + 16 + 32;
 constexpr size_t kTraceCfOff = kTraceHsBlkOff + 3 * (size_t)kTraceBlocks;
-constexpr size_t kTraceWords = kTraceCfOff + 4 * (size_t)kTraceBlocks;
+constexpr size_t kTraceBoxAbs = (size_t)kTraceRounds * kTracePhases + kTraceBoxOff;
+static_assert(kTraceBoxAbs == kTraceCfOff + 4 * (size_t)kTraceBlocks, "trace layout");
+constexpr size_t kTraceWords = kTraceCfOff + 4 * (size_t)kTraceBlocks + 8 * (size_t)kTraceBoxes;
 
 template <int N>
 struct SetupK {

@@ -30,6 +30,9 @@ namespace rb {
 
 constexpr int MAX_N = 16;
 constexpr int kTraceBlocks = 4096;  // RB_TRACE per-block timeline capacity
+constexpr int kTraceBoxes = 8192;   // RB_TRACE per-box HS records (k_hs_fused)
+// per-box records start this many words after HsParams::prof
+constexpr int kTraceBoxOff = 48 + 7 * kTraceBlocks;  // after the HS and classify-filter block records
 
 // ------------------------------------------------------------------ tables
 
@@ -362,6 +365,12 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x);
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
+__device__ __forceinline__ unsigned cas_acq_rel(unsigned* p, unsigned cmp, unsigned val) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(val) : "memory");
+    return old;
+}
+
 // row `i` of f holds (lo[j], hi[j]) and the flags, already stored by this thread or
 // its lane group and fenced; one thread inserts it.
 template <int N>
@@ -376,9 +385,10 @@ __device__ __forceinline__ void dedup_insert_regs(const Front& f, int64_t i, con
     unsigned long long slot = h & d.mask;
     bool dup = false;
     while (true) {
-        const unsigned prev = atomicCAS(&d.table[slot], 0u, (unsigned)(i + 1));
+        // release: this row's stores (and the group's, ordered by __syncwarp) before the slot is
+        // published; acquire: the keeper's row is visible once its slot is seen
+        const unsigned prev = cas_acq_rel(&d.table[slot], 0u, (unsigned)(i + 1));
         if (prev == 0u) break;
-        __threadfence();  // acquire: the keeper stored and fenced its row before its CAS
         const int64_t k = (int64_t)prev - 1;
         bool eq = true;
 #pragma unroll
@@ -492,10 +502,7 @@ __device__ __forceinline__ void k_classify_body(TabMeta meta, Front cur, int64_t
             }
             next.cert[slot] = cert;
             next.unsplit[slot] = uns;
-            if (dd.table) {
-                __threadfence();
-                dedup_insert_regs<N>(next, (int64_t)slot, lo, hi, cert, uns, dd, ctr);
-            }
+            if (dd.table) dedup_insert_regs<N>(next, (int64_t)slot, lo, hi, cert, uns, dd, ctr);
         }
         const unsigned long long ps = warp_append(valid && !carried, &ctr->n_par);
         if (valid && !carried) parents[ps] = (uint32_t)i | (exact ? 0x80000000u : 0u);
@@ -851,7 +858,6 @@ __global__ void __launch_bounds__(256) k_classify_filter(TabMeta meta, const uin
             next.cert[cs] = cert;
             next.unsplit[cs] = uns;
             if (dd.table) {
-                __threadfence();
                 dedup_insert_regs<N>(next, (int64_t)cs, lo, hi, cert, uns, dd, ctr);
             }
         }
@@ -1214,7 +1220,6 @@ __device__ void hs_passthrough(const SBuf& S, int64_t n_in, const Front& out, Co
                     double lo[N], hi[N];
 #pragma unroll
                     for (int j = 0; j < N; j++) lo[j] = S.lo[j * S.cap + i], hi[j] = S.hi[j * S.cap + i];
-                    __threadfence();
                     dedup_insert_regs<N>(out, (int64_t)slot, lo, hi, 0, 0, dd, ctr);
                 }
             }
@@ -1474,7 +1479,7 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
                         c[k] = c[r];
                         c[r] = tmp;
                     }
-                const double inv = __ddiv_rn(1.0, pivot);
+                const double inv = __drcp_rn(pivot);  // RN(1/pivot) == 1.0 / pivot (linalg.py:160)
                 if (l >= k && l < 2 * N) {
                     c[k] = __dmul_rn(c[k], inv);
 #pragma unroll
@@ -1516,7 +1521,7 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
                         c[k] = c[r];
                         c[r] = tmp;
                     }
-                const double inv = __ddiv_rn(1.0, pivot);
+                const double inv = __drcp_rn(pivot);  // RN(1/pivot) == 1.0 / pivot (linalg.py:160)
                 if (l >= k && l < 2 * N) {
                     c[k] = __dmul_rn(c[k], inv);
     #pragma unroll
@@ -1942,6 +1947,8 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
             __syncwarp(gmask);
             // ---- eval: J(X) (hansen.py:61-63) and F(x) (poly.py:205-207)
             if (prof && wb0 == 0) prm.prof[4] = clock64();
+            unsigned long long* brec = (prm.prof && l == 0 && b < kTraceBoxes) ? prm.prof + kTraceBoxOff + 8 * b : nullptr;
+            if (brec) brec[0] = gtimer();
             ExpRange rx, rm;
             rx.init();
             rm.init();
@@ -1979,18 +1986,29 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
             if (l == 0 && !(fastJ && fastF)) exact_acc++;
             __syncwarp(gmask);
             if (prof && wb0 == 0) prm.prof[5] = clock64();
+            if (brec) brec[1] = gtimer();
             // ---- lin: A = mid(J)^-1, M = A J, g = A F(x)
             bool exact_lin;
             const bool singular = lin_group<N, G>(K, s + L::oA, s + L::oCol, l, gmask, exact_lin,
                                                   (prof && wb0 == 0) ? prm.prof + 11 : nullptr);
             __syncwarp(gmask);
             if (prof && wb0 == 0) prm.prof[6] = clock64();
+            if (brec) brec[2] = gtimer();
             if (singular) {
                 kind = HS_SKIP;
             } else {
                 // ---- sweep (hansen.py:91-138)
                 kind = HS_ONE;
                 const double xj = l < N ? s[L::oXm + l] : 0.0;
+                // directed reciprocals of the diagonal, off the sweep's dependency chain: lane l
+                // holds 1/M_ll for row l (the single case of div_extended_fast, recip_dir)
+                bool dfast = false;
+                ival dinv = mk(0.0, 0.0);
+                if (l < N) {
+                    const ival y = mk(s[L::oJl + l * N + l], s[L::oJh + l * N + l]);
+                    dfast = !contains_zero(y) && fabs(y.lo) > 0x1p-990 && fabs(y.hi) < 0x1p990;
+                    if (dfast) dinv = mk(recip_dir(y.hi, false), recip_dir(y.lo, true));
+                }
 #pragma unroll 1
                 for (int i = 0; i < N; i++) {
                     rows = i + 1;
@@ -2014,7 +2032,15 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                     const double xi = s[L::oXm + i];
                     const ival cur_i = mk(gshfl<G>(gmask, cur.lo, i), gshfl<G>(gmask, cur.hi, i));
                     ival q0 = mk(0.0, 0.0), q1 = mk(0.0, 0.0);
-                    const int dk = div_extended_fast(p, mii, q0, q1);
+                    const bool fi = __shfl_sync(gmask, dfast, i, G);
+                    const ival ri = mk(gshfl<G>(gmask, dinv.lo, i), gshfl<G>(gmask, dinv.hi, i));
+                    int dk;
+                    if (fi) {  // == div_extended_fast's single case
+                        q0 = gmul(p, ri);
+                        dk = DIV_SINGLE;
+                    } else {
+                        dk = div_extended(p, mii, q0, q1);
+                    }
                     if (dk == DIV_EMPTY) {
                         kind = HS_EMPTY;
                         break;
@@ -2060,6 +2086,12 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
         }
         // outputs (bnb.py:197-210): group leaders reserve slots for the warp
         if (prof && wb0 == 0) prm.prof[7] = clock64();
+        if (prm.prof && valid && l == 0 && b < kTraceBoxes) {
+            unsigned long long* br = prm.prof + kTraceBoxOff + 8 * b;
+            br[3] = gtimer();
+            br[5] = (unsigned long long)rows | ((unsigned long long)kind << 8) | ((unsigned long long)smid() << 16);
+            br[6] = prm.st ? (unsigned long long)prm.st->round_no : 0ull;
+        }
         int cnt = 0;
         bool use_input = false;
         if (valid) {
@@ -2121,8 +2153,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                     rlo[j] = gshfl<G>(gmask, mlo, j);
                     rhi[j] = gshfl<G>(gmask, mhi, j);
                 }
-                __threadfence();
-                __syncwarp(gmask);
+                __syncwarp(gmask);  // the group's row stores before lane 0's release
                 if (l == 0 && slot < (unsigned long long)out.cap)
                     dedup_insert_regs<N>(out, (int64_t)slot, rlo, rhi, cert ? 1 : 0, 0, prm.dd, ctr);
             }
@@ -2132,6 +2163,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
         if (lane == 0 && wbits) atomicMax(&ctr->wmax, wbits);
         __syncwarp();  // the tile is reused by the next box of this group
         if (prof && wb0 == 0) prm.prof[8] = clock64();
+        if (prm.prof && valid && l == 0 && b < kTraceBoxes) prm.prof[kTraceBoxOff + 8 * b + 4] = gtimer();
     }
     ops_acc = warp_sum(ops_acc);
     calls_acc = warp_sum(calls_acc);
