@@ -449,7 +449,7 @@ static void trace_report(rb_handle* h, int rounds) {
     if (!h->trace) return;
     std::vector<unsigned long long> t(kTraceWords);
     ck(cudaMemcpy(t.data(), h->d_trace, t.size() * 8, cudaMemcpyDeviceToHost), "trace d2h");
-    static const char* names[] = {"classify", "filter", "hs", "dedup", "settle", "round_end", "loop"};
+    static const char* names[] = {"classify", "filter", "hs", "dedup", "tail", "round_end", "loop"};
     {
         const unsigned long long* g = &t[(size_t)(kTraceRounds - 1) * kTracePhases];
         const unsigned long long r1 = t[(size_t)1 * kTracePhases];
@@ -464,7 +464,8 @@ static void trace_report(rb_handle* h, int rounds) {
         std::fprintf(stderr, "[rb trace] round %2d:", r);
         const unsigned long long nxt = r + 1 < kTraceRounds ? t[(size_t)(r + 1) * kTracePhases] : 0;
         for (int k = 0; k < 7; k++) {
-            const unsigned long long b = k < 6 ? p[k + 1] : nxt;
+            if (k == 5) continue;  // no stamp between the round tail and the round end (one kernel)
+            const unsigned long long b = k == 4 ? p[6] : (k < 6 ? p[k + 1] : nxt);
             if (p[k] && b >= p[k]) std::fprintf(stderr, " %s %.1f", names[k], (b - p[k]) * 1e-3);
         }
         std::fprintf(stderr, " us");
@@ -700,6 +701,7 @@ static void release_all(rb_handle* h) {
     fr(h->d_ctr);
     fr(h->d_tags);
     fr(h->d_table);
+    fr(h->d_etable);
     fr(h->d_dead);
     fr(h->d_slot);
     fr(h->d_rstats);
@@ -904,7 +906,7 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     stamp(h, nullptr, kTraceRounds - 1, 2);
     k_solve_finish<<<grid_for(kHostSortRows, 256, h->sms * 4), 256, 0, h->st>>>(
-        h->d_state, h->d_rstats, h->d_order, h->hx_dev, h->hx_stats_dev, h->F[0].f, n, (long long)kHostSortRows,
+        h->d_state, h->d_rstats, h->d_order, h->hx_dev, h->hx_stats_dev, h->F[0].f, h->F[1].f, n, (long long)kHostSortRows,
         h->hx_lo_dev, h->hx_hi_dev, h->hx_c_dev, h->hx_u_dev);
     ck(cudaGetLastError(), "finish launch");
     stamp(h, nullptr, kTraceRounds - 1, 3);
@@ -927,7 +929,43 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     DedupCtx dd{};
     if (append_dedup) dd = DedupCtx{h->d_table, (unsigned long long)(h->table_slots - 1), h->d_slot, h->d_dead};
     const bool cf = h->graph_cf && !(h->meta.ftab && h->use_ftab);
-    for (int u = 0; u < h->graph_unroll; u++) {
+    // ping-pong rounds: round u reads F[u & 1] and writes F[u & 1 ^ 1]; the last k_hs_fused
+    // block ends the round (no round-tail kernel, no frontier copy), duplicates go through
+    // the epoch table (no cleanup pass), and one small kernel per iteration sets the WHILE
+    // condition.  Needs the fused HS, the classify-filter kernel and dedup at append time.
+    const bool pp = h->pingpong && cf && fused_hs && (append_dedup || !dedup);
+    if (pp) {
+        DedupCtx de{};
+        if (dedup) de = DedupCtx{nullptr, (unsigned long long)(h->table_slots - 1), h->d_slot, h->d_dead, h->d_etable,
+                                 (const DevState*)h->d_state};
+        const int U = std::max(2, h->graph_unroll + (h->graph_unroll & 1));
+        for (int u = 0; u < U; u++) {
+            h->cur = u & 1;
+            stamp(h, h->d_state, 0, 0);
+            dispatch_n<ClassifyFilterK>(n, h, de, scap);
+            stamp(h, h->d_state, 0, 1);
+            stamp(h, h->d_state, 0, 2);
+            HsParams p = prm;
+            p.count_from_ctr = 1;
+            p.st = h->d_state;
+            p.dd = de;
+            p.fused_max = LLONG_MAX;
+            p.has_cond = 0;
+            p.round_end = 1;
+            p.rstats = h->d_rstats;
+            p.eq_order = h->d_order;
+            p.s_cap = scap;
+            dispatch_n<HsFusedK>(n, h, (int64_t)0, p, (int64_t*)nullptr, scap);
+            stamp(h, h->d_state, 0, 3);
+            stamp(h, h->d_state, 0, 4);
+            stamp(h, h->d_state, 0, 6, -1);
+        }
+        k_set_cond<<<1, 32, 0, h->st>>>(h->d_state, hw);
+        ck(cudaGetLastError(), "set cond launch");
+        h->launches++;
+        h->cur = 0;
+    }
+    for (int u = 0; u < (pp ? 0 : h->graph_unroll); u++) {
         stamp(h, h->d_state, 0, 0);
         if (cf) {
             dispatch_n<ClassifyFilterK>(n, h, dd, scap);
@@ -959,6 +997,7 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     cudaGraph_t captured = nullptr;
     ck(cudaStreamEndCapture(h->st, &captured), "end capture");
     h->graph_launches_per_iter = h->launches - l0;
+    h->graph_rounds_per_iter = pp ? std::max(2, h->graph_unroll + (h->graph_unroll & 1)) : h->graph_unroll;
     h->launches = l0;
     ck(cudaGraphInstantiate(&h->graph_exec, g, 0), "graph instantiate");
     h->graph = g;
@@ -990,6 +1029,12 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         h->cap_hx_stats = cfg->max_rounds;
     }
     if (!h->d_state) dalloc(&h->d_state, 1);
+    if (h->pingpong && (h->cap_etable < h->table_slots || !h->d_etable)) {  // epoch dedup table, zero = epoch 0
+        dalloc(&h->d_etable, h->table_slots);
+        ck(cudaMemsetAsync(h->d_etable, 0, h->table_slots * sizeof(unsigned long long), h->st), "etable memset");
+        h->cap_etable = h->table_slots;
+        h->epoch_next = 1;
+    }
     HsParams prm{};
     prm.hs_mode = 0;
     prm.hs_enable_round = cfg->hs_enable_round;
@@ -1013,6 +1058,9 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     key.push_back((uintptr_t)h->graph_unroll);
     key.push_back((uintptr_t)h->graph_fused_only);
     key.push_back((uintptr_t)h->graph_cf);
+    key.push_back((uintptr_t)h->pingpong);
+    key.push_back((uintptr_t)h->d_etable);
+    key.push_back((uintptr_t)(h->tail_blocks_per_sm * 64));
     key.push_back((uintptr_t)gen_on(h));
     key.push_back((uintptr_t)h->append_dedup);
     key.push_back((uintptr_t)h->use_mk);
@@ -1029,6 +1077,8 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     st.round_no = 1;
     st.max_rounds = cfg->max_rounds;
     st.status = RB_BUDGET_EXHAUSTED;
+    st.cur = 0;
+    st.epoch = h->epoch_next;
     HostX& X = *h->hx;
     X.start = st;
     X.rows = -1;
@@ -1064,8 +1114,12 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         o.classify_bytes = x.boxes_in * (16 * n + 2);
         h->stats.push_back(o);
     }
-    h->launches += (int64_t)((nr + h->graph_unroll - 1) / h->graph_unroll) * h->graph_launches_per_iter + 2;
-    h->cur = 0;
+    {
+        const int U = h->graph_rounds_per_iter;
+        h->launches += (int64_t)((nr + U - 1) / U) * h->graph_launches_per_iter + 2;
+    }
+    h->cur = r.cur;  // ping-pong rounds leave the frontier in F[cur]
+    h->epoch_next = r.epoch + 1;
     h->n_cur = (int64_t)r.n_cur;
     for (int k = 0; k < 16; k++) h->h_order[k] = X.order[k];
     if (r.done && X.rows >= 0) sort_on_host(h, X.rows, h->hx_lo, h->hx_hi, h->hx_c, h->hx_u);
@@ -1911,6 +1965,14 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
             ck(cudaSetDevice(h->dev), "cudaSetDevice");
             codegen_poll(h, true);
         })
+    }
+    if (k == "tail_blocks_x4") {  // round-tail grid = SMs * value / 4 blocks
+        h->tail_blocks_per_sm = std::max<int64_t>(1, value) / 4.0;
+        return RB_OK;
+    }
+    if (k == "pingpong") {  // round graph: ping-pong frontiers, round end in the HS kernel
+        h->pingpong = value != 0;
+        return RB_OK;
     }
     if (k == "graph_cf") {  // round graph: classify + filter in one kernel
         h->graph_cf = value != 0;

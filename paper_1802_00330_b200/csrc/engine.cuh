@@ -148,9 +148,15 @@ struct rb_handle {
     cudaGraphExec_t graph_exec = nullptr;
     std::vector<uintptr_t> graph_key;
     int64_t graph_launches_per_iter = 0;
-    int graph_unroll = 3;        // rounds per WHILE iteration of the round graph
+    int graph_unroll = 6;        // rounds per WHILE iteration of the round graph (measured: 6 > 4 > 2)
     bool graph_fused_only = true;  // round graph: k_hs_fused for every count (no eval/lin/sweep nodes)
     bool graph_cf = true;        // round graph: k_classify_filter instead of k_classify + k_filter
+    bool pingpong = true;        // round graph: ping-pong frontiers, round end in k_hs_fused
+    unsigned long long* d_etable = nullptr;  // epoch dedup table (ping-pong round graph)
+    size_t cap_etable = 0;
+    unsigned epoch_next = 1;
+    int graph_rounds_per_iter = 1;
+    double tail_blocks_per_sm = 2.0;  // k_round_tail grid
     // system-specialised filter kernels (codegen.cpp); the table kernels when unavailable
     rbg::SystemTerms terms;
     rbg::Loaded gen;

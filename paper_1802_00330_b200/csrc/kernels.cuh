@@ -354,11 +354,16 @@ __device__ __forceinline__ unsigned long long warp_append(bool pred, unsigned lo
 // an equal row already inserted marks its own row dead and ORs its flags into the
 // keeper.  The table, slot_of and dead have the layout k_dedup_insert uses, so the
 // round tail cleans up and compacts the same way.
+struct DevState;
 struct DedupCtx {
-    unsigned* table;            // nullptr: no dedup at append time
+    unsigned* table;            // nullptr (and etable nullptr): no dedup at append time
     unsigned long long mask;
     unsigned* slot_of;
     uint8_t* dead;
+    // epoch table (ping-pong round graph): entries (epoch << 32 | row + 1); an entry of an
+    // older epoch is empty, so the table needs no cleanup pass between rounds
+    unsigned long long* etable;
+    const DevState* st;         // epoch = st->epoch
 };
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long x);
@@ -373,6 +378,19 @@ __device__ __forceinline__ unsigned cas_acq_rel(unsigned* p, unsigned cmp, unsig
 
 // row `i` of f holds (lo[j], hi[j]) and the flags, already stored by this thread or
 // its lane group and fenced; one thread inserts it.
+__device__ __forceinline__ unsigned long long cas_acq_rel64(unsigned long long* p, unsigned long long cmp,
+                                                            unsigned long long val) {
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "l"(p), "l"(cmp), "l"(val) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned state_epoch(const DevState* st);
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <int N>
 __device__ __forceinline__ void dedup_insert_regs(const Front& f, int64_t i, const double* lo, const double* hi,
                                                   uint8_t cert, uint8_t uns, const DedupCtx& d, Counters* ctr) {
@@ -384,12 +402,25 @@ __device__ __forceinline__ void dedup_insert_regs(const Front& f, int64_t i, con
     }
     unsigned long long slot = h & d.mask;
     bool dup = false;
+    const unsigned long long ep = d.etable ? (unsigned long long)state_epoch(d.st) << 32 : 0ull;
+    unsigned long long seen = d.etable ? ld_acquire64(&d.etable[slot]) : 0ull;
     while (true) {
         // release: this row's stores (and the group's, ordered by __syncwarp) before the slot is
         // published; acquire: the keeper's row is visible once its slot is seen
-        const unsigned prev = cas_acq_rel(&d.table[slot], 0u, (unsigned)(i + 1));
-        if (prev == 0u) break;
-        const int64_t k = (int64_t)prev - 1;
+        int64_t k;
+        if (d.etable) {
+            if ((seen >> 32) != (ep >> 32)) {  // empty in this epoch: claim it
+                const unsigned long long prev = cas_acq_rel64(&d.etable[slot], seen, ep | (unsigned long long)(i + 1));
+                if (prev == seen) break;
+                seen = prev;  // lost the race: look at the winner
+                continue;
+            }
+            k = (int64_t)(seen & 0xffffffffull) - 1;
+        } else {
+            const unsigned prev = cas_acq_rel(&d.table[slot], 0u, (unsigned)(i + 1));
+            if (prev == 0u) break;
+            k = (int64_t)prev - 1;
+        }
         bool eq = true;
 #pragma unroll
         for (int j = 0; j < N; j++)
@@ -401,6 +432,7 @@ __device__ __forceinline__ void dedup_insert_regs(const Front& f, int64_t i, con
             break;
         }
         slot = (slot + 1) & d.mask;
+        if (d.etable) seen = ld_acquire64(&d.etable[slot]);
     }
     d.dead[i] = dup ? 1 : 0;
     d.slot_of[i] = dup ? 0xffffffffu : (unsigned)slot;
@@ -421,9 +453,11 @@ struct DevState {
     int done, bail, status, nrounds;
     int n_small_log2;           // bail when n_cur << n exceeds S capacity
     unsigned long long t_round_ns;
-    int cur;                    // k_small_rounds: frontier in F[cur] (0 whenever it exits)
-    int pad_;
+    int cur;                    // frontier in F[cur] (ping-pong round graph; k_small_rounds)
+    unsigned epoch;             // dedup table epoch of the round (ping-pong round graph)
 };
+
+__device__ __forceinline__ unsigned state_epoch(const DevState* st) { return *(volatile const unsigned*)&st->epoch; }
 
 struct DevRoundStats {
     long long round, boxes_in, after_filter, after_hs, children, hs_calls, filter_ops, hs_ops, dups, exact, hs_on;
@@ -502,7 +536,7 @@ __device__ __forceinline__ void k_classify_body(TabMeta meta, Front cur, int64_t
             }
             next.cert[slot] = cert;
             next.unsplit[slot] = uns;
-            if (dd.table) dedup_insert_regs<N>(next, (int64_t)slot, lo, hi, cert, uns, dd, ctr);
+            if (dd.table || dd.etable) dedup_insert_regs<N>(next, (int64_t)slot, lo, hi, cert, uns, dd, ctr);
         }
         const unsigned long long ps = warp_append(valid && !carried, &ctr->n_par);
         if (valid && !carried) parents[ps] = (uint32_t)i | (exact ? 0x80000000u : 0u);
@@ -857,7 +891,7 @@ __global__ void __launch_bounds__(256) k_classify_filter(TabMeta meta, const uin
             }
             next.cert[cs] = cert;
             next.unsplit[cs] = uns;
-            if (dd.table) {
+            if (dd.table || dd.etable) {
                 dedup_insert_regs<N>(next, (int64_t)cs, lo, hi, cert, uns, dd, ctr);
             }
         }
@@ -1149,6 +1183,12 @@ struct HsParams {
     cudaGraphConditionalHandle big_cond;
     unsigned long long* prof;  // RB_TRACE: k_hs_fused phase clocks of block 0's first box (dev aid)
     DedupCtx dd;           // k_hs_fused / pass-through: dedup at append time (table null: off)
+    // ping-pong round graph: the last k_hs_fused block ends the round (statistics,
+    // termination, dedup compaction) instead of a separate round-tail kernel
+    int round_end;
+    DevRoundStats* rstats;
+    int* eq_order;
+    int64_t s_cap;
 };
 
 struct HsScratch {         // SoA with stride B (batch capacity)
@@ -1216,7 +1256,7 @@ __device__ void hs_passthrough(const SBuf& S, int64_t n_in, const Front& out, Co
                 out.cert[slot] = 0;
                 out.unsplit[slot] = 0;
                 if (tags) tags[slot] = 2 * i;
-                if (dd.table) {
+                if (dd.table || dd.etable) {
                     double lo[N], hi[N];
 #pragma unroll
                     for (int j = 0; j < N; j++) lo[j] = S.lo[j * S.cap + i], hi[j] = S.hi[j * S.cap + i];
@@ -1870,6 +1910,70 @@ __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t 
 //          every lane folds the products left to right (the reference order) and
 //          runs the same extended division, so control flow stays group-uniform
 // The arithmetic is operation-for-operation that of the three-kernel pipeline.
+// Stable in-place removal of the dead (duplicate) rows of f[0, n) by one block:
+// chunk by chunk, every row of a chunk is read before any is written, and a row
+// moves only to a lower index, so no unread row is overwritten.
+template <int N>
+__device__ void compact_inplace_block(Front f, int64_t n, const uint8_t* dead) {
+    __shared__ unsigned s_warp[32];
+    __shared__ long long s_written;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) s_written = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool live = i < n && !dead[i];
+        double lo[N], hi[N];
+        uint8_t c = 0, u = 0;
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < N; j++) lo[j] = f.lo[j * f.cap + i], hi[j] = f.hi[j * f.cap + i];
+            c = f.cert[i];
+            u = f.unsplit[i];
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, live);
+        if (lane == 0) s_warp[warp] = __popc(b);
+        __syncthreads();
+        long long pos = s_written + __popc(b & lanemask_lt());
+        for (int w = 0; w < warp; w++) pos += s_warp[w];
+        long long tot = 0;
+        for (int w = 0; w < nw; w++) tot += s_warp[w];
+        __syncthreads();  // every read of the chunk (and of s_warp / s_written) before the writes
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < N; j++) f.lo[j * f.cap + pos] = lo[j], f.hi[j * f.cap + pos] = hi[j];
+            f.cert[pos] = c;
+            f.unsplit[pos] = u;
+        }
+        if (threadIdx.x == 0) s_written += tot;
+        __syncthreads();
+    }
+}
+
+static __device__ __noinline__ bool round_end_warp(DevState* st, Counters* ctr, DevRoundStats* stats, int n,
+                                                   int64_t s_cap, int* eq_order, const TabMeta& meta,
+                                                   bool pingpong);
+
+// End of a round inside the HS kernel (ping-pong round graph): the last block to
+// finish removes duplicate rows and runs the round end (bnb.py:322-352).
+template <int N>
+__device__ void hs_round_end(const HsParams& prm, Counters* ctr, const Front& out, const TabMeta& meta) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&ctr->tail_done, 1ull) == (unsigned long long)(gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (*(volatile unsigned long long*)&ctr->dups != 0ull)
+        compact_inplace_block<N>(out, (int64_t)*(volatile unsigned long long*)&ctr->n_next, prm.dd.dead);
+    __syncthreads();
+    if (threadIdx.x < 32)
+        round_end_warp(const_cast<DevState*>(prm.st), ctr, prm.rstats, N, prm.s_cap, prm.eq_order, meta, true);
+}
+
 #ifndef RB_FUSED_G32
 #define RB_FUSED_G32 0
 #endif
@@ -1905,6 +2009,10 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     STab tab{};
     if constexpr (EV::tables) tab = issue_stab(meta, gtab, smem, false);
     pdl_wait();
+    if (prm.round_end && (prm.st->done || prm.st->bail)) {  // unrolled round after the end of the loop
+        cp_async_wait();
+        return;
+    }
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
     if (prof) prm.prof[2] = clock64();
     if (prm.has_cond && blockIdx.x == 0 && threadIdx.x == 0)
@@ -1914,6 +2022,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
     if (!hs_on) {
         hs_passthrough<N>(S, n_in, out, ctr, tags, prm.dd);
+        if (prm.round_end) hs_round_end<N>(prm, ctr, out, meta);
         return;
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -2145,7 +2254,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                 out.unsplit[slot] = 0;
                 if (tags) tags[slot] = 2 * b + q;
             }
-            if (prm.dd.table) {  // group-uniform: gather the row into lane 0 and insert it
+            if (prm.dd.table || prm.dd.etable) {  // group-uniform: gather the row into lane 0 and insert it
                 double rlo[N], rhi[N];
                 const double mlo = canon0(w_lo), mhi = canon0(w_hi);
 #pragma unroll
@@ -2179,6 +2288,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
         btr[1] = gtimer();
         btr[2] = smid();
     }
+    if (prm.round_end) hs_round_end<N>(prm, ctr, out, meta);
 }
 
 template <int N, class EV = TabEval>
@@ -2378,7 +2488,8 @@ __global__ void k_round_end(DevState* st, Counters* ctr, DevRoundStats* stats, i
 // in parallel (the same stable descending sort as filter_order) and the counters
 // are cleared by all lanes.  Returns the WHILE condition (every lane).
 static __device__ __noinline__ bool round_end_warp(DevState* st, Counters* ctr, DevRoundStats* stats, int n,
-                                            int64_t s_cap, int* eq_order, const TabMeta& meta) {
+                                            int64_t s_cap, int* eq_order, const TabMeta& meta,
+                                            bool pingpong) {
     constexpr int W = (int)(sizeof(Counters) / 8);
     __shared__ unsigned long long sc[W];
     const int lane = threadIdx.x & 31;
@@ -2426,6 +2537,10 @@ static __device__ __noinline__ bool round_end_warp(DevState* st, Counters* ctr, 
         s.t_round_ns = now;
         s.n_cur = after;
         s.nrounds = s0.round_no;
+        if (pingpong) {  // the round's frontier is in the other buffer; fresh dedup table
+            s.cur ^= 1;
+            s.epoch += 1;
+        }
         if (after == 0) {
             s.done = 1;
             s.status = 0;  // no_real_solution
@@ -2483,7 +2598,7 @@ __global__ void __launch_bounds__(256) k_round_tail(Front f1, Front f0, unsigned
     __syncthreads();
     if (!s_last || threadIdx.x >= 32) return;
     __threadfence();
-    const bool cont = round_end_warp(st, ctr, stats, N, s_cap, eq_order, meta);
+    const bool cont = round_end_warp(st, ctr, stats, N, s_cap, eq_order, meta, false);
     if (threadIdx.x == 0) RB_SET_COND(h_while, cont ? 1u : 0u);
 }
 
@@ -2738,14 +2853,23 @@ __global__ void k_solve_start(DevState* st, const HostX* hx, Front f0, Counters*
 }
 #endif
 
+// WHILE condition of the ping-pong round graph, once per loop iteration
+#ifndef RB_KINST_TU
+__global__ void k_set_cond(const DevState* st, cudaGraphConditionalHandle h_while) {
+    pdl_enter();
+    if (threadIdx.x == 0) cudaGraphSetConditional(h_while, (st->done || st->bail) ? 0u : 1u);
+}
+#endif
+
 // final state, round statistics and order to the host; when the solve finished on the
 // device with at most max_rows boxes, also the boxes (row-major, unsorted)
 #ifndef RB_KINST_TU
 __global__ void k_solve_finish(const DevState* st, const DevRoundStats* rs, const int* order, HostX* hx,
-                               DevRoundStats* hstats, Front f0, int n, long long max_rows, double* hlo, double* hhi,
-                               uint8_t* hc, uint8_t* hu) {
+                               DevRoundStats* hstats, Front fa, Front fb, int n, long long max_rows, double* hlo,
+                               double* hhi, uint8_t* hc, uint8_t* hu) {
     pdl_enter();
     const DevState s = *st;
+    const Front f0 = s.cur ? fb : fa;  // frontier in F[cur]
     const long long N = (long long)s.n_cur;
     const bool gather = s.done && N <= max_rows;
     if (blockIdx.x == 0) {

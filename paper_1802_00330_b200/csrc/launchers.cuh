@@ -224,7 +224,7 @@ void DedupInsertK<N>::run(rb_handle* h, Front next) {
 
 template <int N>
 void TailK<N>::run(rb_handle* h, bool dedup, int64_t bound, int64_t scap, cudaGraphConditionalHandle hw) {
-    const int blocks = grid_for(bound, 256, h->sms * 2);
+    const int blocks = grid_for(bound, 256, std::max(1, (int)(h->sms * h->tail_blocks_per_sm)));
     h->launches++;
     klaunch(h, k_round_tail<N>, blocks, 256, 0, h->F[1].f, h->F[0].f, h->d_table, (const unsigned*)h->d_slot,
             (const uint8_t*)h->d_dead, dedup ? 1 : 0, h->d_state, h->d_ctr, h->d_rstats, scap, hw, h->d_order,

@@ -248,11 +248,13 @@ def check_against_golden(case, out, meta):
     assert not np.any(np.signbit(lo) & (lo == 0)) and not np.any(np.signbit(hi) & (hi == 0))
 
 
-@pytest.mark.parametrize("graph,fused,codegen", [(1, 1, 1), (0, 1, 1), (0, 0, 1), (1, 2, 1), (1, 1, 0), (0, 0, 0)],
-                         ids=["device_loop", "host_loop", "host_loop_three_kernel_hs", "device_loop_fused_hs",
-                              "device_loop_tables", "host_loop_three_kernel_hs_tables"])
+@pytest.mark.parametrize("graph,fused,codegen,pingpong",
+                         [(1, 1, 1, 1), (1, 1, 1, 0), (0, 1, 1, 1), (0, 0, 1, 1), (1, 2, 1, 1), (1, 1, 0, 1),
+                          (0, 0, 0, 1)],
+                         ids=["device_loop", "device_loop_round_tail", "host_loop", "host_loop_three_kernel_hs",
+                              "device_loop_fused_hs", "device_loop_tables", "host_loop_three_kernel_hs_tables"])
 @pytest.mark.parametrize("case", solve_cases())
-def test_solve_vs_reference_golden(native, case, graph, fused, codegen):
+def test_solve_vs_reference_golden(native, case, graph, fused, codegen, pingpong):
     """Whole solves, with the round loop on the device (CUDA graph WHILE node)
     and host-driven, with the system-specialised and the table kernels, against
     the reference's recorded results."""
@@ -263,12 +265,14 @@ def test_solve_vs_reference_golden(native, case, graph, fused, codegen):
     _set_codegen(eng, codegen)
     eng.set_option("graph", graph)
     eng.set_option("hs_fused", fused)
+    eng.set_option("pingpong", pingpong)
     try:
         out = eng.solve(bnb.native_config(bnb.SolverConfig(**meta["config"])))
     finally:
         eng.set_option("graph", 1)
         eng.set_option("hs_fused", 1)
         eng.set_option("codegen", 1)
+        eng.set_option("pingpong", 1)
     check_against_golden(case, out, meta)
 
 
@@ -440,9 +444,10 @@ def _dup_systems():
 
 
 @pytest.mark.parametrize("opts", [
-    dict(graph=1), dict(graph=1, append_dedup=0), dict(graph=1, graph_cf=0), dict(graph=1, graph_fused_only=0),
-    dict(graph=0)], ids=["device_loop", "device_loop_dedup_pass", "device_loop_classify_filter_split",
-                         "device_loop_three_kernel_hs", "host_loop"])
+    dict(graph=1), dict(graph=1, pingpong=0), dict(graph=1, pingpong=0, append_dedup=0),
+    dict(graph=1, pingpong=0, graph_cf=0), dict(graph=1, graph_fused_only=0), dict(graph=0)],
+    ids=["device_loop", "device_loop_round_tail", "device_loop_dedup_pass", "device_loop_classify_filter_split",
+         "device_loop_three_kernel_hs", "host_loop"])
 @pytest.mark.parametrize("name", ["lin2", "lin3", "lin2_r2", "lin2_skew", "lin4_r2"])
 def test_solve_with_duplicates_vs_oracle(native, name, opts):
     from paper_1802_00330_b200 import bnb
@@ -450,7 +455,7 @@ def test_solve_with_duplicates_vs_oracle(native, name, opts):
     eng = bnb.engine_for(spec)
     eng.set_option("codegen_wait", 1)  # not in the build-time cache: compiled on first use
     assert eng.codegen_active()[0]
-    defaults = dict(graph=1, append_dedup=1, graph_cf=1, graph_fused_only=1)
+    defaults = dict(graph=1, append_dedup=1, graph_cf=1, graph_fused_only=1, pingpong=1)
     for k, v in opts.items():
         eng.set_option(k, v)
     try:
