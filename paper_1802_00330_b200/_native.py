@@ -54,6 +54,11 @@ class RbResultInfo(C.Structure):
 
 
 STATS_FIELDS = [f for f, _ in RbRoundStats._fields_]
+# numpy view of an rb_round_stats array (same layout as the ctypes structure)
+_STATS_DTYPE = np.dtype({"names": STATS_FIELDS,
+                         "formats": [np.dtype(t) for _, t in RbRoundStats._fields_],
+                         "offsets": [getattr(RbRoundStats, f).offset for f in STATS_FIELDS],
+                         "itemsize": C.sizeof(RbRoundStats)})
 
 _lib = None
 
@@ -207,15 +212,16 @@ class Engine:
         L = lib()
         info = RbResultInfo()
         _check(L.rb_solve(self.h, C.byref(cfg), C.byref(info)), self.h, "rb_solve")
-        N, n = int(info.nboxes), self.n
+        N, n, nr = int(info.nboxes), self.n, int(info.nrounds)
         lo = np.empty((N, n)); hi = np.empty((N, n))
-        cert = np.empty(N, np.uint8); uns = np.empty(N, np.uint8)
-        stats = (RbRoundStats * max(1, info.nrounds))()
-        _check(L.rb_fetch(self.h, _p(lo), _p(hi), _p(cert), _p(uns), C.cast(stats, C.c_void_p)), self.h,
-               "rb_fetch")
-        st = [{f: getattr(stats[i], f) for f in STATS_FIELDS} for i in range(info.nrounds)]
-        return {"status": STATUS_NAMES[info.status], "lo": lo, "hi": hi, "cert": cert.astype(bool),
-                "unsplit": uns.astype(bool), "stats": st, "solve_seconds": info.solve_seconds,
+        flags = np.empty((2, N), np.uint8)  # cert, unsplit
+        stats = np.empty(max(1, nr), _STATS_DTYPE)
+        _check(L.rb_fetch(self.h, lo.ctypes.data, hi.ctypes.data, flags.ctypes.data, flags[1].ctypes.data,
+                          stats.ctypes.data), self.h, "rb_fetch")
+        st = [dict(zip(STATS_FIELDS, row)) for row in stats[:nr].tolist()]
+        fb = flags.view(np.bool_)
+        return {"status": STATUS_NAMES[info.status], "lo": lo, "hi": hi, "cert": fb[0], "unsplit": fb[1],
+                "stats": st, "solve_seconds": info.solve_seconds,
                 "device_ms": info.device_ms, "kernel_launches": int(info.kernel_launches)}
 
     def filter(self, plo, phi):

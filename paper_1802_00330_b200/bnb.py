@@ -287,14 +287,47 @@ class RootBoxes(Sequence):
         return f"RootBoxes({len(self)} boxes)"
 
 
+def _made(cls, **fields):
+    """Instance of one of this module's frozen dataclasses without the per-field
+    frozen __setattr__ of its __init__ (results are built per solve, on the
+    end-to-end path); same object as cls(**fields)."""
+    obj = object.__new__(cls)
+    obj.__dict__.update(fields)
+    return obj
+
+
+def _iv(lo, hi):
+    """Interval of finite engine endpoints (already valid: lo <= hi, no NaN)."""
+    iv = object.__new__(Interval)
+    object.__setattr__(iv, "lo", lo)
+    object.__setattr__(iv, "hi", hi)
+    return iv
+
+
+def _own_result(out):
+    lo, hi, cert, uns = out["lo"], out["hi"], out["cert"], out["unsplit"]
+    if lo.shape[0] > LAZY_THRESHOLD:
+        boxes = RootBoxes(lo, hi, cert, uns, (RootBox, Box, Interval))
+    else:
+        cl, ul = cert.tolist(), uns.tolist()
+        boxes = tuple(
+            _made(RootBox, box=_made(Box, intervals=tuple(map(_iv, a, b))), certified=c, unsplittable=u)
+            for a, b, c, u in zip(lo.tolist(), hi.tolist(), cl, ul))
+    stats = tuple(_made(RoundStats, round=int(st["round"]), boxes_in=int(st["boxes_in"]),
+                        boxes_after_filter=int(st["boxes_after_filter"]),
+                        boxes_after_hs=int(st["boxes_after_hs"]), width=float(st["width"]),
+                        elapsed_seconds=float(st["elapsed_seconds"]))
+                  for st in out["stats"])
+    return _made(SolveResult, status=out["status"], boxes=boxes, stats=stats)
+
+
 def solve(s, cfg=None) -> SolveResult:
     """Isolate all real roots of the system inside its initial box (bnb.py:224)."""
     out = solve_arrays(s, cfg)
     types = _reference_types(s)
     if types is None:
-        SR, RB, RS, BX, IV = SolveResult, RootBox, RoundStats, Box, Interval
-    else:
-        SR, RB, RS, BX, IV = types
+        return _own_result(out)
+    SR, RB, RS, BX, IV = types
     lo, hi, cert, uns = out["lo"], out["hi"], out["cert"], out["unsplit"]
     if lo.shape[0] > LAZY_THRESHOLD:
         boxes = RootBoxes(lo, hi, cert, uns, (RB, BX, IV))
