@@ -875,7 +875,49 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     ck(cudaGraphCreate(&g, 0), "graph create");
     cudaGraphConditionalHandle hw;
     ck(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault), "cond handle");
-    // top level: k_solve_start -> WHILE(round) -> k_solve_finish
+    const bool fused_hs = h->graph_fused_only && h->hs_fused;
+    // exact dedup at append time needs every appender to insert: classify / k_classify_filter
+    // (carried rows) and k_hs_fused (HS outputs, pass-through)
+    const bool append_dedup = dedup && fused_hs && h->append_dedup;
+    const bool cf = h->graph_cf && !(h->meta.ftab && h->use_ftab);
+    // ping-pong rounds: round u reads F[u & 1] and writes F[u & 1 ^ 1]; the last k_hs_fused
+    // block ends the round (no round-tail kernel, no frontier copy), duplicates go through
+    // the epoch table (no cleanup pass), and one small kernel per U rounds sets the WHILE
+    // condition.  Needs the fused HS, the classify-filter kernel and dedup at append time.
+    const bool pp = h->pingpong && cf && fused_hs && (append_dedup || !dedup);
+    const int U_pp = std::max(2, h->graph_unroll + (h->graph_unroll & 1));
+    auto pp_rounds = [&]() {
+        DedupCtx de{};
+        if (dedup) de = DedupCtx{nullptr, (unsigned long long)(h->table_slots - 1), h->d_slot, h->d_dead, h->d_etable,
+                                 (const DevState*)h->d_state};
+        for (int u = 0; u < U_pp; u++) {
+            h->cur = u & 1;
+            stamp(h, h->d_state, 0, 0);
+            dispatch_n<ClassifyFilterK>(n, h, de, scap);
+            stamp(h, h->d_state, 0, 1);
+            stamp(h, h->d_state, 0, 2);
+            HsParams p = prm;
+            p.count_from_ctr = 1;
+            p.st = h->d_state;
+            p.dd = de;
+            p.fused_max = LLONG_MAX;
+            p.has_cond = 0;
+            p.round_end = 1;
+            p.rstats = h->d_rstats;
+            p.eq_order = h->d_order;
+            p.s_cap = scap;
+            dispatch_n<HsFusedK>(n, h, (int64_t)0, p, (int64_t*)nullptr, scap);
+            stamp(h, h->d_state, 0, 3);
+            stamp(h, h->d_state, 0, 4);
+            stamp(h, h->d_state, 0, 6, -1);
+        }
+        k_set_cond<<<1, 32, 0, h->st>>>(h->d_state, hw);
+        ck(cudaGetLastError(), "set cond launch");
+        h->launches++;
+        h->cur = 0;
+    };
+    // top level: k_solve_start -> [U rounds] -> WHILE(U rounds) -> k_solve_finish; the first U
+    // rounds sit before the loop, so a solve that ends in them never pays for a WHILE iteration
     ck(cudaStreamBeginCaptureToGraph(h->st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
        "begin capture");
     {
@@ -890,6 +932,9 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
         stamp(h, nullptr, kTraceRounds - 1, 1);
     }
     if (h->use_mk) dispatch_n<SmallRoundsK>(n, h, prm, dedup, scap, hw);
+    const int64_t l_pro = h->launches;
+    if (pp && h->graph_prologue) pp_rounds();
+    h->launches = l_pro;
     cudaStreamCaptureStatus cs;
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
@@ -922,49 +967,9 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     // U rounds per WHILE iteration: an iteration costs ~5 us on B200 (tools/microbench/
     // graph_nodes.cu) against ~0.8 us per kernel node, so rounds are unrolled; the
     // rounds after the one that ends the solve find st->done / st->bail and exit at once.
-    const bool fused_hs = h->graph_fused_only && h->hs_fused;
-    // exact dedup at append time needs every appender to insert: classify / k_classify_filter
-    // (carried rows) and k_hs_fused (HS outputs, pass-through)
-    const bool append_dedup = dedup && fused_hs && h->append_dedup;
     DedupCtx dd{};
     if (append_dedup) dd = DedupCtx{h->d_table, (unsigned long long)(h->table_slots - 1), h->d_slot, h->d_dead};
-    const bool cf = h->graph_cf && !(h->meta.ftab && h->use_ftab);
-    // ping-pong rounds: round u reads F[u & 1] and writes F[u & 1 ^ 1]; the last k_hs_fused
-    // block ends the round (no round-tail kernel, no frontier copy), duplicates go through
-    // the epoch table (no cleanup pass), and one small kernel per iteration sets the WHILE
-    // condition.  Needs the fused HS, the classify-filter kernel and dedup at append time.
-    const bool pp = h->pingpong && cf && fused_hs && (append_dedup || !dedup);
-    if (pp) {
-        DedupCtx de{};
-        if (dedup) de = DedupCtx{nullptr, (unsigned long long)(h->table_slots - 1), h->d_slot, h->d_dead, h->d_etable,
-                                 (const DevState*)h->d_state};
-        const int U = std::max(2, h->graph_unroll + (h->graph_unroll & 1));
-        for (int u = 0; u < U; u++) {
-            h->cur = u & 1;
-            stamp(h, h->d_state, 0, 0);
-            dispatch_n<ClassifyFilterK>(n, h, de, scap);
-            stamp(h, h->d_state, 0, 1);
-            stamp(h, h->d_state, 0, 2);
-            HsParams p = prm;
-            p.count_from_ctr = 1;
-            p.st = h->d_state;
-            p.dd = de;
-            p.fused_max = LLONG_MAX;
-            p.has_cond = 0;
-            p.round_end = 1;
-            p.rstats = h->d_rstats;
-            p.eq_order = h->d_order;
-            p.s_cap = scap;
-            dispatch_n<HsFusedK>(n, h, (int64_t)0, p, (int64_t*)nullptr, scap);
-            stamp(h, h->d_state, 0, 3);
-            stamp(h, h->d_state, 0, 4);
-            stamp(h, h->d_state, 0, 6, -1);
-        }
-        k_set_cond<<<1, 32, 0, h->st>>>(h->d_state, hw);
-        ck(cudaGetLastError(), "set cond launch");
-        h->launches++;
-        h->cur = 0;
-    }
+    if (pp) pp_rounds();
     for (int u = 0; u < (pp ? 0 : h->graph_unroll); u++) {
         stamp(h, h->d_state, 0, 0);
         if (cf) {
@@ -997,7 +1002,7 @@ static void build_round_graph(rb_handle* h, const HsParams& prm, bool dedup, int
     cudaGraph_t captured = nullptr;
     ck(cudaStreamEndCapture(h->st, &captured), "end capture");
     h->graph_launches_per_iter = h->launches - l0;
-    h->graph_rounds_per_iter = pp ? std::max(2, h->graph_unroll + (h->graph_unroll & 1)) : h->graph_unroll;
+    h->graph_rounds_per_iter = pp ? U_pp : h->graph_unroll;
     h->launches = l0;
     ck(cudaGraphInstantiate(&h->graph_exec, g, 0), "graph instantiate");
     h->graph = g;
@@ -1059,6 +1064,7 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     key.push_back((uintptr_t)h->graph_fused_only);
     key.push_back((uintptr_t)h->graph_cf);
     key.push_back((uintptr_t)h->pingpong);
+    key.push_back((uintptr_t)h->graph_prologue);
     key.push_back((uintptr_t)h->d_etable);
     key.push_back((uintptr_t)(h->tail_blocks_per_sm * 64));
     key.push_back((uintptr_t)gen_on(h));
@@ -1085,6 +1091,10 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     std::atomic_thread_fence(std::memory_order_seq_cst);
     const double tg0 = now_s();
     ck(cudaGraphLaunch(h->graph_exec, h->st), "graph launch");
+    // end-of-device-work event in the same stream pass: a solve that finishes inside the
+    // graph needs no second record + synchronise round trip (solve_impl)
+    ck(cudaEventRecord(h->ev[6], h->st), "ev end");
+    h->ev_end_valid = true;
     const double tg1 = now_s();
     ck(cudaStreamSynchronize(h->st), "graph sync");
     const double tg2 = now_s();
@@ -1136,6 +1146,7 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
     h->stats.clear();
     h->have_result = false;
     h->r_ready = false;
+    h->ev_end_valid = false;
     if (cfg->max_rounds < 1) throw ArgError{RB_ERR_ARG, "max_rounds must be at least 1"};
     if (cfg->max_boxes < 1) throw ArgError{RB_ERR_ARG, "max_boxes must be at least 1"};
     h->cur = 0;
@@ -1174,6 +1185,7 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
         host_init();
     }
     if (!finished) {
+        h->ev_end_valid = false;  // host-driven rounds follow
         for (int round_no = (int)h->stats.size() + 1; round_no <= cfg->max_rounds; round_no++) {
             const double t0 = now_s();
             RoundOut ro{};
@@ -1227,10 +1239,14 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
             }
         }
     }
-    if (!h->r_ready) finalize_sorted(h);
+    if (!h->r_ready) {
+        h->ev_end_valid = false;
+        finalize_sorted(h);
+    }
     if (h->trace) std::fprintf(stderr, "[rb trace] host: solve total %.1f us\n", (now_s() - t_start) * 1e6);
     trace_report(h, (int)h->stats.size());
-    ck(cudaEventRecord(h->ev[6], h->st), "ev end");
+    if (!h->ev_end_valid) ck(cudaEventRecord(h->ev[6], h->st), "ev end");
+    h->ev_end_valid = false;
     ck(cudaEventSynchronize(h->ev[6]), "ev sync");
     float dev_ms = 0.f;
     cudaEventElapsedTime(&dev_ms, h->ev[5], h->ev[6]);
@@ -1968,6 +1984,10 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     }
     if (k == "tail_blocks_x4") {  // round-tail grid = SMs * value / 4 blocks
         h->tail_blocks_per_sm = std::max<int64_t>(1, value) / 4.0;
+        return RB_OK;
+    }
+    if (k == "graph_prologue") {  // ping-pong round graph: the first U rounds before the WHILE node
+        h->graph_prologue = value != 0;
         return RB_OK;
     }
     if (k == "pingpong") {  // round graph: ping-pong frontiers, round end in the HS kernel

@@ -152,10 +152,12 @@ struct rb_handle {
     bool graph_fused_only = true;  // round graph: k_hs_fused for every count (no eval/lin/sweep nodes)
     bool graph_cf = true;        // round graph: k_classify_filter instead of k_classify + k_filter
     bool pingpong = true;        // round graph: ping-pong frontiers, round end in k_hs_fused
+    bool graph_prologue = true;  // ping-pong round graph: the first U rounds outside the WHILE node
     unsigned long long* d_etable = nullptr;  // epoch dedup table (ping-pong round graph)
     size_t cap_etable = 0;
     unsigned epoch_next = 1;
     int graph_rounds_per_iter = 1;
+    bool ev_end_valid = false;   // ev[6] already marks the end of this solve's device work
     double tail_blocks_per_sm = 2.0;  // k_round_tail grid
     // system-specialised filter kernels (codegen.cpp); the table kernels when unavailable
     rbg::SystemTerms terms;
