@@ -1975,7 +1975,7 @@ __device__ void hs_round_end(const HsParams& prm, Counters* ctr, const Front& ou
 }
 
 #ifndef RB_FUSED_G32
-#define RB_FUSED_G32 0
+#define RB_FUSED_G32 1  // one warp per box in k_hs_fused for n >= 3
 #endif
 template <int N>
 struct FusedLayout {
