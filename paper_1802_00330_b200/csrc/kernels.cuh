@@ -376,6 +376,23 @@ __device__ __forceinline__ unsigned cas_acq_rel(unsigned* p, unsigned cmp, unsig
     return old;
 }
 
+// Which rows can be duplicates.  Frontier rows descend from bisection cells with
+// disjoint interiors (children [lo, m], [m, hi]); HS outputs are subsets of their
+// input (intersections with it), kept / skipped rows are their input, carried rows
+// are unchanged.  The only overlap between lineages comes from an HS fork, whose two
+// pieces in the split component are [cur.lo, RU(x + a)] and [RD(x + b), cur.hi] with
+// a < b: they can share at most ~2 ulps.  So two equal rows from different entries
+// lie in a set with empty interior or a few ulps thick in some component, and a row
+// none of whose components is that thin has no duplicate.  Such rows skip the table
+// (dead = 0); `kThinUlps` leaves a wide margin over the 2-ulp bound.
+constexpr long long kThinUlps = 64;
+
+__device__ __forceinline__ long long ordkey(double x) {  // monotone in x, +0 == -0
+    const long long b = __double_as_longlong(x);
+    return b >= 0 ? b : (long long)0x8000000000000000ull - b;
+}
+__device__ __forceinline__ bool thin_comp(double lo, double hi) { return ordkey(hi) - ordkey(lo) <= kThinUlps; }
+
 // row `i` of f holds (lo[j], hi[j]) and the flags, already stored by this thread or
 // its lane group and fenced; one thread inserts it.
 __device__ __forceinline__ unsigned long long cas_acq_rel64(unsigned long long* p, unsigned long long cmp,
@@ -394,6 +411,14 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
 template <int N>
 __device__ __forceinline__ void dedup_insert_regs(const Front& f, int64_t i, const double* lo, const double* hi,
                                                   uint8_t cert, uint8_t uns, const DedupCtx& d, Counters* ctr) {
+    bool thin = false;
+#pragma unroll
+    for (int j = 0; j < N; j++) thin |= thin_comp(lo[j], hi[j]);
+    if (!thin) {  // cannot have a duplicate (see kThinUlps)
+        d.dead[i] = 0;
+        d.slot_of[i] = 0xffffffffu;
+        return;
+    }
     unsigned long long h = 0x9e3779b97f4a7c15ull;  // = row_hash over the stored (canonical) values
 #pragma unroll
     for (int j = 0; j < N; j++) {
@@ -2254,7 +2279,13 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                 out.unsplit[slot] = 0;
                 if (tags) tags[slot] = 2 * b + q;
             }
-            if (prm.dd.table || prm.dd.etable) {  // group-uniform: gather the row into lane 0 and insert it
+            const bool any_thin = __any_sync(gmask, l < N && thin_comp(w_lo, w_hi));
+            if ((prm.dd.table || prm.dd.etable) && !any_thin) {  // no duplicate possible (kThinUlps)
+                if (l == 0 && slot < (unsigned long long)out.cap) {
+                    prm.dd.dead[slot] = 0;
+                    prm.dd.slot_of[slot] = 0xffffffffu;
+                }
+            } else if (prm.dd.table || prm.dd.etable) {  // group-uniform: gather the row into lane 0, insert it
                 double rlo[N], rhi[N];
                 const double mlo = canon0(w_lo), mhi = canon0(w_hi);
 #pragma unroll
