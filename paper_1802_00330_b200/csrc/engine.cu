@@ -551,10 +551,10 @@ static void trace_report(rb_handle* h, int rounds) {
             for (int q : {(int)ids.size() / 2, (int)(ids.size() * 9 / 10), (int)ids.size() - 1}) {
                 const unsigned long long* x = &br[8 * ids[q]];
                 std::fprintf(stderr, "[rb trace]   box %d (end rank %d): start %.2f eval %.2f lin %.2f sweep %.2f out %.2f "
-                                     "end %.2f us, rows %llu kind %llu sm %llu\n",
+                                     "(to loop end %.2f) end %.2f us, rows %llu kind %llu sm %llu\n",
                              ids[q], q, (x[0] - t0) * 1e-3, (x[1] - x[0]) * 1e-3, (x[2] - x[1]) * 1e-3,
-                             (x[3] - x[2]) * 1e-3, (x[4] - x[3]) * 1e-3, (x[4] - t0) * 1e-3, x[5] & 0xff,
-                             (x[5] >> 8) & 0xff, x[5] >> 16);
+                             (x[3] - x[2]) * 1e-3, (x[4] - x[3]) * 1e-3, x[7] ? (x[7] - x[3]) * 1e-3 : 0.0,
+                             (x[4] - t0) * 1e-3, x[5] & 0xff, (x[5] >> 8) & 0xff, x[5] >> 16 & 0xffff);
             }
         }
     }
@@ -1436,7 +1436,7 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
             size_t off = 0;
             auto take = [&](size_t bytes) {
                 const size_t o = off;
-                off = (off + bytes + 63) & ~size_t(63);
+                off = (off + bytes + 127) & ~size_t(127);  // Counters is 128-byte aligned
                 return o;
             };
             const size_t o_ctr = take(sizeof(Counters)), o_state = take(sizeof(DevState)), o_hx = take(sizeof(HostX));

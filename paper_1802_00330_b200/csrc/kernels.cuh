@@ -264,13 +264,17 @@ struct Front {
     int64_t cap;
 };
 
+// The counters every block of a round updates.  The latency-critical ones (the slot
+// reservations of the appenders, the block-done counter of the round end) sit on
+// their own 128-byte lines, so their atomics do not queue behind each other at L2.
 struct Counters {
-    unsigned long long n_next;       // rows appended to the next frontier
-    unsigned long long n_carried;    // of which carried (done / degenerate)
-    unsigned long long n_par;        // active parents
-    unsigned long long n_surv;       // filter survivors (may exceed S capacity)
-    unsigned long long child_wmax;   // bits of max child width over survivors
-    unsigned long long wmax;         // bits of max width over the next frontier
+    alignas(128) unsigned long long n_next;  // rows appended to the next frontier
+    alignas(128) unsigned long long n_surv;  // filter survivors (may exceed S capacity)
+    alignas(128) unsigned long long tail_done;  // blocks finished (the last one runs the round end)
+    alignas(128) unsigned long long wmax;    // bits of max width over the next frontier
+    unsigned long long child_wmax;           // bits of max child width over survivors
+    alignas(128) unsigned long long n_carried;  // of n_next, carried (done / degenerate)
+    unsigned long long n_par;                // active parents
     unsigned long long filter_ops;
     unsigned long long hs_ops;
     unsigned long long hs_calls;
@@ -278,12 +282,10 @@ struct Counters {
     unsigned long long dups;
     unsigned long long hs_on;
     unsigned long long n_compact;
-    unsigned long long tail_done;    // k_round_tail: blocks finished (last one runs the round end)
-    unsigned long long pad[2];
     // per-equation filter statistics (evaluations, rejections): the next round
     // evaluates the equations in descending rejections-per-op order.  Any order
     // gives the same survivor set -- a child is kept iff every equation encloses 0.
-    unsigned long long f_eval[16];
+    alignas(128) unsigned long long f_eval[16];
     unsigned long long f_rej[16];
 };
 
@@ -1981,13 +1983,20 @@ static __device__ __noinline__ bool round_end_warp(DevState* st, Counters* ctr, 
 
 // End of a round inside the HS kernel (ping-pong round graph): the last block to
 // finish removes duplicate rows and runs the round end (bnb.py:322-352).
+// Only the blocks that can have written rows take part: `rows_per_block` rows (or
+// boxes) per block in a grid-stride loop over `n` -- the others return at once, so the
+// block-done counter sees a few atomics instead of one per block of the grid.
 template <int N>
-__device__ void hs_round_end(const HsParams& prm, Counters* ctr, const Front& out, const TabMeta& meta) {
+__device__ void hs_round_end(const HsParams& prm, Counters* ctr, const Front& out, const TabMeta& meta,
+                             int64_t n, int rows_per_block) {
     __shared__ int s_last;
+    const int64_t need = (n + rows_per_block - 1) / rows_per_block;
+    const unsigned parts = (unsigned)(need < 1 ? 1 : (need > (int64_t)gridDim.x ? (int64_t)gridDim.x : need));
+    if (blockIdx.x >= parts) return;  // block-uniform
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        s_last = atomicAdd(&ctr->tail_done, 1ull) == (unsigned long long)(gridDim.x - 1);
+        s_last = atomicAdd(&ctr->tail_done, 1ull) == (unsigned long long)(parts - 1);
     }
     __syncthreads();
     if (!s_last) return;
@@ -2047,7 +2056,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
     if (!hs_on) {
         hs_passthrough<N>(S, n_in, out, ctr, tags, prm.dd);
-        if (prm.round_end) hs_round_end<N>(prm, ctr, out, meta);
+        if (prm.round_end) hs_round_end<N>(prm, ctr, out, meta, n_in, (int)blockDim.x);
         return;
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -2298,6 +2307,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                     dedup_insert_regs<N>(out, (int64_t)slot, rlo, rhi, cert ? 1 : 0, 0, prm.dd, ctr);
             }
         }
+        if (prm.prof && valid && l == 0 && b < kTraceBoxes) prm.prof[kTraceBoxOff + 8 * b + 7] = gtimer();
         unsigned long long wbits = (unsigned long long)__double_as_longlong(wmax);
         wbits = warp_max(wbits);
         if (lane == 0 && wbits) atomicMax(&ctr->wmax, wbits);
@@ -2319,7 +2329,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
         btr[1] = gtimer();
         btr[2] = smid();
     }
-    if (prm.round_end) hs_round_end<N>(prm, ctr, out, meta);
+    if (prm.round_end) hs_round_end<N>(prm, ctr, out, meta, n_in, (int)(blockDim.x >> 5) * L::BPW);
 }
 
 template <int N, class EV = TabEval>
@@ -2522,7 +2532,7 @@ static __device__ __noinline__ bool round_end_warp(DevState* st, Counters* ctr, 
                                             int64_t s_cap, int* eq_order, const TabMeta& meta,
                                             bool pingpong) {
     constexpr int W = (int)(sizeof(Counters) / 8);
-    __shared__ unsigned long long sc[W];
+    __shared__ __align__(128) unsigned long long sc[W];
     const int lane = threadIdx.x & 31;
     unsigned long long* w = reinterpret_cast<unsigned long long*>(ctr);
     for (int i = lane; i < W; i += 32) sc[i] = w[i];
