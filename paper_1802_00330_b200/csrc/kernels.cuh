@@ -2043,6 +2043,15 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
     STab tab{};
     if constexpr (EV::tables) tab = issue_stab(meta, gtab, smem, false);
     pdl_wait();
+    // this group's first box, loaded speculatively (any row below S.cap is addressable)
+    // so its latency overlaps the survivor-count read; used only if the box exists
+    const int lane0 = threadIdx.x & 31, warp0 = threadIdx.x >> 5;
+    const int64_t b_first = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp0) * L::BPW + lane0 / G;
+    double pre_lo = 0.0, pre_hi = 0.0;
+    if (lane0 % G < N && b_first < S.cap) {
+        pre_lo = S.lo[(lane0 % G) * S.cap + b_first];
+        pre_hi = S.hi[(lane0 % G) * S.cap + b_first];
+    }
     if (prm.round_end && (prm.st->done || prm.st->bail)) {  // unrolled round after the end of the loop
         cp_async_wait();
         return;
@@ -2081,7 +2090,8 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
         int rows = 0;
         if (valid) {
             if (l < N) {
-                const double lo = S.lo[l * S.cap + b], hi = S.hi[l * S.cap + b];
+                const bool first = b == b_first;
+                const double lo = first ? pre_lo : S.lo[l * S.cap + b], hi = first ? pre_hi : S.hi[l * S.cap + b];
                 s[L::oXl + l] = lo;
                 s[L::oXh + l] = hi;
                 s[L::oXm + l] = mid_of(lo, hi);  // Box.midpoint, poly.py:114-115
