@@ -526,9 +526,13 @@ static void trace_report(rb_handle* h, int rounds) {
     }
     {  // per-box k_hs_fused records of the last round that ran HS
         const unsigned long long* br = &t[kTraceBoxAbs];
-        unsigned long long rmax = 0;
+        std::vector<unsigned long long> rounds_seen;  // a later round overwrites the first records
         for (int b = 0; b < kTraceBoxes; b++)
-            if (br[8 * b + 4]) rmax = std::max(rmax, br[8 * b + 6]);
+            if (br[8 * b + 4] &&
+                std::find(rounds_seen.begin(), rounds_seen.end(), br[8 * b + 6]) == rounds_seen.end())
+                rounds_seen.push_back(br[8 * b + 6]);
+        std::sort(rounds_seen.begin(), rounds_seen.end());
+        for (unsigned long long rmax : rounds_seen) {
         std::vector<int> ids;
         for (int b = 0; b < kTraceBoxes; b++)
             if (br[8 * b + 4] && br[8 * b + 6] == rmax) ids.push_back(b);
@@ -556,6 +560,7 @@ static void trace_report(rb_handle* h, int rounds) {
                              (x[3] - x[2]) * 1e-3, (x[4] - x[3]) * 1e-3, x[7] ? (x[7] - x[3]) * 1e-3 : 0.0,
                              (x[4] - t0) * 1e-3, x[5] & 0xff, (x[5] >> 8) & 0xff, x[5] >> 16 & 0xffff);
             }
+        }
         }
     }
     ck(cudaMemset(h->d_trace, 0, t.size() * 8), "trace clear");
