@@ -1428,9 +1428,20 @@ struct LinLayout {
 __device__ __forceinline__ ival pmul_minmax(double a, ival y) {
     return mk(py_min(__dmul_rd(a, y.lo), __dmul_rd(a, y.hi)), py_max(__dmul_ru(a, y.lo), __dmul_ru(a, y.hi)));
 }
-template <class A>
+// The same two products chosen by a's sign bit (integer pipe: no FP64 compare, half
+// the DMULs of pmul_minmax).  a = -0.0 takes the a < 0 operands: both products are
+// then zeros, equal in value to pmul_minmax's (zero signs are canonicalised on output).
+__device__ __forceinline__ ival pmul_sign(double a, ival y) {
+    const bool neg = __double_as_longlong(a) < 0;
+    const double p = neg ? y.hi : y.lo, q = neg ? y.lo : y.hi;
+    return mk(__dmul_rd(a, p), __dmul_ru(a, q));
+}
+// Measured (bench other_configs, full solves): sign-bit products cut banded12's HS time
+// 6.29 -> 5.84 ms (N = 12, 32 lanes per box) but cost katsura6 (N = 7) 3%.
+template <class A, int N>
 __device__ __forceinline__ ival pmul(double a, ival y) {
     if constexpr (A::exact) return A::mul_point(a, y);
+    else if constexpr (N > 8) return pmul_sign(a, y);
     else return pmul_minmax(a, y);
 }
 
@@ -1458,7 +1469,7 @@ __device__ __forceinline__ void lin_products(const double* Am, const ival* jcol,
             if (i < N) {
                 ival acc = mk(0.0, 0.0);
 #pragma unroll
-                for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A>(Am[i * N + u], jcol[u]));
+                for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A, N>(Am[i * N + u], jcol[u]));
                 K.jl[(i * N + col) * K.ws] = acc.lo;
                 K.jh[(i * N + col) * K.ws] = acc.hi;
             }
@@ -1467,7 +1478,7 @@ __device__ __forceinline__ void lin_products(const double* Am, const ival* jcol,
     ival acc = mk(0.0, 0.0);
     if (l < N) {
 #pragma unroll
-        for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A>(Am[l * N + u], mk(K.fl[u * K.ws], K.fh[u * K.ws])));
+        for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A, N>(Am[l * N + u], mk(K.fl[u * K.ws], K.fh[u * K.ws])));
     }
     __syncwarp(gmask);  // every lane has read F(x) before g overwrites it
     if (l < N) {
