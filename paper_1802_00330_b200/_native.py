@@ -208,7 +208,10 @@ class Engine:
         except Exception:
             pass
 
-    def solve(self, cfg: RbConfig):
+    def solve(self, cfg: RbConfig, stats_rows: bool = False):
+        """One rb_solve + rb_fetch.  stats_rows: per-round statistics as raw tuples in
+        STATS_FIELDS order under "stats_rows" (the public solve() path) instead of
+        dicts under "stats"."""
         L = lib()
         info = RbResultInfo()
         _check(L.rb_solve(self.h, C.byref(cfg), C.byref(info)), self.h, "rb_solve")
@@ -218,10 +221,11 @@ class Engine:
         stats = np.empty(max(1, nr), _STATS_DTYPE)
         _check(L.rb_fetch(self.h, lo.ctypes.data, hi.ctypes.data, flags.ctypes.data, flags[1].ctypes.data,
                           stats.ctypes.data), self.h, "rb_fetch")
-        st = [dict(zip(STATS_FIELDS, row)) for row in stats[:nr].tolist()]
+        rows = stats[:nr].tolist()
         fb = flags.view(np.bool_)
         return {"status": STATUS_NAMES[info.status], "lo": lo, "hi": hi, "cert": fb[0], "unsplit": fb[1],
-                "stats": st, "solve_seconds": info.solve_seconds,
+                **({"stats_rows": rows} if stats_rows else {"stats": [dict(zip(STATS_FIELDS, r)) for r in rows]}),
+                "solve_seconds": info.solve_seconds,
                 "device_ms": info.device_ms, "kernel_launches": int(info.kernel_launches)}
 
     def filter(self, plo, phi):

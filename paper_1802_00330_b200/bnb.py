@@ -168,7 +168,19 @@ _LOCK = threading.Lock()
 _MAX_ENGINES = 8
 
 
+_DEFAULT_DEVICE = None
+
+
 def default_device() -> int:
+    """RB_DEVICE, else LOCAL_RANK, else 0 -- read once per process (os.environ
+    lookups cost microseconds on the per-solve path)."""
+    global _DEFAULT_DEVICE
+    if _DEFAULT_DEVICE is None:
+        _DEFAULT_DEVICE = _env_device()
+    return _DEFAULT_DEVICE
+
+
+def _env_device() -> int:
     for k in ("RB_DEVICE", "LOCAL_RANK"):
         v = os.environ.get(k)
         if v is not None and v.strip().isdigit():
@@ -304,6 +316,21 @@ def _iv(lo, hi):
     return iv
 
 
+# RoundStats fields in an rb_round_stats row (_native.STATS_FIELDS order)
+_RS_IDX = tuple(_native.STATS_FIELDS.index(f) for f in
+                ("round", "boxes_in", "boxes_after_filter", "boxes_after_hs", "width", "elapsed_seconds"))
+
+
+def _stats_tuples(out):
+    """(round, boxes_in, after_filter, after_hs, width, elapsed) per round, from the
+    raw rows of Engine.solve(stats_rows=True) or from the dicts of solve_arrays."""
+    if "stats_rows" in out:
+        a, b, c, d, e, f = _RS_IDX
+        return [(r[a], r[b], r[c], r[d], r[e], r[f]) for r in out["stats_rows"]]
+    return [(int(st["round"]), int(st["boxes_in"]), int(st["boxes_after_filter"]), int(st["boxes_after_hs"]),
+             float(st["width"]), float(st["elapsed_seconds"])) for st in out["stats"]]
+
+
 def _own_result(out):
     lo, hi, cert, uns = out["lo"], out["hi"], out["cert"], out["unsplit"]
     if lo.shape[0] > LAZY_THRESHOLD:
@@ -313,17 +340,17 @@ def _own_result(out):
         boxes = tuple(
             _made(RootBox, box=_made(Box, intervals=tuple(map(_iv, a, b))), certified=c, unsplittable=u)
             for a, b, c, u in zip(lo.tolist(), hi.tolist(), cl, ul))
-    stats = tuple(_made(RoundStats, round=int(st["round"]), boxes_in=int(st["boxes_in"]),
-                        boxes_after_filter=int(st["boxes_after_filter"]),
-                        boxes_after_hs=int(st["boxes_after_hs"]), width=float(st["width"]),
-                        elapsed_seconds=float(st["elapsed_seconds"]))
-                  for st in out["stats"])
+    stats = tuple(_made(RoundStats, round=r, boxes_in=bi, boxes_after_filter=af, boxes_after_hs=ah, width=w,
+                        elapsed_seconds=el) for r, bi, af, ah, w, el in _stats_tuples(out))
     return _made(SolveResult, status=out["status"], boxes=boxes, stats=stats)
 
 
 def solve(s, cfg=None) -> SolveResult:
     """Isolate all real roots of the system inside its initial box (bnb.py:224)."""
-    out = solve_arrays(s, cfg)
+    cfg = cfg or SolverConfig()
+    validate_config(cfg)
+    spec = as_spec(s)
+    out = engine_for(spec).solve(native_config(cfg), stats_rows=True)
     types = _reference_types(s)
     if types is None:
         return _own_result(out)
@@ -335,8 +362,6 @@ def solve(s, cfg=None) -> SolveResult:
         boxes = tuple(
             RB(BX(tuple(IV(a, b) for a, b in zip(lo[r].tolist(), hi[r].tolist()))), bool(cert[r]), bool(uns[r]))
             for r in range(lo.shape[0]))
-    stats = tuple(RS(round=int(st["round"]), boxes_in=int(st["boxes_in"]),
-                     boxes_after_filter=int(st["boxes_after_filter"]), boxes_after_hs=int(st["boxes_after_hs"]),
-                     width=float(st["width"]), elapsed_seconds=float(st["elapsed_seconds"]))
-                  for st in out["stats"])
+    stats = tuple(RS(round=r, boxes_in=bi, boxes_after_filter=af, boxes_after_hs=ah, width=w, elapsed_seconds=el)
+                  for r, bi, af, ah, w, el in _stats_tuples(out))
     return SR(out["status"], boxes, stats)

@@ -482,6 +482,7 @@ struct DevState {
     unsigned long long t_round_ns;
     int cur;                    // frontier in F[cur] (ping-pong round graph; k_small_rounds)
     unsigned epoch;             // dedup table epoch of the round (ping-pong round graph)
+    int round0;                 // round the graph launch started from (k_solve_start)
 };
 
 __device__ __forceinline__ unsigned state_epoch(const DevState* st) { return *(volatile const unsigned*)&st->epoch; }
@@ -2899,6 +2900,7 @@ __global__ void k_solve_start(DevState* st, const HostX* hx, Front f0, Counters*
     if (t == 0) {
         DevState s = hx->start;
         s.t_round_ns = gtimer();
+        s.round0 = s.round_no;
         *st = s;
     }
     if (t < n) {
@@ -2935,7 +2937,7 @@ __global__ void k_solve_finish(const DevState* st, const DevRoundStats* rs, cons
     const long long N = (long long)s.n_cur;
     const bool gather = s.done && N <= max_rows;
     if (blockIdx.x == 0) {
-        const int first = hx->start.round_no - 1;
+        const int first = s.round0 - 1;  // device copy: no PCIe read of hx->start
         for (int r = first + (int)threadIdx.x; r < s.nrounds; r += blockDim.x) hstats[r] = rs[r];
         if (threadIdx.x < 16) hx->order[threadIdx.x] = order[threadIdx.x];
         if (threadIdx.x == 0) {
