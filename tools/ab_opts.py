@@ -1,6 +1,6 @@
 """A/B device time of engine options on one config (dev tool):
 python tools/ab_opts.py CONFIG 'opt=v,opt=v' 'opt=v' ..."""
-import os, sys
+import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from bench import CONFIGS, load_spec
 from paper_1802_00330_b200 import SolverConfig, bnb
@@ -14,5 +14,11 @@ for variant in sys.argv[2:]:
     for k, v in opts:
         eng.set_option(k, int(v))
     eng.solve(cfg)
-    ts = sorted(eng.solve(cfg)["device_ms"] for _ in range(reps))
-    print(f"{name:16s} {variant:28s} median {ts[len(ts)//2]:8.3f} min {ts[0]:8.3f} ms", flush=True)
+    ts, ws = [], []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        ts.append(eng.solve(cfg)["device_ms"])
+        ws.append(1e3 * (time.perf_counter() - t0))
+    ts.sort(); ws.sort()
+    print(f"{name:16s} {variant:28s} device median {ts[len(ts)//2]:8.3f} min {ts[0]:8.3f} ms, "
+          f"host wall median {ws[len(ws)//2]:8.3f} min {ws[0]:8.3f} ms", flush=True)
