@@ -379,12 +379,54 @@ def run_ours(args, world, rank, local):
         "roofline": roofline,
         "clocks": clocks,
     }
+    if args.sharded:
+        line["sharded"] = sharded_solve(args, world, rank, local)
     if rank == 0 and world == 1 and not args.no_other_configs:
         line["other_configs"] = other_configs(args, local, peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(spec, kw, budget_s=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def sharded_solve(args, world, rank, local):
+    """--sharded CONFIG: one large BASELINE config solved with its frontier sharded
+    across the ranks (dist.solve_sharded: all-reduce of the HS trigger and round
+    statistics, all_to_all of every row to its hash owner each round).  Time per
+    solve = host wall clock around barrier + synchronize on every rank, max over
+    ranks: the protocol synchronises with the host every round, so the wall clock is
+    the solve's own time.  Opt-in (not part of the default line)."""
+    import torch
+    from paper_1802_00330_b200 import SolverConfig, bnb
+    from paper_1802_00330_b200.dist import CudaShardBackend, solve_sharded
+    sysname, kw, desc = CONFIGS[args.sharded]
+    spec = load_spec(sysname)
+    cfg = SolverConfig(**kw)
+    backend = CudaShardBackend(spec, local, device_exchange=True)
+    res = solve_sharded(spec, cfg, backend=backend)  # warm-up: buffers, specialised kernels
+    ts = []
+    for _ in range(args.sharded_steps):
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = solve_sharded(spec, cfg, backend=backend)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+        barrier(world)
+    t = allreduce_max(world, statistics.median(ts), local)
+    if rank != 0:
+        return None
+    boxes = sum(st.boxes_after_filter for st in res.stats)
+    out = {"workload": desc, "n_gpus": world, "steps": args.sharded_steps, "status": res.status,
+           "rounds": len(res.stats), "final_boxes": len(res.boxes),
+           "time_to_solution_ms": 1e3 * t, "timing": "host wall, median over steps, max over ranks",
+           "boxes_after_filter_per_s": boxes / t,
+           "path": "dist.solve_sharded (rb_round_* protocol, NCCL all_reduce / all_to_all of rows; none at world 1)"}
+    if world == 1:  # the same solve through rb_solve (device-resident rounds) for comparison
+        ref = bnb.solve_arrays(spec, cfg)
+        out["single_engine_final_boxes"] = int(ref["lo"].shape[0])
+        out["matches_single_engine"] = bool(ref["lo"].shape[0] == len(res.boxes) and ref["status"] == res.status)
+    return out
 
 
 def main():
@@ -397,6 +439,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--sharded", choices=sorted(CONFIGS), default=None,
+                    help="also solve this config with the frontier sharded across the ranks")
+    ap.add_argument("--sharded-steps", type=int, default=5)
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     try:
