@@ -187,6 +187,7 @@ class Engine:
         rc = L.rb_create(C.byref(sysd), int(device), C.byref(h))
         _check(rc, None, "rb_create")
         self.h = h
+        self._device_timing = True
 
     def codegen_active(self):
         """(True, '') when the system-specialised kernels run, else (False, reason)."""
@@ -196,6 +197,8 @@ class Engine:
 
     def set_option(self, key: str, value: int):
         _check(lib().rb_set_option(self.h, key.encode(), int(value)), self.h, "rb_set_option")
+        if key == "device_timing":
+            self._device_timing = bool(value)
 
     def close(self):
         if getattr(self, "h", None):
@@ -208,11 +211,16 @@ class Engine:
         except Exception:
             pass
 
-    def solve(self, cfg: RbConfig, stats_rows: bool = False):
+    def solve(self, cfg: RbConfig, stats_rows: bool = False, device_timing: bool = True):
         """One rb_solve + rb_fetch.  stats_rows: per-round statistics as raw tuples in
         STATS_FIELDS order under "stats_rows" (the public solve() path) instead of
-        dicts under "stats"."""
+        dicts under "stats".  device_timing=False: a solve the round graph finishes
+        returns as soon as its results are visible in mapped host memory, without
+        waiting for the stream (device_ms is then -1)."""
         L = lib()
+        if device_timing != self._device_timing:
+            self.set_option("device_timing", 1 if device_timing else 0)
+            self._device_timing = device_timing
         info = RbResultInfo()
         _check(L.rb_solve(self.h, C.byref(cfg), C.byref(info)), self.h, "rb_solve")
         N, n, nr = int(info.nboxes), self.n, int(info.nrounds)

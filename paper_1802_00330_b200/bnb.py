@@ -350,7 +350,7 @@ def solve(s, cfg=None) -> SolveResult:
     cfg = cfg or SolverConfig()
     validate_config(cfg)
     spec = as_spec(s)
-    out = engine_for(spec).solve(native_config(cfg), stats_rows=True)
+    out = engine_for(spec).solve(native_config(cfg), stats_rows=True, device_timing=False)
     types = _reference_types(s)
     if types is None:
         return _own_result(out)

@@ -1091,8 +1091,16 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     st.cur = 0;
     st.epoch = h->epoch_next;
     HostX& X = *h->hx;
+    st.finish_blocks = 0;
+    // process-wide sequence: the pinned block of a destroyed handle is reused by the next
+    // one, whose HostX may still hold an old done_seq
+    static std::atomic<unsigned long long> g_solve_seq{0};
+    st.seq = ++g_solve_seq;
+    h->solve_seq = st.seq;
+    X.done_seq = 0;
     X.start = st;
     X.rows = -1;
+    if (h->trace) X.state.nrounds = -7;  // sentinel for the visibility measurement below
     std::atomic_thread_fence(std::memory_order_seq_cst);
     const double tg0 = now_s();
     ck(cudaGraphLaunch(h->graph_exec, h->st), "graph launch");
@@ -1101,11 +1109,37 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     ck(cudaEventRecord(h->ev[6], h->st), "ev end");
     h->ev_end_valid = true;
     const double tg1 = now_s();
-    ck(cudaStreamSynchronize(h->st), "graph sync");
+    double tflag = 0.0;
+    if (h->trace) {  // when the finish kernel's state write becomes visible to the host (measurement only)
+        const volatile int* nr = &X.state.nrounds;
+        while (*nr == -7 && now_s() - tg1 < 0.1) {
+        }
+        tflag = now_s();
+    }
+    h->graph_fast_return = false;
+    if (!h->device_timing) {
+        // spin on the completion flag the finish kernel publishes after its mapped writes;
+        // the stream is polled now and then so a fault or an early end is still seen
+        const volatile unsigned long long* ds = &X.done_seq;
+        for (unsigned it = 1;; it++) {
+            if (*ds == st.seq) {
+                h->graph_fast_return = true;
+                break;
+            }
+            if ((it & 1023u) == 0) {
+                const cudaError_t e = cudaStreamQuery(h->st);
+                if (e == cudaSuccess) break;
+                if (e != cudaErrorNotReady) ck(e, "graph");
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+    }
+    if (!h->graph_fast_return) ck(cudaStreamSynchronize(h->st), "graph sync");
     const double tg2 = now_s();
     if (h->trace)
-        std::fprintf(stderr, "[rb trace] host: solve start -> graph launch %.1f us, launch call %.1f us, sync %.1f us\n",
-                     (tg0 - h->t_solve0) * 1e6, (tg1 - tg0) * 1e6, (tg2 - tg1) * 1e6);
+        std::fprintf(stderr, "[rb trace] host: solve start -> graph launch %.1f us, launch call %.1f us, sync %.1f us "
+                             "(state visible after %.1f us)\n",
+                     (tg0 - h->t_solve0) * 1e6, (tg1 - tg0) * 1e6, (tg2 - tg1) * 1e6, (tflag - tg1) * 1e6);
     const DevState r = X.state;
     const int first = (int)h->stats.size();
     const int nr = r.nrounds - first;
@@ -1250,11 +1284,17 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
     }
     if (h->trace) std::fprintf(stderr, "[rb trace] host: solve total %.1f us\n", (now_s() - t_start) * 1e6);
     trace_report(h, (int)h->stats.size());
-    if (!h->ev_end_valid) ck(cudaEventRecord(h->ev[6], h->st), "ev end");
+    float dev_ms = -1.f;
+    if (h->graph_fast_return && h->ev_end_valid && h->r_ready && h->r_on_host) {
+        // the graph finished the solve and its results are on the host: no stream wait
+        // (the events complete on their own; device time is not measured in this mode)
+    } else {
+        if (!h->ev_end_valid) ck(cudaEventRecord(h->ev[6], h->st), "ev end");
+        ck(cudaEventSynchronize(h->ev[6]), "ev sync");
+        cudaEventElapsedTime(&dev_ms, h->ev[5], h->ev[6]);
+    }
     h->ev_end_valid = false;
-    ck(cudaEventSynchronize(h->ev[6]), "ev sync");
-    float dev_ms = 0.f;
-    cudaEventElapsedTime(&dev_ms, h->ev[5], h->ev[6]);
+    h->graph_fast_return = false;
     h->have_result = true;
     if (info) {
         info->device_ms = dev_ms;
@@ -1955,6 +1995,10 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     if (k == "hs_fused") {  // 0: eval/lin/sweep only, 1: by batch size, 2: fused only
         h->hs_fused = value != 0 && h->fused_smem <= (size_t)h->smem_optin;
         h->fused_rows = value == 2 ? INT64_MAX : (int64_t)h->sms * 80;
+        return RB_OK;
+    }
+    if (k == "device_timing") {  // 0: return on the graph's completion flag, device_ms = -1
+        h->device_timing = value != 0;
         return RB_OK;
     }
     if (k == "pdl") {

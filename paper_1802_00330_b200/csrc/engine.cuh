@@ -196,6 +196,9 @@ struct rb_handle {
     // RB_TRACE=1: device timestamps (%globaltimer) at the phase boundaries of every
     // round, printed to stderr after each solve (a profiling aid; adds one tiny launch per phase)
     bool trace = false;
+    bool device_timing = true;   // false: a graph-finished solve returns on HostX::done_seq, device_ms = -1
+    unsigned long long solve_seq = 0;
+    bool graph_fast_return = false;  // this solve's graph ended on done_seq (no stream sync yet)
     double t_solve0 = 0.0;
     unsigned long long* d_trace = nullptr;
     size_t fused_smem = 0;

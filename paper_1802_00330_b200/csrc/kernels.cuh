@@ -483,6 +483,8 @@ struct DevState {
     int cur;                    // frontier in F[cur] (ping-pong round graph; k_small_rounds)
     unsigned epoch;             // dedup table epoch of the round (ping-pong round graph)
     int round0;                 // round the graph launch started from (k_solve_start)
+    unsigned finish_blocks;     // k_solve_finish blocks done (host sets 0 in the start state)
+    unsigned long long seq;     // solve sequence number, echoed to HostX::done_seq at the end
 };
 
 __device__ __forceinline__ unsigned state_epoch(const DevState* st) { return *(volatile const unsigned*)&st->epoch; }
@@ -2889,6 +2891,7 @@ struct HostX {                  // pinned, mapped host memory shared with the gr
     DevState state;             // device -> host: state after the device rounds
     int order[16];              // device -> host: filter equation order
     long long rows;             // device -> host: rows gathered (-1: none)
+    unsigned long long done_seq;// device -> host: start.seq once everything above is visible
 };
 
 // initial frontier = the initial box (bnb.py:229-232), device state, counters, filter order
@@ -2945,14 +2948,28 @@ __global__ void k_solve_finish(const DevState* st, const DevRoundStats* rs, cons
             hx->rows = gather ? N : -1;
         }
     }
-    if (!gather) return;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
-        for (int j = 0; j < n; j++) {
-            hlo[i * n + j] = canon0(f0.lo[j * f0.cap + i]);
-            hhi[i * n + j] = canon0(f0.hi[j * f0.cap + i]);
+    if (gather) {
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+             i += (long long)gridDim.x * blockDim.x) {
+            for (int j = 0; j < n; j++) {
+                hlo[i * n + j] = canon0(f0.lo[j * f0.cap + i]);
+                hhi[i * n + j] = canon0(f0.hi[j * f0.cap + i]);
+            }
+            hc[i] = f0.cert[i];
+            hu[i] = f0.unsplit[i];
         }
-        hc[i] = f0.cert[i];
-        hu[i] = f0.unsplit[i];
+    }
+    // completion flag in mapped memory: every block's host writes are fenced before it
+    // counts itself; the last block publishes the sequence number, so a host spinning on
+    // done_seq may read the results without waiting for the stream (rb_solve fast return)
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&const_cast<DevState*>(st)->finish_blocks, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            *reinterpret_cast<volatile unsigned long long*>(&hx->done_seq) = s.seq;
+        }
     }
 }
 #endif
