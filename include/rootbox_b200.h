@@ -211,7 +211,11 @@ int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const 
  *                 0: direct per-child evaluation (k_filter).
  *   "graph"       1 (default): rounds whose worst case fits the survivor buffer run
  *                 in one CUDA graph (device-side WHILE loop, no host round trip);
- *                 0: host-driven rounds (per-kernel CUDA-event timings in the stats). */
+ *                 0: host-driven rounds (per-kernel CUDA-event timings in the stats).
+ *   "device_timing" 1 (default): rb_solve waits for the stream and reports CUDA-event
+ *                 device time in rb_result_info.device_ms; 0: a solve the round graph
+ *                 finishes returns as soon as its results are visible in mapped host
+ *                 memory (completion flag), device_ms = -1. */
 int rb_set_option(rb_handle* h, const char* key, int64_t value);
 
 /* ---- system-specialised kernels ----------------------------------------------
