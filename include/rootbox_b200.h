@@ -207,8 +207,14 @@ int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const 
                            const uint8_t* duns, int64_t count);
 
 /* Engine tuning knobs (results never depend on them):
- *   "filter_tab"  1 (default): tabulated per-parent term filter when the tables fit;
- *                 0: direct per-child evaluation (k_filter).
+ *   "filter_tab"  1: tabulated per-parent term filter (k_filter_tab) when the tables
+ *                 fit; 0: direct per-child evaluation (k_filter).  Default: the direct
+ *                 filter when the system-specialised kernels are loaded (they beat the
+ *                 tables), else the tables when the F terms multiply several variables.
+ *   "force_exact" 0 (default): exponent guards pick IEEE directed rounding wherever it
+ *                 provably equals the reference; 1: every guard fails, so every box
+ *                 runs the Exact policy (the reference's error-free transformations,
+ *                 interval.py:66-205).  For the parity tests of that path.
  *   "graph"       1 (default): rounds whose worst case fits the survivor buffer run
  *                 in one CUDA graph (device-side WHILE loop, no host round trip);
  *                 0: host-driven rounds (per-kernel CUDA-event timings in the stats).
@@ -241,6 +247,26 @@ int rb_merge(int n, const double* init_lo, const double* init_hi, const double* 
              const uint8_t* cert, int64_t N, double stop_width, int stop_on_plateau, double* out_lo,
              double* out_hi, uint8_t* out_cert, int64_t cap, int64_t* M, double* levels, int64_t cap_levels,
              int64_t* K, char* err, int64_t err_len);
+
+/* ---- interval-layer known-answer hook (tests) --------------------------------
+ * m operand pairs through one device operation of interval.cuh on `device`
+ * (host arrays in and out).  x = [xl, xh], y = [yl, yh]; policy 0 = Fast (IEEE
+ * directed instructions), 1 = Exact (the reference's emulation,
+ * interval.py:66-205), 2 = guarded (what the kernels run: Fast when the exponent
+ * guard proves it equal to Exact, else Exact).
+ *   op 0..5   scalar _add_rd/_add_ru/_mul_rd/_mul_ru/_div_rd/_div_ru (xl, yl) -> o0
+ *   op 10     interval product x*y -> [o0, o1]       (interval.py:322-326)
+ *   op 11     recip(x) -> [o0, o1]                    (interval.py:347-351)
+ *   op 12     mid(x) -> o0                            (interval.py:269-281)
+ *   op 20+k   x**k (k = 0..9) -> [o0, o1]              (interval.py:328-345)
+ *   op 40     div_extended(x, y) -> kind, [o0, o1], [o2, o3]  (interval.py:394-432);
+ *             policy 0 = div_extended_fast (reciprocal fast path), 1 = forced Exact,
+ *             2 = div_extended with the guarded product
+ * Replaces no reference entry point: it exposes the device twins of the
+ * reference's scalar/interval functions to tests/test_gpu_exact.py. */
+int rb_interval_kat(int device, int op, int policy, int64_t m, const double* xl, const double* xh,
+                    const double* yl, const double* yh, double* o0, double* o1, double* o2, double* o3,
+                    int8_t* kind);
 
 /* ---- measurement utility ----------------------------------------------------
  * Measured throughput of the FP64 pipe on `device` for the directed-rounding

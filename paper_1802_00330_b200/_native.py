@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 
 import numpy as np
 
@@ -127,6 +128,8 @@ def lib():
     L.rb_codegen_prepare.restype = i32
     L.rb_codegen_active.argtypes = [P, C.c_char_p, i64]
     L.rb_codegen_active.restype = i32
+    L.rb_interval_kat.argtypes = [i32, i32, i32, i64, P, P, P, P, P, P, P, P, P]
+    L.rb_interval_kat.restype = i32
     _lib = L
     return L
 
@@ -135,7 +138,7 @@ EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch"
             "rb_last_error", "rb_destroy", "rb_shard_load", "rb_round_filter", "rb_round_hs",
             "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak", "rb_set_option",
             "rb_shard_partition", "rb_shard_dedup", "rb_shard_export_device", "rb_shard_import_device",
-            "rb_merge", "rb_krawczyk", "rb_codegen_prepare", "rb_codegen_active"]
+            "rb_merge", "rb_krawczyk", "rb_codegen_prepare", "rb_codegen_active", "rb_interval_kat"]
 
 
 def _p(a):
@@ -188,6 +191,10 @@ class Engine:
         _check(rc, None, "rb_create")
         self.h = h
         self._device_timing = True
+        # rb_solve + rb_fetch (and the other multi-call sequences below) run as one
+        # unit per engine: ctypes releases the GIL, and the engine cache hands the
+        # same Engine to every thread solving the same system.
+        self._lock = threading.RLock()
 
     def codegen_active(self):
         """(True, '') when the system-specialised kernels run, else (False, reason)."""
@@ -196,14 +203,24 @@ class Engine:
         return on == 1, why.value.decode(errors="replace")
 
     def set_option(self, key: str, value: int):
-        _check(lib().rb_set_option(self.h, key.encode(), int(value)), self.h, "rb_set_option")
-        if key == "device_timing":
-            self._device_timing = bool(value)
+        with self._lock:
+            self._live()
+            _check(lib().rb_set_option(self.h, key.encode(), int(value)), self.h, "rb_set_option")
+            if key == "device_timing":
+                self._device_timing = bool(value)
+
+    def _live(self):
+        if not self.h:
+            raise NativeError("engine is closed")
 
     def close(self):
-        if getattr(self, "h", None):
-            lib().rb_destroy(self.h)
-            self.h = None
+        lock = getattr(self, "_lock", None)
+        if lock is None:
+            return
+        with lock:  # waits for a solve in flight on another thread
+            if getattr(self, "h", None):
+                lib().rb_destroy(self.h)
+                self.h = None
 
     def __del__(self):
         try:
@@ -218,17 +235,19 @@ class Engine:
         returns as soon as its results are visible in mapped host memory, without
         waiting for the stream (device_ms is then -1)."""
         L = lib()
-        if device_timing != self._device_timing:
-            self.set_option("device_timing", 1 if device_timing else 0)
-            self._device_timing = device_timing
-        info = RbResultInfo()
-        _check(L.rb_solve(self.h, C.byref(cfg), C.byref(info)), self.h, "rb_solve")
-        N, n, nr = int(info.nboxes), self.n, int(info.nrounds)
-        lo = np.empty((N, n)); hi = np.empty((N, n))
-        flags = np.empty((2, N), np.uint8)  # cert, unsplit
-        stats = np.empty(max(1, nr), _STATS_DTYPE)
-        _check(L.rb_fetch(self.h, lo.ctypes.data, hi.ctypes.data, flags.ctypes.data, flags[1].ctypes.data,
-                          stats.ctypes.data), self.h, "rb_fetch")
+        with self._lock:
+            self._live()
+            if device_timing != self._device_timing:
+                self.set_option("device_timing", 1 if device_timing else 0)
+                self._device_timing = device_timing
+            info = RbResultInfo()
+            _check(L.rb_solve(self.h, C.byref(cfg), C.byref(info)), self.h, "rb_solve")
+            N, n, nr = int(info.nboxes), self.n, int(info.nrounds)
+            lo = np.empty((N, n)); hi = np.empty((N, n))
+            flags = np.empty((2, N), np.uint8)  # cert, unsplit
+            stats = np.empty(max(1, nr), _STATS_DTYPE)
+            _check(L.rb_fetch(self.h, lo.ctypes.data, hi.ctypes.data, flags.ctypes.data, flags[1].ctypes.data,
+                              stats.ctypes.data), self.h, "rb_fetch")
         rows = stats[:nr].tolist()
         fb = flags.view(np.bool_)
         return {"status": STATUS_NAMES[info.status], "lo": lo, "hi": hi, "cert": fb[0], "unsplit": fb[1],
@@ -243,8 +262,10 @@ class Engine:
         for _ in range(2):
             olo = np.empty((cap, self.n)); ohi = np.empty((cap, self.n))
             M = C.c_int64()
-            _check(lib().rb_filter(self.h, _p(plo), _p(phi), P, _p(olo), _p(ohi), cap, C.byref(M)), self.h,
-                   "rb_filter")
+            with self._lock:
+                self._live()
+                rc = lib().rb_filter(self.h, _p(plo), _p(phi), P, _p(olo), _p(ohi), cap, C.byref(M))
+                _check(rc, self.h, "rb_filter")
             if M.value <= cap:
                 return olo[:M.value].copy(), ohi[:M.value].copy()
             cap = M.value
@@ -256,8 +277,10 @@ class Engine:
         cap = max(1, 2 * M)
         olo = np.empty((cap, self.n)); ohi = np.empty((cap, self.n)); oc = np.empty(cap, np.uint8)
         M2 = C.c_int64()
-        _check(lib().rb_hs(self.h, _p(lo), _p(hi), M, int(bool(contract_output)), _p(olo), _p(ohi), _p(oc), cap,
-                           C.byref(M2)), self.h, "rb_hs")
+        with self._lock:
+            self._live()
+            _check(lib().rb_hs(self.h, _p(lo), _p(hi), M, int(bool(contract_output)), _p(olo), _p(ohi), _p(oc),
+                               cap, C.byref(M2)), self.h, "rb_hs")
         m = M2.value
         return olo[:m].copy(), ohi[:m].copy(), oc[:m].astype(bool)
 
@@ -265,8 +288,28 @@ class Engine:
         lo = np.ascontiguousarray(lo, np.float64); hi = np.ascontiguousarray(hi, np.float64)
         M = lo.shape[0]
         olo = np.empty((M, self.n)); ohi = np.empty((M, self.n)); ok = np.empty(M, np.uint8)
-        _check(lib().rb_krawczyk(self.h, _p(lo), _p(hi), M, _p(olo), _p(ohi), _p(ok)), self.h, "rb_krawczyk")
+        with self._lock:
+            self._live()
+            _check(lib().rb_krawczyk(self.h, _p(lo), _p(hi), M, _p(olo), _p(ohi), _p(ok)), self.h, "rb_krawczyk")
         return ok.astype(bool), olo, ohi
+
+
+KAT_OPS = {"_add_rd": 0, "_add_ru": 1, "_mul_rd": 2, "_mul_ru": 3, "_div_rd": 4, "_div_ru": 5,
+           "mul": 10, "recip": 11, "mid": 12, "div_extended": 40}
+KAT_POLICY = {"fast": 0, "exact": 1, "guarded": 2}
+
+
+def interval_kat(op, policy, xl, xh, yl=None, yh=None, device: int = 0):
+    """One interval.cuh operation on the device over arrays (rb_interval_kat): op is a
+    name of KAT_OPS or ("pow", k); returns (o0, o1, o2, o3, kind)."""
+    code = 20 + int(op[1]) if isinstance(op, tuple) else KAT_OPS[op]
+    arr = [np.ascontiguousarray(v, np.float64) for v in (xl, xh, xl if yl is None else yl, xh if yh is None else yh)]
+    m = arr[0].size
+    outs = [np.empty(m) for _ in range(4)]
+    kind = np.empty(m, np.int8)
+    _check(lib().rb_interval_kat(int(device), code, KAT_POLICY[policy], m, *[_p(a) for a in arr],
+                                 *[_p(o) for o in outs], _p(kind)), None, "rb_interval_kat")
+    return (*outs, kind)
 
 
 def device_count() -> int:

@@ -206,7 +206,9 @@ def engine_for(spec: SystemSpec, device: int | None = None) -> _native.Engine:
         e = _ENGINES.get((key, device))
         if e is None:
             if len(_ENGINES) >= _MAX_ENGINES:
-                _ENGINES.pop(next(iter(_ENGINES))).close()
+                # dropped, not closed: a thread still solving on it holds a reference,
+                # and the engine is destroyed with its last reference (Engine.__del__)
+                _ENGINES.pop(next(iter(_ENGINES)))
             e = _native.Engine(tables, device)
             _ENGINES[(key, device)] = e
         return e
@@ -260,10 +262,11 @@ class RootBoxes(Sequence):
     iteration, ``len`` and equality with a tuple behave like the tuple the
     reference returns; ``.lo/.hi/.cert/.unsplit`` expose the arrays."""
 
-    __slots__ = ("lo", "hi", "cert", "unsplit", "_types")
+    __slots__ = ("lo", "hi", "cert", "unsplit", "_types", "_hash")
 
     def __init__(self, lo, hi, cert, unsplit, types):
         self.lo, self.hi, self.cert, self.unsplit, self._types = lo, hi, cert, unsplit, types
+        self._hash = None
 
     def __len__(self):
         return self.lo.shape[0]
@@ -294,6 +297,19 @@ class RootBoxes(Sequence):
         if isinstance(other, (tuple, list)):
             return len(other) == len(self) and all(a == b for a, b in zip(self, other))
         return NotImplemented
+
+    def __hash__(self):
+        # equal to a tuple of the same RootBox objects, so hash like that tuple (the
+        # reference's frozen SolveResult hashes its boxes tuple)
+        if self._hash is None:
+            self._hash = hash(tuple(self))
+        return self._hash
+
+    def __add__(self, other):
+        return tuple(self) + tuple(other)
+
+    def __radd__(self, other):
+        return tuple(other) + tuple(self)
 
     def __repr__(self):
         return f"RootBoxes({len(self)} boxes)"

@@ -355,6 +355,8 @@ static void build_tables(rb_handle* h, const rb_system* sys) {
     // ops_HS = ops_J + 2n^2 (mid) + ops_GJ + 2n (mid x) + ops_F + 4n^2 (g) + 4n^3 (M) + sweep
     m.ops_hs_pre = ops_j + 2 * n * n + ops_gj + 2 * n + ops_f + 4 * n * n + 4 * n * n * n;
     m.ops_hs_row = 6 * (n - 1) + 8;
+    h->guard_f_ecmin = m.f_ecmin;
+    h->guard_j_ecmin = m.j_ecmin;
     h->meta = m;
     dalloc(&h->d_tab, (size_t)m.bytes3);
     ck(cudaMemcpyAsync(h->d_tab, buf.data(), m.bytes3, cudaMemcpyHostToDevice, h->st), "tables h2d");
@@ -1080,6 +1082,7 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     key.push_back((uintptr_t)h->hx_stats_dev);
     key.push_back((uintptr_t)h->pdl);
     key.push_back((uintptr_t)h->trace);
+    key.push_back((uintptr_t)h->force_exact);
     if (key != h->graph_key || !h->graph_exec) build_round_graph(h, prm, dedup, scap, key);
     DevState st{};
     st.n_cur = 1;
@@ -2061,6 +2064,13 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     }
     if (k == "graph") {
         h->use_graph = value != 0;
+        return RB_OK;
+    }
+    if (k == "force_exact") {  // Exact policy everywhere (parity tests of interval.cuh's Exact)
+        h->force_exact = value != 0;
+        // poly_guard_ok fails for any coefficient exponent below -965 (kernels.cuh)
+        h->meta.f_ecmin = h->force_exact ? -100000 : h->guard_f_ecmin;
+        h->meta.j_ecmin = h->force_exact ? -100000 : h->guard_j_ecmin;
         return RB_OK;
     }
     h->err = "unknown option " + k;

@@ -205,6 +205,11 @@ struct rb_handle {
     int fused_blocks_per_sm = 1;
     HsScratch W{};
     int smem_optin = 48 * 1024;
+    // rb_set_option("force_exact"): every exponent guard fails, so the filter, HS and
+    // sweep run the Exact policy (interval.cuh) on every box -- the parity tests of
+    // that path; the guard constants of build_tables are kept here to restore them
+    bool force_exact = false;
+    int guard_f_ecmin = 0, guard_j_ecmin = 0;
 };
 
 struct PoolScope {

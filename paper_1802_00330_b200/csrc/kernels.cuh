@@ -206,12 +206,13 @@ __device__ __forceinline__ bool prod_in_band(double v) {
 // operands reached the reference's untrusted band (a nonzero exact product below
 // it has its away-from-zero rounding nonzero and below 2^-965), so the Dekker
 // error is exact and IEEE RD/RU equal _mul_rd/_mul_ru (interval.py:98-136).
-__device__ __forceinline__ ival gmul(ival x, ival y) {
+// force: always take the Exact product (rb_set_option "force_exact", parity tests of the Exact policy)
+__device__ __forceinline__ ival gmul(ival x, ival y, bool force = false) {
     const double p0 = __dmul_rd(x.lo, y.lo), p1 = __dmul_rd(x.lo, y.hi);
     const double p2 = __dmul_rd(x.hi, y.lo), p3 = __dmul_rd(x.hi, y.hi);
     const double q0 = __dmul_ru(x.lo, y.lo), q1 = __dmul_ru(x.lo, y.hi);
     const double q2 = __dmul_ru(x.hi, y.lo), q3 = __dmul_ru(x.hi, y.hi);
-    const bool ok = op_small(x.lo) & op_small(x.hi) & op_small(y.lo) & op_small(y.hi) & prod_in_band(p0) &
+    const bool ok = !force & op_small(x.lo) & op_small(x.hi) & op_small(y.lo) & op_small(y.hi) & prod_in_band(p0) &
                     prod_in_band(p1) & prod_in_band(p2) & prod_in_band(p3) & prod_in_band(q0) & prod_in_band(q1) &
                     prod_in_band(q2) & prod_in_band(q3);
     if (ok) return mk(py_min(py_min(p0, p1), py_min(p2, p3)), py_max(py_max(q0, q1), py_max(q2, q3)));
@@ -221,10 +222,10 @@ __device__ __forceinline__ ival gmul(ival x, ival y) {
 enum { DIV_EMPTY = 0, DIV_SINGLE = 1, DIV_SPLIT = 2, DIV_WHOLE = 3 };
 
 // interval.py:394-432 (div_extended), Hanson/Kahan case table.
-static __device__ __noinline__ int div_extended(ival x, ival y, ival& p0, ival& p1) {
+static __device__ __noinline__ int div_extended(ival x, ival y, ival& p0, ival& p1, bool force = false) {
     if (!contains_zero(y)) {
         ival r = mk(div_rd(1.0, y.hi), div_ru(1.0, y.lo));  // recip, interval.py:347-351
-        p0 = gmul(x, r);  // guarded product: Fast when provably trusted
+        p0 = gmul(x, r, force);  // guarded product: Fast when provably trusted
         return DIV_SINGLE;
     }
     if (y.lo == 0.0 && y.hi == 0.0) {
@@ -1219,6 +1220,7 @@ struct HsParams {
     DevRoundStats* rstats;
     int* eq_order;
     int64_t s_cap;
+    int force_exact;       // every guard fails: the Exact policy everywhere (parity tests)
 };
 
 struct HsScratch {         // SoA with stride B (batch capacity)
@@ -1501,7 +1503,7 @@ static __device__ __noinline__ void lin_products_exact(const double* Am, const i
 // M = A J and g = A F(x) over J / F(x) in place.  Returns true when singular.
 template <int N, int G>
 __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* sCol, int l, unsigned gmask,
-                                          bool& exact_lin, unsigned long long* pr = nullptr) {
+                                          bool& exact_lin, bool force, unsigned long long* pr = nullptr) {
     // J column (l % N), kept in registers for M
     ival jcol[N];
     double c[N];
@@ -1640,7 +1642,7 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
     group_reduce<G>(gmask, rf);
     rj.emin = min(rj.emin, rf.emin);
     rj.emax = max(rj.emax, rf.emax);
-    const bool fastM = prod_guard_ok(ra, rj);
+    const bool fastM = !force && prod_guard_ok(ra, rj);
     if (pr) pr[3] = clock64() + (unsigned long long)fastM * 0ull;
     __syncwarp(gmask);
     if (fastM) lin_products<N, Fast>(Am, jcol, l, K, gmask);
@@ -1673,7 +1675,7 @@ __global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_
             const int64_t t = b - b0;
             const LinSink K{W.jl + t, W.jh + t, W.fl + t, W.fh + t, W.B};
             bool exact_lin;
-            const bool singular = lin_group<N, G>(K, s + L::oA, s + L::oCol, l, gmask, exact_lin);
+            const bool singular = lin_group<N, G>(K, s + L::oA, s + L::oCol, l, gmask, exact_lin, prm.force_exact);
             if (l == 0) W.flags[t] |= singular ? HSF_SINGULAR : (exact_lin ? HSF_EXACT_LIN : 0);
             __syncwarp(gmask);
         }
@@ -1749,8 +1751,8 @@ __device__ __forceinline__ double recip_dir(double y, bool up) {
 }
 
 // fast reciprocal-based single case of div_extended; exact emulation elsewhere
-__device__ __forceinline__ int div_extended_fast(ival p, ival y, ival& q0, ival& q1) {
-    if (!contains_zero(y)) {
+__device__ __forceinline__ int div_extended_fast(ival p, ival y, ival& q0, ival& q1, bool force = false) {
+    if (!force && !contains_zero(y)) {
         const double al = fabs(y.lo), ah = fabs(y.hi);
         if (al > 0x1p-990 && ah < 0x1p990) {
             // _div_rd/_div_ru (interval.py:157-190) == IEEE directed division inside the trusted band
@@ -1759,7 +1761,7 @@ __device__ __forceinline__ int div_extended_fast(ival p, ival y, ival& q0, ival&
             return DIV_SINGLE;
         }
     }
-    return div_extended(p, y, q0, q1);
+    return div_extended(p, y, q0, q1, force);
 }
 
 // K2c: thread per box: the Gauss-Seidel sweep (hansen.py:91-138) and the
@@ -1815,7 +1817,7 @@ __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t 
                         if (j == i) continue;
                         if (mrow[j].lo == 0.0 && mrow[j].hi == 0.0) continue;
                         const ival d = Fast::sub(mk(cl[j * stride], ch[j * stride]), mk(xv[j], xv[j]));
-                        p = Fast::sub(p, gmul(mrow[j], d));
+                        p = Fast::sub(p, gmul(mrow[j], d, prm.force_exact));
                     }
                     ival mii = mrow[0];
                     double xi = xv[0];
@@ -1826,7 +1828,7 @@ __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t 
                             xi = xv[j];
                         }
                     ival q0 = mk(0.0, 0.0), q1 = mk(0.0, 0.0);
-                    const int dk = div_extended_fast(p, mii, q0, q1);
+                    const int dk = div_extended_fast(p, mii, q0, q1, prm.force_exact);
                     if (dk == DIV_EMPTY) {
                         kind = HS_EMPTY;
                         break;
@@ -2156,7 +2158,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
             if (brec) brec[1] = gtimer();
             // ---- lin: A = mid(J)^-1, M = A J, g = A F(x)
             bool exact_lin;
-            const bool singular = lin_group<N, G>(K, s + L::oA, s + L::oCol, l, gmask, exact_lin,
+            const bool singular = lin_group<N, G>(K, s + L::oA, s + L::oCol, l, gmask, exact_lin, prm.force_exact,
                                                   (prof && wb0 == 0) ? prm.prof + 11 : nullptr);
             __syncwarp(gmask);
             if (prof && wb0 == 0) prm.prof[6] = clock64();
@@ -2173,7 +2175,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                 ival dinv = mk(0.0, 0.0);
                 if (l < N) {
                     const ival y = mk(s[L::oJl + l * N + l], s[L::oJh + l * N + l]);
-                    dfast = !contains_zero(y) && fabs(y.lo) > 0x1p-990 && fabs(y.hi) < 0x1p990;
+                    dfast = !prm.force_exact && !contains_zero(y) && fabs(y.lo) > 0x1p-990 && fabs(y.hi) < 0x1p990;
                     if (dfast) dinv = mk(recip_dir(y.hi, false), recip_dir(y.lo, true));
                 }
 #pragma unroll 1
@@ -2184,7 +2186,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                     if (l < N && l != i) {
                         const ival m = mk(s[L::oJl + i * N + l], s[L::oJh + i * N + l]);
                         use = !(m.lo == 0.0 && m.hi == 0.0);
-                        if (use) prod = gmul(m, Fast::sub(cur, mk(xj, xj)));
+                        if (use) prod = gmul(m, Fast::sub(cur, mk(xj, xj)), prm.force_exact);
                     }
                     const unsigned um = __ballot_sync(gmask, use) >> (gi * G);
                     // p = -g_i - sum_{j != i, M_ij != [0,0]} M_ij (current_j - [x_j, x_j]), left to right
@@ -2206,7 +2208,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
                         q0 = gmul(p, ri);
                         dk = DIV_SINGLE;
                     } else {
-                        dk = div_extended(p, mii, q0, q1);
+                        dk = div_extended(p, mii, q0, q1, prm.force_exact);
                     }
                     if (dk == DIV_EMPTY) {
                         kind = HS_EMPTY;

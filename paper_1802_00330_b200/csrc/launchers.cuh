@@ -111,6 +111,7 @@ void FilterK<N>::run(rb_handle* h, int64_t max_parents, int64_t* tags) {
 
 template <int N>
 void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* tags, int64_t batch_bound) {
+    prm.force_exact = h->force_exact ? 1 : 0;
     const int T = h->hs_threads;
     const int64_t B = h->W.B;
     Front out = h->F[h->cur ^ 1].f;
@@ -133,6 +134,7 @@ void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* 
 
 template <int N>
 void HsFusedK<N>::run(rb_handle* h, int64_t n_in, HsParams prm, int64_t* tags, int64_t bound) {
+    prm.force_exact = h->force_exact ? 1 : 0;
     const int T = h->hs_threads;
     h->launches++;
     const int64_t lanes = std::max<int64_t>(1, bound) * FusedLayout<N>::G;

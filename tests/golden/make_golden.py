@@ -85,8 +85,17 @@ def quirk17b_text():
     return "vars: x y\ninit: x in [0,2]; y in [-2,2]\neq: x - 1\neq: y^3 - y - 1\n"
 
 
+def wide_circle_text():
+    # coefficients 2^1000 > 2^995: every product with them is in the reference's
+    # "untrusted" band (interval.py:38-39, 98-136), so the engine's exponent guards
+    # must route the filter, HS preconditioning and sweep to the Exact policy
+    return ("vars: x y\ninit: x in [-2,2]; y in [-2,2]\n"
+            "eq: 2^1000*x^2 + 2^1000*y^2 - 2^1000\neq: x - y\n")
+
+
 def synthetic_texts():
     return {
+        "wide_circle": wide_circle_text(),
         "circle_line": circle_line_text(),
         "broyden_tri4": broyden_tri_text(4, -2, 2),
         "broyden_tri6": broyden_tri_text(6, -2, 2),
@@ -407,6 +416,9 @@ SOLVE_CASES = [
     ("mickey_maxboxes", "mickey", dict(max_boxes=3), False),
     ("rediff3_rounds3", "rediff3", dict(max_rounds=3), False),
     ("brown5", "brown5", dict(target_width=1e-8), False),
+    ("wide_circle", "wide_circle", dict(target_width=1e-6), True),
+    ("wide_circle_r8", "wide_circle", dict(target_width=1e-6, max_rounds=8, hs_enable_round=1,
+                                          hs_enable_width=None), False),
     ("broyden_banded6", "broyden_banded6", dict(target_width=1e-8), False),
     # slow (tens of seconds to minutes on one core)
     ("trinks1", "trinks1", dict(), False),
@@ -510,8 +522,10 @@ def run_solve_case(case):
     return cname, res.status, N, wall
 
 
-def part_solve(which):
+def part_solve(which, only=None):
     cases = [c for c in SOLVE_CASES if (c[0] in SLOW) == (which == "slow")]
+    if only:
+        cases = [c for c in SOLVE_CASES if c[0] in only]
     with ProcessPoolExecutor(max_workers=min(8, len(cases))) as ex:
         for cname, status, N, wall in ex.map(run_solve_case, cases):
             print(f"solve {cname}: {status} boxes={N} wall={wall:.1f}s", flush=True)
@@ -612,6 +626,7 @@ def part_krawczyk():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--part", nargs="*", default=["systems", "interval", "poly", "gj", "hs", "solve"])
+    ap.add_argument("--case", nargs="*", default=None, help="solve only these SOLVE_CASES")
     a = ap.parse_args()
     for p in a.part:
         t0 = time.time()
@@ -626,7 +641,7 @@ def main():
         elif p == "hs":
             part_hs()
         elif p == "solve":
-            part_solve("fast")
+            part_solve("fast", a.case)
         elif p == "solve_slow":
             part_solve("slow")
         elif p == "merge":

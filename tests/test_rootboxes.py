@@ -23,3 +23,14 @@ def test_rootboxes_sequence_semantics():
     empty = RootBoxes(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros(0, bool), np.zeros(0, bool),
                       (RootBox, Box, Interval))
     assert not empty and len(empty) == 0 and empty == ()
+
+
+def test_rootboxes_hash_and_concat():
+    """A frozen SolveResult holding RootBoxes is hashable like the tuple it equals."""
+    from paper_1802_00330_b200.bnb import SolveResult
+    lo, hi, c, u = _mk()
+    rb = RootBoxes(lo, hi, c, u, (RootBox, Box, Interval))
+    eager = tuple(rb)
+    assert hash(rb) == hash(eager)
+    assert hash(SolveResult("width_reached", rb, ())) == hash(SolveResult("width_reached", eager, ()))
+    assert rb + () == eager and () + rb == eager and rb + rb == eager + eager
