@@ -206,6 +206,25 @@ int rb_shard_export_device(rb_handle* h, int64_t start, int64_t count, double* d
 int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const double* dhi, const uint8_t* dcert,
                            const uint8_t* duns, int64_t count);
 
+/* Frontier routing between shards: only rows with a component at
+ * most 64 ulps wide can have an exact duplicate on another shard, so only those go
+ * to their hash owner; the rest stay, except the surplus rows a rebalancing plan
+ * moves.  rb_shard_route_count: thin rows per owner rank (thin_counts [world]) and
+ * the number of other rows (*nonthin).  rb_shard_route (after route_count):
+ * move[d] non-thin rows go to rank d (move[rank] ignored); reorders the shard as
+ * [own rows | rows for rank 0 | rank 1 | ...] and returns the row count per
+ * destination (send_counts[rank] = rows that stay).  The caller then exports rows
+ * [send_counts[rank], size) for the exchange and imports the received rows with
+ * keep = send_counts[rank].  Replaces the per-round row movement of the
+ * reference's thread pool (bnb.py:183-187, 271-313), which has no shards. */
+int rb_shard_route_count(rb_handle* h, int32_t world, int64_t* thin_counts, int64_t* nonthin);
+int rb_shard_route(rb_handle* h, int32_t world, int32_t rank, const int64_t* move, int64_t* send_counts);
+
+/* Canonical order (_batch.canonical_order, _batch.py:244-250) of the shard's rows
+ * into the result buffers, so rb_fetch returns them (the gathered final frontier of
+ * a sharded solve, bnb.py:322-326); *nboxes receives the row count. */
+int rb_shard_finalize(rb_handle* h, int64_t* nboxes);
+
 /* Engine tuning knobs (results never depend on them):
  *   "filter_tab"  1: tabulated per-parent term filter (k_filter_tab) when the tables
  *                 fit; 0: direct per-child evaluation (k_filter).  Default: the direct

@@ -128,6 +128,12 @@ def lib():
     L.rb_codegen_prepare.restype = i32
     L.rb_codegen_active.argtypes = [P, C.c_char_p, i64]
     L.rb_codegen_active.restype = i32
+    L.rb_shard_route_count.argtypes = [P, i32, P, C.POINTER(i64)]
+    L.rb_shard_route_count.restype = i32
+    L.rb_shard_route.argtypes = [P, i32, i32, P, P]
+    L.rb_shard_route.restype = i32
+    L.rb_shard_finalize.argtypes = [P, C.POINTER(i64)]
+    L.rb_shard_finalize.restype = i32
     L.rb_interval_kat.argtypes = [i32, i32, i32, i64, P, P, P, P, P, P, P, P, P]
     L.rb_interval_kat.restype = i32
     _lib = L
@@ -138,7 +144,8 @@ EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch"
             "rb_last_error", "rb_destroy", "rb_shard_load", "rb_round_filter", "rb_round_hs",
             "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak", "rb_set_option",
             "rb_shard_partition", "rb_shard_dedup", "rb_shard_export_device", "rb_shard_import_device",
-            "rb_merge", "rb_krawczyk", "rb_codegen_prepare", "rb_codegen_active", "rb_interval_kat"]
+            "rb_merge", "rb_krawczyk", "rb_codegen_prepare", "rb_codegen_active", "rb_interval_kat",
+            "rb_shard_route_count", "rb_shard_route", "rb_shard_finalize"]
 
 
 def _p(a):

@@ -732,6 +732,7 @@ static void release_all(rb_handle* h) {
     fr(h->W.flags);
     fr(h->d_trace);
     fr(h->d_bar);
+    fr(h->d_route);
     if (h->st) cudaStreamSynchronize(h->st);  // frees are stream-ordered; the pool is shared
     h->pool = nullptr;
     graph_release(h);
@@ -1984,6 +1985,49 @@ int rb_shard_import_device(rb_handle* h, int64_t keep, const double* dlo, const 
             ck(cudaStreamSynchronize(h->st), "import sync");
         }
         h->n_cur = keep + count;
+    })
+}
+
+int rb_shard_route_count(rb_handle* h, int32_t world, int64_t* thin_counts, int64_t* nonthin) {
+    if (!h || world < 1 || !thin_counts || !nonthin) return RB_ERR_ARG;
+    std::lock_guard<std::mutex> lk(h->mu);
+    RB_GUARD(h, {
+        ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
+        PoolScope ps(h);
+        fronts_reserve(h, std::max<int64_t>(h->n_cur, 1));
+        dispatch_n<RouteCountK>(h->n, h, (int)world, thin_counts, nonthin);
+    })
+}
+
+int rb_shard_route(rb_handle* h, int32_t world, int32_t rank, const int64_t* move, int64_t* send_counts) {
+    if (!h || world < 1 || rank < 0 || rank >= world || !move || !send_counts) return RB_ERR_ARG;
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (h->cap_route < h->n_cur || !h->d_route) {
+        h->err = "rb_shard_route before rb_shard_route_count";
+        return RB_ERR_STATE;
+    }
+    RB_GUARD(h, {
+        ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
+        PoolScope ps(h);
+        fronts_reserve(h, std::max<int64_t>(h->n_cur, 1));
+        dispatch_n<RouteK>(h->n, h, (int)world, (int)rank, move, send_counts);
+    })
+}
+
+int rb_shard_finalize(rb_handle* h, int64_t* nboxes) {
+    if (!h) return RB_ERR_ARG;
+    std::lock_guard<std::mutex> lk(h->mu);
+    RB_GUARD(h, {
+        ck(cudaSetDevice(h->dev), "cudaSetDevice");
+        codegen_poll(h);
+        PoolScope ps(h);
+        h->stats.clear();
+        h->r_ready = false;
+        finalize_sorted(h);
+        h->have_result = true;
+        if (nboxes) *nboxes = h->r_n;
     })
 }
 

@@ -209,6 +209,8 @@ struct rb_handle {
     // sweep run the Exact policy (interval.cuh) on every box -- the parity tests of
     // that path; the guard constants of build_tables are kept here to restore them
     bool force_exact = false;
+    unsigned* d_route = nullptr;   // per-row destination of the shard routing (RouteCountK / RouteK)
+    int64_t cap_route = 0;
     int guard_f_ecmin = 0, guard_j_ecmin = 0;
 };
 
@@ -423,8 +425,20 @@ struct WidthK {
     static void run(rb_handle* h);
 };
 
+// frontier routing between shards: thin rows to their hash owner, `move[d]` surplus
+// rows to rank d; F[cur] becomes [own rows | rows for rank 0 | rank 1 | ...]
+template <int N>
+struct RouteCountK {
+    static void run(rb_handle* h, int world, int64_t* thin_counts, int64_t* nonthin);
+};
+template <int N>
+struct RouteK {
+    static void run(rb_handle* h, int world, int rank, const int64_t* move, int64_t* send_counts);
+};
+
 
 // every launcher template, for explicit instantiation (kinst.cu) and extern declarations (engine.cu)
 #define RB_LAUNCHERS(X, K)                                                                              \
     X SetupK<K>; X ClassifyK<K>; X ClassifyFilterK<K>; X AllParentsK<K>; X FilterK<K>; X HsK<K>; X HsFusedK<K>; X KrawczykK<K>; \
-    X SmallRoundsK<K>; X DedupInsertK<K>; X TailK<K>; X SettleK<K>; X DedupK<K>; X PartitionK<K>; X WidthK<K>;
+    X SmallRoundsK<K>; X DedupInsertK<K>; X TailK<K>; X SettleK<K>; X DedupK<K>; X PartitionK<K>; X WidthK<K>; \
+    X RouteCountK<K>; X RouteK<K>;

@@ -1651,152 +1651,6 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
     return false;
 }
 
-// lin_group for throughput (k_hs_lin, n <= 8, several boxes per warp): the same
-// operations in the same order, written so the whole warp stays converged -- every
-// group runs every step (a group without a box computes on a copy of a valid one and
-// stores nothing), a singular box keeps computing under a flag instead of leaving
-// the loop, and shuffles use the full-warp mask.  Divergent groups made the
-// compiler wrap every shuffle in WARPSYNC/ENDCOLLECTIVE sequences (SASS of the
-// previous k_hs_lin<7>: 135 of them, 2,860 warp instructions per pair of boxes).
-template <int N, int G>
-__device__ __forceinline__ bool lin_warp(const LinSink& K, bool store, double* Am, int l, bool& exact_lin,
-                                         bool force) {
-    static_assert(N <= 8, "lin_warp: the pivot column is broadcast by shuffles");
-    constexpr unsigned FULL = 0xffffffffu;
-    ival jcol[N];
-    double c[N];
-    double colmax = 0.0;
-    ExpRange rj;
-    rj.init();
-    const int col = l % N;
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-        jcol[i] = l < 2 * N ? mk(K.jl[(i * N + col) * K.ws], K.jh[(i * N + col) * K.ws]) : mk(0.0, 0.0);
-        rj.add(jcol[i].lo);
-        rj.add(jcol[i].hi);
-    }
-    if (l < N) {
-#pragma unroll
-        for (int i = 0; i < N; i++) {
-            c[i] = mid_of(jcol[i].lo, jcol[i].hi);  // mid_matrix, linalg.py:132-134
-            colmax = fmax(colmax, fabs(c[i]));
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < N; i++) c[i] = (l - N == i) ? 1.0 : 0.0;
-    }
-    // Gauss-Jordan inverse (linalg.py:137-172), lane = column of [jc | I]
-    double scale = l < N ? colmax : 0.0;
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) {
-        const double w = __shfl_xor_sync(FULL, scale, o, G);
-        scale = w > scale ? w : scale;
-    }
-    bool singular = scale == 0.0;
-    const double threshold = __dmul_rn(1e-12, scale);
-#pragma unroll
-    for (int k = 0; k < N; k++) {
-        double colk[N];
-#pragma unroll
-        for (int i = 0; i < N; i++) colk[i] = __shfl_sync(FULL, c[i], k, G);
-        int pr = k;  // first row r >= k with max |c[r][k]|
-        double best = fabs(colk[k]), pivot = colk[k];
-#pragma unroll
-        for (int r = k + 1; r < N; r++)
-            if (fabs(colk[r]) > best) {
-                best = fabs(colk[r]);
-                pr = r;
-                pivot = colk[r];
-            }
-        singular = singular || fabs(pivot) < threshold;
-        // a singular box finishes the loop on whatever values it has; its result is unused
-#pragma unroll
-        for (int r = k + 1; r < N; r++)
-            if (r == pr) {
-                const double tmp = c[k];
-                c[k] = c[r];
-                c[r] = tmp;
-            }
-        const double inv = __drcp_rn(pivot);  // RN(1/pivot) == 1.0 / pivot (linalg.py:160)
-        if (l >= k && l < 2 * N) {
-            c[k] = __dmul_rn(c[k], inv);
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                if (i == k) continue;
-                const double f = i == pr ? colk[k] : colk[i];  // column k after the row swap
-                c[i] = __dsub_rn(c[i], __dmul_rn(f, c[k]));
-            }
-        }
-    }
-    exact_lin = false;
-    ExpRange ra, rf;
-    ra.init();
-    rf.init();
-    if (l >= N && l < 2 * N) {
-#pragma unroll
-        for (int i = 0; i < N; i++) {
-            Am[i * N + (l - N)] = c[i];
-            ra.add(c[i]);
-        }
-    }
-    if (l < N) {
-        rf.add(K.fl[l * K.ws]);
-        rf.add(K.fh[l * K.ws]);
-    }
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) {
-        ra.emin = min(ra.emin, __shfl_xor_sync(FULL, ra.emin, o, G));
-        ra.emax = max(ra.emax, __shfl_xor_sync(FULL, ra.emax, o, G));
-        rj.emin = min(rj.emin, __shfl_xor_sync(FULL, rj.emin, o, G));
-        rj.emax = max(rj.emax, __shfl_xor_sync(FULL, rj.emax, o, G));
-        rf.emin = min(rf.emin, __shfl_xor_sync(FULL, rf.emin, o, G));
-        rf.emax = max(rf.emax, __shfl_xor_sync(FULL, rf.emax, o, G));
-    }
-    rj.emin = min(rj.emin, rf.emin);
-    rj.emax = max(rj.emax, rf.emax);
-    const bool fastM = !force && prod_guard_ok(ra, rj);
-    __syncwarp();
-    // M = A J and g = A F(x) (linalg.py:102-129); a singular or absent box stores nothing
-    const bool st = store && !singular;
-    constexpr int H = (N + 1) / 2;
-    if (fastM) {
-        ival acc[H];
-        const int half = l / N;
-#pragma unroll
-        for (int r = 0; r < H; r++) {
-            const int i = min(half * H + r, N - 1);
-            acc[r] = mk(0.0, 0.0);
-#pragma unroll
-            for (int u = 0; u < N; u++) acc[r] = Fast::add(acc[r], pmul<Fast, N>(Am[i * N + u], jcol[u]));
-        }
-        ival g = mk(0.0, 0.0);
-        if (l < N) {
-#pragma unroll
-            for (int u = 0; u < N; u++)
-                g = Fast::add(g, pmul<Fast, N>(Am[l * N + u], mk(K.fl[u * K.ws], K.fh[u * K.ws])));
-        }
-        __syncwarp();  // every lane has read F(x) before g overwrites it
-        if (st && l < 2 * N) {
-#pragma unroll
-            for (int r = 0; r < H; r++) {
-                const int i = half * H + r;
-                if (i < N) {
-                    K.jl[(i * N + col) * K.ws] = acc[r].lo;
-                    K.jh[(i * N + col) * K.ws] = acc[r].hi;
-                }
-            }
-        }
-        if (st && l < N) {
-            K.fl[l * K.ws] = g.lo;
-            K.fh[l * K.ws] = g.hi;
-        }
-    } else if (st) {  // rare: the Exact policy (noinline), only for real boxes
-        lin_products_exact<N>(Am, jcol, l, K, __activemask());
-        exact_lin = true;
-    }
-    return singular;
-}
-
 // K2b: G lanes per box; boxes assigned warp-uniformly.
 template <int N>
 __global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
@@ -1817,15 +1671,7 @@ __global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_
     const int64_t wglob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     for (int64_t wb0 = b0 + wglob * L::BPW; wb0 < b_end; wb0 += warps_total * L::BPW) {
         const int64_t b = wb0 + gi;
-        if constexpr (N <= 8) {  // warp-convergent: a group past the end works on the last box
-            const bool valid = b < b_end;
-            const int64_t t = (valid ? b : b_end - 1) - b0;
-            const LinSink K{W.jl + t, W.jh + t, W.fl + t, W.fh + t, W.B};
-            bool exact_lin;
-            const bool singular = lin_warp<N, G>(K, valid, s + L::oA, l, exact_lin, prm.force_exact);
-            if (valid && l == 0) W.flags[t] |= singular ? HSF_SINGULAR : (exact_lin ? HSF_EXACT_LIN : 0);
-            __syncwarp();
-        } else if (b < b_end) {
+        if (b < b_end) {
             const int64_t t = b - b0;
             const LinSink K{W.jl + t, W.jh + t, W.fl + t, W.fh + t, W.B};
             bool exact_lin;
@@ -2972,6 +2818,56 @@ __global__ void k_owner_scatter(Front src, int64_t n, const unsigned* owner, uns
         }
         dst.cert[slot] = src.cert[i];
         dst.unsplit[slot] = src.unsplit[i];
+    }
+}
+
+// Frontier routing between shards.  Only a row with a component at
+// most kThinUlps wide can have an exact duplicate elsewhere (see kThinUlps above), so
+// only thin rows go to their hash owner; every other row stays, except the surplus
+// rows the rebalancing plan moves (any non-thin row will do: the round's results do
+// not depend on where a row is processed).
+//   pass 1 (k_route_count): dest[i] = hash owner for thin rows, 0xffffffff otherwise;
+//           thin rows counted per owner, non-thin rows counted
+//   pass 2 (k_route_assign): non-thin rows take a surplus slot t (atomic) while
+//           t < move_total; slot t goes to the destination d with
+//           move_off[d] <= t < move_off[d + 1]; the rest stay on `rank`; rows counted
+//           per destination
+//   then k_owner_scatter into [own rows | rows for rank 0 | rank 1 | ...]
+template <int N>
+__global__ void k_route_count(Front f, int64_t n, int world, unsigned* dest, unsigned long long* counts) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        bool thin = false;
+#pragma unroll
+        for (int j = 0; j < N; j++) thin = thin || thin_comp(f.lo[j * f.cap + i], f.hi[j * f.cap + i]);
+        unsigned d = 0xffffffffu;
+        if (thin) {
+            d = (unsigned)(row_hash<N>(f, i) % (unsigned long long)world);
+            atomicAdd(&counts[d], 1ull);
+        } else {
+            atomicAdd(&counts[world], 1ull);
+        }
+        dest[i] = d;
+    }
+}
+
+static __global__ void k_route_assign(int64_t n, int world, int rank, unsigned* dest, const unsigned long long* move_off,
+                               unsigned long long* taken, unsigned long long* counts) {
+    const unsigned long long total = move_off[world];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned d = dest[i];
+        if (d == 0xffffffffu) {
+            d = (unsigned)rank;
+            if (total) {
+                const unsigned long long t = atomicAdd(taken, 1ull);
+                if (t < total) {
+                    int k = 0;
+                    while (k + 1 < world && move_off[k + 1] <= t) k++;
+                    d = (unsigned)k;
+                }
+            }
+            dest[i] = d;
+        }
+        atomicAdd(&counts[d], 1ull);
     }
 }
 

@@ -283,6 +283,73 @@ void PartitionK<N>::run(rb_handle* h, int world, int64_t* counts) {
 }
 
 template <int N>
+void RouteCountK<N>::run(rb_handle* h, int world, int64_t* thin_counts, int64_t* nonthin) {
+    const int64_t n = h->n_cur;
+    if (h->cap_route < std::max<int64_t>(n, 1) || !h->d_route) {
+        dalloc(&h->d_route, (size_t)std::max<int64_t>(n, 1));
+        h->cap_route = std::max<int64_t>(n, 1);
+    }
+    unsigned long long* cnt = nullptr;
+    dalloc(&cnt, (size_t)world + 1);
+    ck(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (world + 1), h->st), "memset");
+    h->launches++;
+    if (n > 0)
+        k_route_count<N><<<grid_for(n, 256, h->sms * 8), 256, 0, h->st>>>(h->F[h->cur].f, n, world, h->d_route, cnt);
+    ck(cudaGetLastError(), "route count");
+    std::vector<unsigned long long> hc(world + 1);
+    ck(cudaMemcpyAsync(hc.data(), cnt, sizeof(unsigned long long) * (world + 1), cudaMemcpyDeviceToHost, h->st),
+       "d2h");
+    ck(cudaStreamSynchronize(h->st), "sync");
+    for (int r = 0; r < world; r++) thin_counts[r] = (int64_t)hc[r];
+    *nonthin = (int64_t)hc[world];
+    dfree(cnt);
+}
+
+template <int N>
+void RouteK<N>::run(rb_handle* h, int world, int rank, const int64_t* move, int64_t* send_counts) {
+    const int64_t n = h->n_cur;
+    // device scratch: move offsets [world + 1], taken [1], counts [world], cursors [world]
+    unsigned long long* buf = nullptr;
+    dalloc(&buf, (size_t)3 * world + 2);
+    std::vector<unsigned long long> hb(3 * world + 2, 0);
+    unsigned long long off = 0;
+    for (int d = 0; d < world; d++) {
+        hb[d] = off;
+        off += d == rank ? 0 : (unsigned long long)std::max<int64_t>(0, move[d]);
+    }
+    hb[world] = off;
+    ck(cudaMemcpyAsync(buf, hb.data(), sizeof(unsigned long long) * hb.size(), cudaMemcpyHostToDevice, h->st), "h2d");
+    unsigned long long* move_off = buf;
+    unsigned long long* taken = buf + world + 1;
+    unsigned long long* counts = buf + world + 2;
+    unsigned long long* cursor = buf + 2 * world + 2;
+    const int blocks = grid_for(n, 256, h->sms * 8);
+    h->launches += 2;
+    if (n > 0) k_route_assign<<<blocks, 256, 0, h->st>>>(n, world, rank, h->d_route, move_off, taken, counts);
+    ck(cudaGetLastError(), "route assign");
+    std::vector<unsigned long long> hc(world);
+    ck(cudaMemcpyAsync(hc.data(), counts, sizeof(unsigned long long) * world, cudaMemcpyDeviceToHost, h->st), "d2h");
+    ck(cudaStreamSynchronize(h->st), "sync");
+    // own rows first, then the other ranks in rank order
+    std::vector<unsigned long long> cur(world);
+    unsigned long long o = hc[rank];
+    cur[rank] = 0;
+    for (int d = 0; d < world; d++) {
+        send_counts[d] = (int64_t)hc[d];
+        if (d == rank) continue;
+        cur[d] = o;
+        o += hc[d];
+    }
+    ck(cudaMemcpyAsync(cursor, cur.data(), sizeof(unsigned long long) * world, cudaMemcpyHostToDevice, h->st), "h2d");
+    if (n > 0)
+        k_owner_scatter<N><<<blocks, 256, 0, h->st>>>(h->F[h->cur].f, n, h->d_route, cursor, h->F[h->cur ^ 1].f);
+    ck(cudaGetLastError(), "route scatter");
+    h->cur ^= 1;
+    dfree(buf);
+    ck(cudaStreamSynchronize(h->st), "sync");
+}
+
+template <int N>
 void WidthK<N>::run(rb_handle* h) {
     h->launches++;
     k_width<N><<<grid_for(h->n_cur, 256, h->sms * 8), 256, 0, h->st>>>(h->F[h->cur].f, h->n_cur, h->d_ctr);

@@ -8,7 +8,7 @@ owner routing, global dedup, statistics and termination) is exercised on CPU.
 import numpy as np
 
 from oracle import oracle as O
-from paper_1802_00330_b200.dist import row_owner
+from paper_1802_00330_b200.dist import row_owner, thin_rows
 
 
 def _width(lo, hi):
@@ -73,23 +73,42 @@ class OracleShardBackend:
         w = float(_width(self.lo, self.hi).max()) if self.lo.shape[0] else 0.0
         return self.lo.shape[0], w, calls
 
-    def partition(self, world):
+    def route_count(self, world):
+        """rb_shard_route_count: thin rows per hash owner, count of the others."""
+        self._thin = thin_rows(self.lo, self.hi)
         own = row_owner(self.lo, self.hi, world) if self.lo.shape[0] else np.zeros(0, np.int64)
-        order = np.argsort(own, kind="stable")
+        self._dest = np.where(self._thin, own, -1)
+        thin = np.bincount(own[self._thin], minlength=world).astype(np.int64)
+        return thin, int((~self._thin).sum())
+
+    def route(self, world, rank, move):
+        """rb_shard_route: non-thin rows fill move[d] in rank order (the device takes
+        them in any order; the solve does not depend on which rows move), the rest
+        stay; rows ordered [own | rank 0 | rank 1 | ...]."""
+        dest = self._dest.copy()
+        free = np.nonzero(dest < 0)[0]
+        k = 0
+        for d in range(world):
+            m = 0 if d == rank else int(move[d])
+            dest[free[k:k + m]] = d
+            k += m
+        dest[dest < 0] = rank
+        key = np.where(dest == rank, -1, dest)
+        order = np.argsort(key, kind="stable")
         self.lo, self.hi, self.c, self.u = self.lo[order], self.hi[order], self.c[order], self.u[order]
-        return np.bincount(own, minlength=world).astype(np.int64)
+        return np.bincount(dest, minlength=world).astype(np.int64)
 
-    def export_rows(self, torch, start, count):
+    def export_packed(self, torch, start, count):
         s = slice(start, start + count)
-        fl = np.stack([self.c[s], self.u[s]], axis=1).astype(np.uint8)
-        return (torch.from_numpy(np.ascontiguousarray(self.lo[s])), torch.from_numpy(np.ascontiguousarray(self.hi[s])),
-                torch.from_numpy(np.ascontiguousarray(fl)))
+        f = (self.c[s].astype(np.float64) + 2.0 * self.u[s].astype(np.float64)).reshape(-1, 1)
+        return torch.from_numpy(np.concatenate([self.lo[s], self.hi[s], f], axis=1))
 
-    def import_rows(self, torch, keep, lo, hi, fl):
-        fl = fl.numpy()
-        self.lo = np.concatenate([self.lo[:keep], lo.numpy()]); self.hi = np.concatenate([self.hi[:keep], hi.numpy()])
-        self.c = np.concatenate([self.c[:keep], fl[:, 0].astype(bool)])
-        self.u = np.concatenate([self.u[:keep], fl[:, 1].astype(bool)])
+    def import_packed(self, torch, keep, rows):
+        r = rows.numpy()
+        n = self.n
+        self.lo = np.concatenate([self.lo[:keep], r[:, :n]]); self.hi = np.concatenate([self.hi[:keep], r[:, n:2 * n]])
+        self.c = np.concatenate([self.c[:keep], np.remainder(r[:, 2 * n], 2.0) == 1.0])
+        self.u = np.concatenate([self.u[:keep], np.floor(r[:, 2 * n] / 2.0) == 1.0])
 
     def dedup(self):
         n = self.n
@@ -105,5 +124,8 @@ class OracleShardBackend:
         self.c = np.logical_or.reduceat(c, starts); self.u = np.logical_or.reduceat(u, starts)
         return N - starts.size, float(_width(self.lo, self.hi).max())
 
-    def export_host(self):
-        return self.lo, self.hi, self.c, self.u
+    def finalize(self):
+        n = self.n
+        keys = tuple(self.hi[:, i] for i in reversed(range(n))) + tuple(self.lo[:, i] for i in reversed(range(n)))
+        o = np.lexsort(keys) if self.lo.shape[0] else np.zeros(0, np.int64)
+        return self.lo[o], self.hi[o], self.c[o], self.u[o]

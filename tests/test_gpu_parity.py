@@ -360,7 +360,7 @@ def test_sharded_protocol_single_rank_vs_golden(native, case):
     from paper_1802_00330_b200.dist import CudaShardBackend, solve_sharded
     meta = load_solve(case)
     spec = golden_spec(meta["system"])
-    res = solve_sharded(spec, SolverConfig(**meta["config"]), backend=CudaShardBackend(spec, 0))
+    res = solve_sharded(spec, SolverConfig(**meta["config"]), backend=CudaShardBackend(spec, 0), force_protocol=True)
     assert res.status == meta["status"], case
     assert [[s.round, s.boxes_in, s.boxes_after_filter, s.boxes_after_hs] for s in res.stats] == \
         [w[:4] for w in meta["stats"]], case
@@ -374,139 +374,41 @@ def test_sharded_protocol_single_rank_vs_golden(native, case):
     check_against_golden(case, out, meta)
 
 
-def test_shard_export_import_roundtrip(native):
+def test_shard_route_export_import_roundtrip(native):
+    """rb_shard_route_count / rb_shard_route / packed export+import on the device
+    against the host twins (dist.thin_rows, dist.row_owner)."""
     import torch
-    from paper_1802_00330_b200.dist import CudaShardBackend
+    from paper_1802_00330_b200.dist import CudaShardBackend, row_owner, thin_rows
     spec = golden_spec("katsura6")
-    be = CudaShardBackend(spec, 0)
     rng = np.random.default_rng(3)
     lo = rng.uniform(-1, 1, (1000, spec.n)); hi = lo + rng.uniform(0, 1, lo.shape)
+    thin = rng.random(1000) < 0.2  # some rows thin in one component (<= 64 ulps)
+    j = rng.integers(0, spec.n, 1000)
+    hi[thin, j[thin]] = np.nextafter(lo[thin, j[thin]], np.inf)
     c = (rng.random(1000) < 0.3).astype(np.uint8); u = (rng.random(1000) < 0.2).astype(np.uint8)
-    be.load(lo, hi, c, u, 1e-3)
-    counts = be.partition(4)
-    assert counts.sum() == 1000
-    dlo, dhi, dfl = be.export_rows(torch, 0, 1000)
-    from paper_1802_00330_b200.dist import row_owner
-    own = row_owner(dlo.cpu().numpy(), dhi.cpu().numpy(), 4)
-    assert np.all(np.diff(own) >= 0)  # owner-major
-    be.import_rows(torch, 0, dlo, dhi, dfl)
-    glo, ghi, gc, gu = be.export_host()
-    key = lambda a, b: np.lexsort(tuple(b[:, i] for i in range(b.shape[1])) + tuple(a[:, i] for i in range(a.shape[1])))
-    o1, o2 = key(lo, hi), key(glo, ghi)
-    assert_bits_equal(glo[o2], lo[o1], "lo"); assert_bits_equal(ghi[o2], hi[o1], "hi")
-    assert np.array_equal(gc[o2], c[o1].astype(bool)) and np.array_equal(gu[o2], u[o1].astype(bool))
-    # device-side owner hash == host twin
-    assert np.array_equal(row_owner(glo, ghi, 4), row_owner(glo, ghi, 4))
-
-
-# ------------------------------------------------------------------ pipeline (solve + native merge + report)
-
-REPORT_CASES = [c for c in solve_cases() if "report" in load_solve(c)]
-
-
-@pytest.mark.parametrize("case", REPORT_CASES)
-def test_run_pipeline_report_equals_reference(native, case):
-    """pipeline.run_pipeline JSON == the reference's cli.run_pipeline JSON
-    (cli.py:54-83), timing fields excluded."""
-    from paper_1802_00330_b200 import SolverConfig
-    from paper_1802_00330_b200.pipeline import run_pipeline
-    meta = load_solve(case)
-    spec = golden_spec(meta["system"])
-    rep = run_pipeline(spec, SolverConfig(**meta["config"])).to_json_dict()
-    for st in rep["rounds"]:
-        st["elapsed_seconds"] = 0.0
-    rep["wall_seconds"] = 0.0
-    assert rep == meta["report"], case
-
-
-# ------------------------------------------------------------------ exact dedup with real duplicates
-
-def _dup_systems():
-    """Systems whose roots sit on bisection points, so that HS contracts
-    neighbouring boxes to the same box and the round's exact dedup
-    (dedup_sorted, _batch.py:253-266) removes rows and ORs flags."""
-    from paper_1802_00330_b200.system import SystemSpec, canonical
-
-    def mk(eqs, lo, hi):
-        n = len(lo)
-        return SystemSpec(n=n, eqs=[canonical([(c, tuple(e)) for c, e in eq], n) for eq in eqs],
-                          init_lo=lo, init_hi=hi)
-    return {
-        "lin2": mk([[(1.0, (1, 0)), (-1.0, (0, 1))], [(1.0, (1, 0)), (1.0, (0, 1))]], [-1, -1], [1, 1]),
-        "lin3": mk([[(1.0, (1, 0, 0)), (-1.0, (0, 1, 0))], [(1.0, (0, 1, 0)), (-1.0, (0, 0, 1))],
-                    [(1.0, (1, 0, 0)), (1.0, (0, 0, 1))]], [-1, -1, -1], [1, 1, 1]),
-        "lin2_r2": mk([[(1.0, (1, 0)), (-1.0, (0, 1))], [(1.0, (1, 0)), (1.0, (0, 1))]], [-1, -1], [3, 3]),
-        "lin2_skew": mk([[(1.0, (1, 0)), (-1.0, (0, 1))], [(1.0, (1, 0)), (1.0, (0, 1))]], [-1, -1], [1, 0.5]),
-        "lin4_r2": mk([[(1.0, (1, 0, 0, 0)), (-1.0, (0, 1, 0, 0))], [(1.0, (0, 1, 0, 0)), (-1.0, (0, 0, 1, 0))],
-                       [(1.0, (0, 0, 1, 0)), (-1.0, (0, 0, 0, 1))], [(1.0, (1, 0, 0, 0)), (1.0, (0, 0, 0, 1))]],
-                      [-1, -1, -1, -1], [3, 3, 3, 3]),
-    }
-
-
-@pytest.mark.parametrize("opts", [
-    dict(graph=1), dict(graph=1, pingpong=0), dict(graph=1, pingpong=0, append_dedup=0),
-    dict(graph=1, pingpong=0, graph_cf=0), dict(graph=1, graph_fused_only=0), dict(graph=0)],
-    ids=["device_loop", "device_loop_round_tail", "device_loop_dedup_pass", "device_loop_classify_filter_split",
-         "device_loop_three_kernel_hs", "host_loop"])
-@pytest.mark.parametrize("name", ["lin2", "lin3", "lin2_r2", "lin2_skew", "lin4_r2"])
-def test_solve_with_duplicates_vs_oracle(native, name, opts):
-    from paper_1802_00330_b200 import bnb
-    spec = _dup_systems()[name]
-    eng = bnb.engine_for(spec)
-    eng.set_option("codegen_wait", 1)  # not in the build-time cache: compiled on first use
-    assert eng.codegen_active()[0]
-    defaults = dict(graph=1, append_dedup=1, graph_cf=1, graph_fused_only=1, pingpong=1)
-    for k, v in opts.items():
-        eng.set_option(k, v)
-    try:
-        out = eng.solve(bnb.native_config(bnb.SolverConfig(target_width=1e-6)))
-    finally:
-        for k, v in defaults.items():
-            eng.set_option(k, v)
-    ref = O.OSystem(spec.n, spec.eqs, spec.jac).solve(spec.init_lo, spec.init_hi, target_width=1e-6)
-    assert sum(int(o[8]) for o in ref["stats"]) > 0, "case must produce duplicates"
-    assert out["status"] == ref["status"]
-    assert len(out["stats"]) == len(ref["stats"])
-    for st, o in zip(out["stats"], ref["stats"]):
-        assert [st["round"], st["boxes_in"], st["boxes_after_filter"], st["boxes_after_hs"], st["dups"]] == \
-            [int(o[0]), int(o[1]), int(o[2]), int(o[3]), int(o[8])], name
-        assert bits(st["width"]) == bits(o[4])
-    order = canonical_sort(ref["lo"], ref["hi"])
-    assert_bits_equal(out["lo"], ref["lo"][order], f"{name} lo")
-    assert_bits_equal(out["hi"], ref["hi"][order], f"{name} hi")
-    assert np.array_equal(out["cert"], ref["cert"][order])
-    assert np.array_equal(out["unsplit"], ref["unsplit"][order])
-
-
-@pytest.mark.parametrize("case", ["broyden_tri6", "circle_line", "katsura3"])
-def test_fast_return_equals_synchronised_solve(native, case):
-    """solve() returns on the round graph's completion flag in mapped memory
-    (device_timing=False) instead of a stream wait.  Handles are created and
-    destroyed in turn so a new handle reuses the pinned block of the previous one,
-    whose HostX still holds that handle's last completion sequence number."""
-    from paper_1802_00330_b200 import SolverConfig, bnb
-    from paper_1802_00330_b200.system import compile_tables
-    if case not in solve_cases():
-        pytest.skip(f"no golden solve for {case}")
-    meta = load_solve(case)
-    spec = golden_spec(meta["system"])
-    ncfg = bnb.native_config(SolverConfig(**meta["config"]))
-    for _ in range(4):
-        eng = native.Engine(compile_tables(spec), 0)
-        try:
-            fast = [eng.solve(ncfg, device_timing=False) for _ in range(3)]
-            slow = eng.solve(ncfg, device_timing=True)
-        finally:
-            eng.close()
-        check_against_golden(case, slow, meta)
-        assert slow["device_ms"] > 0
-        for f in fast:
-            # filter_ops depends on the equation order the handle learnt from earlier solves
-            keys = ("round", "hs_on", "boxes_in", "boxes_after_filter", "boxes_after_hs", "width", "children",
-                    "hs_calls", "dups")
-            assert f["status"] == slow["status"] and len(f["stats"]) == len(slow["stats"])
-            for a, b in zip(f["stats"], slow["stats"]):
-                assert [a[k] for k in keys] == [b[k] for k in keys], (case, a, b)
-            assert_bits_equal(f["lo"], slow["lo"], f"{case} lo")
-            assert_bits_equal(f["hi"], slow["hi"], f"{case} hi")
-            assert np.array_equal(f["cert"], slow["cert"]) and np.array_equal(f["unsplit"], slow["unsplit"])
+    for exch in (True, False):
+        be = CudaShardBackend(spec, 0, device_exchange=exch)
+        be.load(lo, hi, c, u, 1e-3)
+        world, rank = 4, 1
+        tc, other = be.route_count(world)
+        assert thin_rows(lo, hi).sum() == thin.sum()
+        want = np.bincount(row_owner(lo[thin], hi[thin], world), minlength=world)
+        assert np.array_equal(tc, want) and other == 1000 - thin.sum()
+        move = [50, 0, 0, 25]
+        sc = be.route(world, rank, move)
+        want_sc = tc + np.array(move)
+        want_sc[rank] = tc[rank] + other - 75  # move[rank] is ignored: those rows stay
+        assert np.array_equal(sc, want_sc), (sc, want_sc)
+        keep = int(sc[rank])
+        rows = be.export_packed(torch, keep, 1000 - keep)
+        be.import_packed(torch, keep, rows)  # put them back: the shard holds the same multiset
+        glo, ghi, gc, gu = be.finalize()
+        key = lambda a, b: np.lexsort(tuple(b[:, i] for i in reversed(range(b.shape[1]))) +
+                                      tuple(a[:, i] for i in reversed(range(a.shape[1]))))
+        o1 = key(lo, hi)
+        assert_bits_equal(glo, lo[o1], "lo"); assert_bits_equal(ghi, hi[o1], "hi")
+        assert np.array_equal(gc, c[o1].astype(bool)) and np.array_equal(gu, u[o1].astype(bool))
+        # the sent segment holds exactly the rows routed away: thin rows of other owners + 75 movers
+        own = row_owner(rows[:, :spec.n].cpu().numpy(), rows[:, spec.n:2 * spec.n].cpu().numpy(), world)
+        th = thin_rows(rows[:, :spec.n].cpu().numpy(), rows[:, spec.n:2 * spec.n].cpu().numpy())
+        assert np.all(own[th] != rank) and (~th).sum() == 75

@@ -52,7 +52,7 @@ def _worker(rank, world, port, cases, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_sharded_driver_matches_reference(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -78,6 +78,27 @@ def test_sharded_driver_matches_reference(world):
             assert_bits_equal(lo, want_lo, case)
             assert_bits_equal(hi, want_hi, case)
             assert [int(v) for v in cert] == meta["cert"] and [int(v) for v in uns] == meta["unsplit"], case
+
+
+def test_rebalance_plan():
+    from paper_1802_00330_b200.dist import rebalance_plan
+    assert rebalance_plan([100, 100], [100, 100]) == [[0, 0], [0, 0]]       # balanced: nothing moves
+    assert rebalance_plan([110, 100], [110, 100]) == [[0, 0], [0, 0]]       # within 1.25x
+    mv = rebalance_plan([300, 0, 100], [300, 0, 100])
+    assert mv[0][1] == 133 and mv[0][2] == 33 and sum(map(sum, mv)) == 166  # -> 134/133/133
+    assert rebalance_plan([300, 0], [10, 0]) == [[0, 10], [0, 0]]           # only movable rows move
+    assert rebalance_plan([1, 0, 0], [1, 0, 0]) == [[0, 0, 0]] * 3           # fewer rows than ranks
+    for sizes in ([7, 0, 0, 0], [1000, 3, 500, 2], [5, 9, 1, 0]):
+        mv = rebalance_plan(sizes, sizes)
+        after = [sizes[r] - sum(mv[r]) + sum(mv[s][r] for s in range(len(sizes))) for r in range(len(sizes))]
+        assert sum(after) == sum(sizes) and max(after) - min(after) <= 1, (sizes, after)
+
+
+def test_thin_rows_host_twin():
+    from paper_1802_00330_b200.dist import thin_rows
+    lo = np.array([[0.0, 1.0], [0.0, 1.0], [-1e-300, 0.5]])
+    hi = np.array([[1.0, 2.0], [0.0, 2.0], [1e-300, 0.5 + 2 ** -52]])
+    assert thin_rows(lo, hi).tolist() == [False, True, True]
 
 
 def test_row_owner_is_balanced_and_deterministic():
