@@ -38,6 +38,7 @@ struct Compiled {
     std::string name_filter;
     std::string name_hs_fused;
     std::string name_hs_eval;
+    std::string name_hs_tile;
 };
 
 // CUDA source of the specialised translation unit
@@ -55,6 +56,7 @@ struct Loaded {
     cudaKernel_t filter = nullptr;  // k_filter<N, GenEval>
     cudaKernel_t hs_fused = nullptr;  // k_hs_fused<N, GenEval>
     cudaKernel_t hs_eval = nullptr;   // k_hs_eval<N, GenEval>
+    cudaKernel_t hs_tile = nullptr;   // k_hs_tile<N, GenEval>
 };
 
 // load the compiled kernels into the current device's context (process-wide cache)

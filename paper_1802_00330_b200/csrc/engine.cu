@@ -106,8 +106,13 @@ static void scratch_reserve(rb_handle* h, int64_t want) {
     h->W.B = B;
 }
 
-// all batches of the HS pipeline over at most `bound` survivors
+// all batches of the HS pipeline over at most `bound` survivors: the tiled kernel
+// (one launch, no scratch) when it applies, else eval/lin/sweep per scratch batch
 static void launch_hs_three(rb_handle* h, int64_t bound, int64_t n_in, const HsParams& prm, int64_t* tags) {
+    if (h->hs_tile) {
+        dispatch_n<HsTileK>(h->n, h, n_in, prm, tags, bound);
+        return;
+    }
     scratch_reserve(h, std::max<int64_t>(bound, 1));
     const int64_t B = h->W.B;
     for (int64_t b0 = 0; b0 == 0 || b0 < bound; b0 += B)
@@ -409,9 +414,9 @@ struct RoundOut {
 
 // both frontier buffers share one capacity (the dedup compaction may target
 // either); the current one keeps its rows when grown
-static void fronts_reserve(rb_handle* h, int64_t need) {
+static void fronts_reserve(rb_handle* h, int64_t need, int64_t keep_next = 0) {
     front_reserve(h, h->F[h->cur], need, h->n_cur);
-    front_reserve(h, h->F[h->cur ^ 1], h->F[h->cur].f.cap, 0);
+    front_reserve(h, h->F[h->cur ^ 1], h->F[h->cur].f.cap, keep_next);
     if (h->F[h->cur ^ 1].f.cap != h->F[h->cur].f.cap) front_reserve(h, h->F[h->cur], h->F[h->cur ^ 1].f.cap, h->n_cur);
     const int64_t cap = h->F[h->cur].f.cap;
     if (h->cap_dead < cap || !h->d_dead) {
@@ -629,10 +634,109 @@ struct NvtxRange {  // profiler-visible round ranges (ncu --nvtx --nvtx-include 
     ~NvtxRange() { nvtxRangePop(); }
 };
 
+// Largest survivor buffer a round may use (a quarter of the engine's memory budget);
+// a round with more survivors streams its parents in chunks (run_round_streamed).
+static int64_t s_cap_limit(rb_handle* h) {
+    return std::max<int64_t>(65536, (int64_t)(h->mem_budget / 4 / (16 * (size_t)h->n)));
+}
+
+// One round with its parents processed in chunks (bnb.py:271-313 chunks them by
+// batch_size for its thread pool): the chunk's 2^n children per parent fit the survivor
+// buffer S, and each chunk's survivors are contracted (or passed through) into F_next
+// before the next chunk is filtered, so a round needs S for one chunk and F_next for the
+// next frontier -- bounded by max_boxes -- instead of S for every survivor of the round.
+// The HS trigger (bnb.py:289-296) depends on the widest survivor of the WHOLE round, so a
+// first pass filters every parent without storing (counts + max width only); the chunks
+// then run with the decision fixed.  Results are identical to the unchunked round: every
+// output row is a function of its parent alone and the frontier is order-free.
+static void run_round_streamed(rb_handle* h, double target, const HsParams& prm0, bool dedup, RoundOut& ro) {
+    const int n = h->n;
+    int64_t scap = h->stream_parents > 0 ? std::max<int64_t>(4096, h->stream_parents << n)
+                                         : std::max<int64_t>(h->S.cap, (int64_t)1 << n);
+    scap = std::min<int64_t>(scap, std::max<int64_t>(s_cap_limit(h), (int64_t)1 << n));
+    surv_reserve(h, scap);
+    scap = h->S.cap;
+    const int64_t chunk = h->stream_parents > 0 ? h->stream_parents : std::max<int64_t>(1, scap >> n);
+    fronts_reserve(h, h->n_cur + 2 * std::min<int64_t>(scap, h->n_cur << n) + 1);
+    parents_reserve(h, std::max<int64_t>(h->n_cur, 1));
+    // pass 1: classify (carried rows into F_next, the parents list) + a count-only filter
+    ck(cudaMemsetAsync(h->d_ctr, 0, sizeof(Counters), h->st), "ctr memset");
+    record(h, 0);
+    dispatch_n<ClassifyK>(n, h, target);
+    record(h, 1);
+    const SBuf S0 = h->S;
+    h->S.cap = 0;  // nothing stored: n_surv and child_wmax only
+    dispatch_n<FilterK>(n, h, h->n_cur, (int64_t*)nullptr);
+    h->S = S0;
+    record(h, 2);
+    sync_counters(h);
+    const Counters c1 = *h->h_ctr;
+    const int64_t npar = (int64_t)c1.n_par;
+    bool hs_on = false;  // hs_count's trigger, on the whole round's survivors
+    if (c1.n_surv > 0 && prm0.hs_possible) {
+        if (prm0.hs_enable_round >= 0 && prm0.round_no >= prm0.hs_enable_round) hs_on = true;
+        if (!std::isnan(prm0.hs_enable_width) && bits_to_double(c1.child_wmax) <= prm0.hs_enable_width) hs_on = true;
+    }
+    double classify_ms = elapsed(h, 0, 1), filter_ms = 0.0, hs_ms = 0.0;
+    // the chunks re-count survivors, filter work and exact boxes
+    {
+        Counters z = c1;
+        z.n_surv = 0;
+        z.filter_ops = 0;
+        z.exact_boxes = 0;
+        ck(cudaMemcpyAsync(h->d_ctr, &z, sizeof(Counters), cudaMemcpyHostToDevice, h->st), "ctr h2d");
+    }
+    HsParams prm = prm0;
+    prm.hs_mode = hs_on ? 1 : 2;
+    prm.count_from_ctr = 1;
+    int64_t surv_total = 0, n_next = (int64_t)c1.n_next;
+    unsigned long long filter_ops = 0, exact = 0;
+    for (int64_t p0 = 0; p0 < npar; p0 += chunk) {
+        const int64_t pc = std::min<int64_t>(chunk, npar - p0);
+        const int64_t worst = std::min<int64_t>(scap, pc << n);
+        if (n_next + 2 * worst + 1 > h->F[h->cur ^ 1].f.cap)  // F_next keeps its rows when it grows
+            fronts_reserve(h, grow_cap(n_next + 2 * worst + 1), n_next);
+        scratch_reserve(h, std::max<int64_t>(1, worst));
+        ck(cudaMemsetAsync(&h->d_ctr->n_surv, 0, sizeof(unsigned long long), h->st), "memset");
+        record(h, 1);
+        dispatch_n<FilterK>(n, h, pc, (int64_t*)nullptr, p0, pc);
+        record(h, 2);
+        launch_hs_batches(h, worst, 0, prm, nullptr);
+        record(h, 3);
+        sync_counters(h);
+        const Counters& c = *h->h_ctr;
+        if (c.n_surv > (unsigned long long)scap) throw ArgError{RB_ERR_STATE, "streamed chunk overflowed S"};
+        surv_total += (int64_t)c.n_surv;
+        n_next = (int64_t)c.n_next;
+        filter_ms += elapsed(h, 1, 2);
+        hs_ms += elapsed(h, 2, 3);
+    }
+    filter_ops = h->h_ctr->filter_ops;
+    exact = h->h_ctr->exact_boxes;
+    if (dedup) {
+        dispatch_n<DedupK>(n, h, h->F[h->cur ^ 1].f, h->F[h->cur].f);
+        sync_counters(h);
+    }
+    fill_round_out(h, ro);
+    ro.survivors = surv_total;
+    ro.filter_ops = filter_ops;
+    ro.exact = (int64_t)exact;
+    ro.hs_on = hs_on;
+    update_order(h);
+    ro.attempts = 1;
+    ro.classify_ms = classify_ms;
+    ro.filter_ms = filter_ms;
+    ro.hs_ms = hs_ms;
+}
+
 static void run_round(rb_handle* h, double target, const HsParams& prm, bool dedup, RoundOut& ro) {
     char nv[32];
     std::snprintf(nv, sizeof(nv), "rb_round_%d", prm.round_no);
     NvtxRange range(nv);
+    if (h->stream_parents > 0 && h->n_cur > 0) {  // forced (tests): every round in chunks
+        run_round_streamed(h, target, prm, dedup, ro);
+        return;
+    }
     int64_t need_s, need_f;
     plan_capacity(h, need_s, need_f);
     for (int attempt = 1;; attempt++) {
@@ -648,6 +752,11 @@ static void run_round(rb_handle* h, double target, const HsParams& prm, bool ded
         const Counters& c = *h->h_ctr;
         if (c.n_surv > (unsigned long long)h->S.cap) {
             need_s = (int64_t)(c.n_surv + c.n_surv / 4);
+            if (need_s > s_cap_limit(h)) {  // too many survivors for one buffer: stream the parents
+                run_round_streamed(h, target, prm, dedup, ro);
+                ro.attempts = attempt + 1;
+                return;
+            }
             need_f = h->n_cur + 2 * need_s + 1;
             continue;
         }
@@ -1084,6 +1193,7 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     key.push_back((uintptr_t)h->pdl);
     key.push_back((uintptr_t)h->trace);
     key.push_back((uintptr_t)h->force_exact);
+    key.push_back((uintptr_t)h->hs_tile);
     if (key != h->graph_key || !h->graph_exec) build_round_graph(h, prm, dedup, scap, key);
     DevState st{};
     st.n_cur = 1;
@@ -1222,7 +1332,7 @@ static void solve_impl(rb_handle* h, const rb_config* cfg, rb_result_info* info)
         host_init();
         status = RB_WIDTH_REACHED;
         finished = true;
-    } else if (h->use_graph && !has_max_seconds) {
+    } else if (h->use_graph && !has_max_seconds && h->stream_parents == 0) {
         finished = graph_rounds(h, cfg, target, hs_possible, &status);
     } else {
         host_init();
@@ -1469,6 +1579,7 @@ int rb_create(const rb_system* sys, int device, rb_handle** out) {
         size_t free_b = 0, total_b = 0;
         ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
         h->mem_budget = (size_t)(0.80 * (double)free_b);
+        h->mem_budget_default = h->mem_budget;
         dalloc(&h->d_ctr, 1);
         dalloc(&h->d_bar, 2);
         ck(cudaMemsetAsync(h->d_bar, 0, 2 * sizeof(unsigned), h->st), "barrier clear");
@@ -2108,6 +2219,18 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     }
     if (k == "graph") {
         h->use_graph = value != 0;
+        return RB_OK;
+    }
+    if (k == "stream_parents") {  // > 0: every host-driven round streams its parents in chunks of this size
+        h->stream_parents = std::max<int64_t>(0, value);
+        return RB_OK;
+    }
+    if (k == "mem_budget_mb") {  // engine memory budget (tests of the streamed rounds at small budgets)
+        h->mem_budget = value > 0 ? (size_t)value << 20 : h->mem_budget_default;  // 0: the default
+        return RB_OK;
+    }
+    if (k == "hs_tile") {  // large HS batches: 1 = k_hs_tile (n <= 8), 0 = eval/lin/sweep
+        h->hs_tile = value != 0 && h->n <= 8 && h->tile_tb > 0;
         return RB_OK;
     }
     if (k == "force_exact") {  // Exact policy everywhere (parity tests of interval.cuh's Exact)

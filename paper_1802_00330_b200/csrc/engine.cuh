@@ -105,6 +105,7 @@ struct rb_handle {
     int64_t cap_dead = 0;
     // capacity prediction from the previous round
     size_t mem_budget = 0;     // bytes the engine may hold
+    size_t mem_budget_default = 0;
     // sort scratch
     void* d_cub = nullptr;
     size_t cub_bytes = 0;
@@ -209,6 +210,13 @@ struct rb_handle {
     // sweep run the Exact policy (interval.cuh) on every box -- the parity tests of
     // that path; the guard constants of build_tables are kept here to restore them
     bool force_exact = false;
+    // k_hs_tile (throughput HS, n <= 8): boxes per tile (= threads per block), shared memory,
+    // blocks per SM; table-evaluator and specialised builds
+    bool hs_tile = true;
+    int64_t stream_parents = 0;  // > 0: host-driven rounds stream parents in chunks of this size (tests)
+    int tile_tb = 0, gen_tile_tb = 0;
+    size_t tile_smem = 0, gen_tile_smem = 0;
+    int tile_bps = 1, gen_tile_bps = 1;
     unsigned* d_route = nullptr;   // per-row destination of the shard routing (RouteCountK / RouteK)
     int64_t cap_route = 0;
     int guard_f_ecmin = 0, guard_j_ecmin = 0;
@@ -306,11 +314,31 @@ static void klaunch_k(rb_handle* h, cudaKernel_t k, int grid, int block, size_t 
 
 static inline bool gen_on(const rb_handle* h) { return h->use_gen && h->gen.ok; }
 
+// k_hs_tile shape: the tile size (32/64/128 boxes, one thread each) with the most
+// resident warps per SM under the tile's shared memory; ties go to the larger tile
+template <typename K>
+static void choose_tile(rb_handle* h, K kernel, int n, int tab_bytes, int& tb_out, size_t& smem_out, int& bps_out) {
+    tb_out = 0;
+    int best = 0;
+    for (int tb : {128, 64, 32}) {
+        const size_t sm = tile_smem_bytes(n, tb, tab_bytes);
+        if ((int)sm > h->smem_optin - 256) continue;
+        int nb = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, tb, sm), "occ tile");
+        if (nb * tb > best) {
+            best = nb * tb;
+            tb_out = tb;
+            smem_out = sm;
+            bps_out = std::max(1, nb);
+        }
+    }
+}
+
 // launch attributes of the specialised kernels (same shared-memory layouts as the
 // table kernels, whose sizes SetupK computed)
 static inline void gen_configure(rb_handle* h) {
     if (!h->gen.ok) return;
-    for (cudaKernel_t k : {h->gen.cf, h->gen.filter, h->gen.hs_fused, h->gen.hs_eval}) {
+    for (cudaKernel_t k : {h->gen.cf, h->gen.filter, h->gen.hs_fused, h->gen.hs_eval, h->gen.hs_tile}) {
         cudaFuncAttributes fa;
         ck(cudaFuncGetAttributes(&fa, (const void*)k), "gen attrs");
         ck(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -329,6 +357,7 @@ static inline void gen_configure(rb_handle* h) {
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)h->gen.hs_fused, T, h->fused_smem), "occ");
         h->gen_hsf_bps = std::max(1, nb);
     }
+    choose_tile(h, (const void*)h->gen.hs_tile, h->n, 0, h->gen_tile_tb, h->gen_tile_smem, h->gen_tile_bps);
     h->use_ftab = false;  // the specialised direct filter beats the tabulated one (eco8 47.9 vs 54.6 ms)
 }
 
@@ -351,13 +380,19 @@ struct AllParentsK {
 
 template <int N>
 struct FilterK {
-    static void run(rb_handle* h, int64_t max_parents, int64_t* tags);
+    static void run(rb_handle* h, int64_t max_parents, int64_t* tags, int64_t p0 = 0, int64_t pcount = -1);
 };
 
 // K2a + K2b + K2c over rows [b0, b0 + W.B) of S (n_in read on the device when prm.count_from_ctr)
 template <int N>
 struct HsK {
     static void run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* tags, int64_t batch_bound);
+};
+
+// tiled K2 (k_hs_tile) over all n_in rows of S (n_in read on the device when prm.count_from_ctr)
+template <int N>
+struct HsTileK {
+    static void run(rb_handle* h, int64_t n_in, HsParams prm, int64_t* tags, int64_t bound);
 };
 
 // fused K2 over all n_in rows of S (n_in read on the device when prm.count_from_ctr); `bound`
@@ -439,6 +474,6 @@ struct RouteK {
 
 // every launcher template, for explicit instantiation (kinst.cu) and extern declarations (engine.cu)
 #define RB_LAUNCHERS(X, K)                                                                              \
-    X SetupK<K>; X ClassifyK<K>; X ClassifyFilterK<K>; X AllParentsK<K>; X FilterK<K>; X HsK<K>; X HsFusedK<K>; X KrawczykK<K>; \
+    X SetupK<K>; X ClassifyK<K>; X ClassifyFilterK<K>; X AllParentsK<K>; X FilterK<K>; X HsK<K>; X HsTileK<K>; X HsFusedK<K>; X KrawczykK<K>; \
     X SmallRoundsK<K>; X DedupInsertK<K>; X TailK<K>; X SettleK<K>; X DedupK<K>; X PartitionK<K>; X WidthK<K>; \
     X RouteCountK<K>; X RouteK<K>;

@@ -724,7 +724,8 @@ __host__ __device__ inline int filter_off_xs(const TabMeta& m) { return filter_o
 template <int N, class EV = TabEval>
 __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                 const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
-                                                int64_t* tags, const int* __restrict__ eq_order) {
+                                                int64_t* tags, const int* __restrict__ eq_order,
+                                                int64_t pcount = -1) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_order[16];
     __shared__ unsigned s_eval[16], s_rej[16];
@@ -743,7 +744,9 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
     }
     const int stride = blockDim.x;
     double2* xs2 = reinterpret_cast<double2*>(smem + filter_off_xs(meta)) + threadIdx.x;
-    const unsigned long long total = ctr->n_par << N;  // read while the table copies are in flight
+    // parents[0, pcount) (a chunk of a streamed round), else all ctr->n_par of the round;
+    // read while the table copies are in flight
+    const unsigned long long total = (pcount >= 0 ? (unsigned long long)pcount : ctr->n_par) << N;
     cp_async_wait();
     __syncthreads();
     const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
@@ -807,9 +810,9 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
 template <int N, class EV = TabEval>
 __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                 const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
-                                                int64_t* tags, const int* __restrict__ eq_order) {
+                                                int64_t* tags, const int* __restrict__ eq_order, int64_t pcount) {
     pdl_launch();
-    k_filter_body<N, EV>(meta, gtab, cur, parents, ctr, S, tags, eq_order);  // waits after the table copies
+    k_filter_body<N, EV>(meta, gtab, cur, parents, ctr, S, tags, eq_order, pcount);  // waits after the table copies
 }
 
 // K3 + K1 in one launch for the device round loop: thread per (frontier row, child).
@@ -1049,7 +1052,7 @@ static __device__ __noinline__ ival term_value_exact(const STab& t, int q, int c
 template <int N>
 __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                     const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
-                                                    int64_t* tags, const int* __restrict__ eq_order) {
+                                                    int64_t* tags, const int* __restrict__ eq_order, int64_t pcount) {
     pdl_enter();
     using Sh = FtabShape<N>;
     __shared__ int s_order[16];
@@ -1073,7 +1076,7 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
     cp_async_wait();
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const unsigned long long n_par = ctr->n_par;
+    const unsigned long long n_par = pcount >= 0 ? (unsigned long long)pcount : ctr->n_par;
     const unsigned long long units =
         N >= 8 ? (n_par << Sh::CHLOG) : ((n_par + Sh::PPB - 1) >> Sh::LOGPPB);
     unsigned long long ops_acc = 0, exact_acc = 0;
@@ -1443,10 +1446,13 @@ __device__ __forceinline__ ival pmul_sign(double a, ival y) {
 }
 // Measured (bench other_configs, full solves): sign-bit products cut banded12's HS time
 // 6.29 -> 5.84 ms (N = 12, 32 lanes per box) but cost katsura6 (N = 7) 3%.
+#ifndef RB_PMUL_SIGN_MIN_N
+#define RB_PMUL_SIGN_MIN_N 9  // sign-bit point products from this n up (A/B: tools/hs_bench.py)
+#endif
 template <class A, int N>
 __device__ __forceinline__ ival pmul(double a, ival y) {
     if constexpr (A::exact) return A::mul_point(a, y);
-    else if constexpr (N > 8) return pmul_sign(a, y);
+    else if constexpr (N >= RB_PMUL_SIGN_MIN_N) return pmul_sign(a, y);
     else return pmul_minmax(a, y);
 }
 
@@ -1535,7 +1541,10 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
     if (pr) pr[1] = clock64() + (unsigned long long)scale * 0ull;
     bool singular = scale == 0.0;
     const double threshold = __dmul_rn(1e-12, scale);
-    if constexpr (N <= 8) {
+#ifndef RB_GJ_SHFL_MAX_N
+#define RB_GJ_SHFL_MAX_N 8  // pivot column broadcast by shuffles up to this n, through shared memory above
+#endif
+    if constexpr (N <= RB_GJ_SHFL_MAX_N) {
         // column k broadcast by shuffles; every lane repeats the pivot search on it
 #pragma unroll
         for (int k = 0; k < N; k++) {
@@ -1653,7 +1662,10 @@ __device__ __forceinline__ bool lin_group(const LinSink& K, double* Am, double* 
 
 // K2b: G lanes per box; boxes assigned warp-uniformly.
 template <int N>
-__global__ void __launch_bounds__(128) k_hs_lin(SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
+#ifndef RB_LIN_MINB
+#define RB_LIN_MINB 1  // __launch_bounds__ min blocks per SM of k_hs_lin (register cap)
+#endif
+__global__ void __launch_bounds__(128, RB_LIN_MINB) k_hs_lin(SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
                                                 Counters* ctr) {
     pdl_enter();
     using L = LinLayout<N>;
@@ -1945,6 +1957,282 @@ __global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t 
     }
 }
 
+
+// ------------------------------------------------------------------ K2 tiled (throughput HS)
+//
+// k_hs_tile: the whole HS pass over tiles of TB boxes per block (TB = blockDim.x),
+// every operand of a tile in shared memory -- the throughput replacement of
+// k_hs_eval -> k_hs_lin -> k_hs_sweep, whose J / M / g round trip through an HBM
+// scratch (uncoalesced column reads in k_hs_lin) cost ~4.5 KB of DRAM traffic per
+// box against ~0.3 KB algorithmic (ncu, katsura6 round 5).  Per tile:
+//   load   thread per box: X -> tile (lo, hi, mid), coalesced SoA reads of S
+//   eval   thread per box: J(X) and F(x) into the tile, layout [q][box] with a padded
+//          stride (conflict-free stores; the lin groups' column reads hit distinct banks)
+//   lin    G lanes per box (lin_group: Gauss-Jordan, M = A J, g = A F(x) in place)
+//   sweep  thread per box on the tile (the sweep of k_hs_sweep); outputs appended to F_next
+// The arithmetic is operation-for-operation that of the three-kernel pipeline.  DRAM
+// traffic per box: 16n B read, <= 2 (16n + 2) B written.
+template <int N>
+struct TileLayout {
+    static constexpr int G = LinLayout<N>::G;
+    static constexpr int BPW = 32 / G;
+    static constexpr int rows = 2 * N * N + 5 * N;   // J/M lo, hi; F/g lo, hi; X lo, hi, mid
+    static constexpr int oJl = 0, oJh = N * N, oFl = 2 * N * N, oFh = 2 * N * N + N;
+    static constexpr int oXl = 2 * N * N + 2 * N, oXh = oXl + N, oXm = oXh + N;
+    static constexpr int per_group = N * N + N + 1;  // A, pivot column
+};
+// bytes of shared memory of a TB-box tile (after the system tables of the table evaluator)
+__host__ __device__ inline size_t tile_smem_bytes(int n, int tb, int tab_bytes) {
+    const int G = n <= 2 ? 4 : (n <= 4 ? 8 : (n <= 8 ? 16 : 32));
+    return (size_t)align16(tab_bytes) + sizeof(double) * ((size_t)(2 * n * n + 5 * n) * (tb + 1) +
+                                                          (size_t)(tb / 32) * (32 / G) * (n * n + n + 1));
+}
+
+template <int N, class EV = TabEval>
+__global__ void __launch_bounds__(128) k_hs_tile(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
+                                                 int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
+                                                 int64_t* tags) {
+    pdl_enter();
+    using L = TileLayout<N>;
+    constexpr int G = L::G;
+    constexpr int P = N * N + N;
+    extern __shared__ __align__(16) uint8_t smem[];
+    bool hs_on;
+    const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
+    if (n_in < 0 || n_in <= prm.fused_max) return;  // small counts: k_hs_fused
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hs_on = hs_on ? 1ull : 0ull;
+    if (!hs_on) {
+        hs_passthrough<N>(S, n_in, out, ctr, tags);
+        return;
+    }
+    const int TB = blockDim.x, SP = TB + 1;  // boxes per tile, padded row stride
+    STab tab{};
+    int tab_bytes = 0;
+    if constexpr (EV::tables) {
+        tab = load_stab(meta, gtab, smem, false);
+        tab_bytes = stab_bytes(meta, false);
+    }
+    double* T = reinterpret_cast<double*>(smem + align16(tab_bytes));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gi = lane / G, l = lane % G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
+    double* grp = T + (size_t)L::rows * SP + (size_t)(warp * L::BPW + gi) * L::per_group;
+    const int groups = (TB / 32) * L::BPW, my_group = warp * L::BPW + gi;
+    const int t = threadIdx.x;
+    double* cl = T + L::oXl * SP + t;  // this thread's box during load / eval / sweep: [j * SP]
+    double* ch = T + L::oXh * SP + t;
+    double* cm = T + L::oXm * SP + t;
+    __shared__ uint8_t s_sing[128];
+    unsigned long long ops_acc = 0, calls_acc = 0, exact_acc = 0;
+    for (int64_t base = (int64_t)blockIdx.x * TB; base < n_in; base += (int64_t)gridDim.x * TB) {
+        const int nb = (int)min((int64_t)TB, n_in - base);
+        const int64_t b = base + t;
+        const bool valid = t < nb;
+        __syncthreads();  // the previous tile is consumed
+        // ---- load + eval: J(X) (hansen.py:61-63), F(x) (poly.py:205-207), thread per box
+        if (valid) {
+            ExpRange rx, rm;
+            rx.init();
+            rm.init();
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                const double lo = S.lo[j * S.cap + b], hi = S.hi[j * S.cap + b];
+                const double m = mid_of(lo, hi);  // Box.midpoint, poly.py:114-115
+                cl[j * SP] = lo;
+                ch[j * SP] = hi;
+                cm[j * SP] = m;
+                rx.add(lo);
+                rx.add(hi);
+                rm.add(m);
+            }
+            const bool fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
+            const bool fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
+            double* jl = T + L::oJl * SP + t;
+            double* jh = T + L::oJh * SP + t;
+            double* fl = T + L::oFl * SP + t;
+            double* fh = T + L::oFh * SP + t;
+            if constexpr (EV::whole_box) {
+                if (fastJ) EV::template J<Fast>(cl, ch, SP, jl, jh, SP);
+                else EV::template J<Exact>(cl, ch, SP, jl, jh, SP);
+                if (fastF) EV::template F<Fast>(cm, cm, SP, fl, fh, SP);
+                else EV::template F<Exact>(cm, cm, SP, fl, fh, SP);
+            } else {
+#pragma unroll 1
+                for (int q = 0; q < P; q++) {
+                    if (q < N * N) {
+                        const ival v = fastJ ? eval_poly<Fast>(tab, N + q, cl, ch, SP)
+                                             : eval_poly_exact(tab, N + q, cl, ch, SP);
+                        jl[q * SP] = v.lo;
+                        jh[q * SP] = v.hi;
+                    } else {
+                        const int i = q - N * N;
+                        const ival v = fastF ? eval_poly<Fast>(tab, i, cm, cm, SP)
+                                             : eval_poly_exact(tab, i, cm, cm, SP);
+                        fl[i * SP] = v.lo;
+                        fh[i * SP] = v.hi;
+                    }
+                }
+            }
+            exact_acc += !(fastJ && fastF);
+        }
+        __syncthreads();
+        // ---- lin: A = mid(J)^-1, M = A J, g = A F(x), G lanes per box (linalg.py:102-172)
+        for (int bb = my_group; bb - gi < nb; bb += groups) {  // warp-uniform trip count
+            if (bb < nb) {
+                const LinSink K{T + L::oJl * SP + bb, T + L::oJh * SP + bb, T + L::oFl * SP + bb,
+                                T + L::oFh * SP + bb, SP};
+                bool exact_lin;
+                const bool singular = lin_group<N, G>(K, grp, grp + N * N, l, gmask, exact_lin, prm.force_exact);
+                if (l == 0) s_sing[bb] = singular ? 1 : 0;
+                __syncwarp(gmask);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        // ---- sweep (hansen.py:91-138), thread per box; the tile's X lo/hi become the current box
+        int kind = HS_EMPTY;
+        bool cert = false;
+        int fork_i = -1;
+        ival fp0 = mk(0.0, 0.0), fp1 = mk(0.0, 0.0);
+        int rows = 0;
+        if (valid) {
+            const double* Ml = T + L::oJl * SP + t;
+            const double* Mh = T + L::oJh * SP + t;
+            if (s_sing[t]) {
+                kind = HS_SKIP;
+            } else {
+                kind = HS_ONE;
+#pragma unroll 1
+                for (int i = 0; i < N; i++) {
+                    rows = i + 1;
+                    // p = -g_i - sum_{j != i, M_ij != [0,0]} M_ij (current_j - [x_j, x_j]), left to right
+                    ival p = mk(-T[L::oFh * SP + i * SP + t], -T[L::oFl * SP + i * SP + t]);
+#pragma unroll
+                    for (int j = 0; j < N; j++) {
+                        if (j == i) continue;
+                        const ival m = mk(Ml[(i * N + j) * SP], Mh[(i * N + j) * SP]);
+                        if (m.lo == 0.0 && m.hi == 0.0) continue;
+                        const ival d = Fast::sub(mk(cl[j * SP], ch[j * SP]), mk(cm[j * SP], cm[j * SP]));
+                        p = Fast::sub(p, gmul(m, d, prm.force_exact));
+                    }
+                    const ival mii = mk(Ml[(i * N + i) * SP], Mh[(i * N + i) * SP]);
+                    const double xi = cm[i * SP];
+                    ival q0 = mk(0.0, 0.0), q1 = mk(0.0, 0.0);
+                    const int dk = div_extended_fast(p, mii, q0, q1, prm.force_exact);
+                    if (dk == DIV_EMPTY) {
+                        kind = HS_EMPTY;
+                        break;
+                    }
+                    if (dk == DIV_WHOLE) continue;
+                    const ival cur_i = mk(cl[i * SP], ch[i * SP]);
+                    ival pieces[2];
+                    int npieces = 0;
+                    const int np = dk == DIV_SPLIT ? 2 : 1;
+#pragma unroll
+                    for (int q = 0; q < 2; q++) {
+                        if (q < np) {
+                            const ival y = Fast::add(mk(xi, xi), q == 0 ? q0 : q1);
+                            const double lo = py_max(y.lo, cur_i.lo);  // Interval.intersect
+                            const double hi = py_min(y.hi, cur_i.hi);
+                            if (!(lo > hi)) pieces[npieces++] = mk(lo, hi);
+                        }
+                    }
+                    if (npieces == 0) {
+                        kind = HS_EMPTY;
+                        break;
+                    }
+                    ival nc = pieces[0];
+                    if (npieces == 2) {
+                        nc = mk(py_min(pieces[0].lo, pieces[1].lo), py_max(pieces[0].hi, pieces[1].hi));  // hull
+                        if (fork_i < 0) {
+                            fork_i = i;
+                            fp0 = pieces[0];
+                            fp1 = pieces[1];
+                        }
+                    }
+                    cl[i * SP] = nc.lo;
+                    ch[i * SP] = nc.hi;
+                }
+                if (kind == HS_ONE && fork_i >= 0) kind = HS_TWO;
+                if (kind == HS_ONE) {  // certified iff strictly inside the input (hansen.py:129-132)
+                    cert = true;
+#pragma unroll
+                    for (int j = 0; j < N; j++)
+                        cert = cert && (S.lo[j * S.cap + b] < cl[j * SP]) && (ch[j * SP] < S.hi[j * S.cap + b]);
+                }
+            }
+            calls_acc++;
+            ops_acc += meta.ops_hs_pre + (unsigned long long)meta.ops_hs_row * rows;
+        }
+        // outputs (bnb.py:197-210)
+        int cnt = 0;
+        bool use_input = false;
+        if (valid) {
+            if (kind == HS_SKIP) {
+                cnt = 1;
+                use_input = true;
+                cert = false;
+            } else if (kind == HS_EMPTY) {
+                cnt = 0;
+            } else if (!prm.contract_output) {
+                cnt = 1;
+                use_input = true;
+            } else {
+                cnt = kind == HS_TWO ? 2 : 1;
+            }
+        }
+        const unsigned b1 = __ballot_sync(0xffffffffu, cnt == 1);
+        const unsigned b2 = __ballot_sync(0xffffffffu, cnt == 2);
+        const unsigned lt = lanemask_lt();
+        const unsigned off = __popc(b1 & lt) + 2 * __popc(b2 & lt);
+        const unsigned total = __popc(b1) + 2 * __popc(b2);
+        unsigned long long wbase = 0;
+        if (lane == 0 && total) wbase = atomicAdd(&ctr->n_next, (unsigned long long)total);
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        double wmax = 0.0;
+        for (int q = 0; q < cnt; q++) {
+            const unsigned long long slot = wbase + off + q;
+            double w = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                double lo, hi;
+                if (use_input) {
+                    lo = S.lo[j * S.cap + b];
+                    hi = S.hi[j * S.cap + b];
+                } else if (j == fork_i) {
+                    lo = q == 0 ? fp0.lo : fp1.lo;
+                    hi = q == 0 ? fp0.hi : fp1.hi;
+                } else {
+                    lo = cl[j * SP];
+                    hi = ch[j * SP];
+                }
+                const double d = __dsub_rn(hi, lo);
+                w = j == 0 ? d : (d > w ? d : w);
+                if (slot < (unsigned long long)out.cap) {
+                    out.lo[j * out.cap + slot] = canon0(lo);
+                    out.hi[j * out.cap + slot] = canon0(hi);
+                }
+            }
+            wmax = fmax(wmax, w);
+            if (slot < (unsigned long long)out.cap) {
+                out.cert[slot] = cert ? 1 : 0;
+                out.unsplit[slot] = 0;
+                if (tags) tags[slot] = 2 * b + q;
+            }
+        }
+        unsigned long long wbits = (unsigned long long)__double_as_longlong(wmax);
+        wbits = warp_max(wbits);
+        if (lane == 0 && wbits) atomicMax(&ctr->wmax, wbits);
+    }
+    ops_acc = warp_sum(ops_acc);
+    calls_acc = warp_sum(calls_acc);
+    exact_acc = warp_sum(exact_acc);
+    if (lane == 0) {
+        if (ops_acc) atomicAdd(&ctr->hs_ops, ops_acc);
+        if (calls_acc) atomicAdd(&ctr->hs_calls, calls_acc);
+        if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
+    }
+}
 
 // ------------------------------------------------------------------ K2 fused
 //

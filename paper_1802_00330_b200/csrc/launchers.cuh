@@ -26,6 +26,9 @@ void SetupK<N>::run(rb_handle* h) {
     set_max_dyn_smem(k_hs_lin<N>, h->smem_optin);
     set_max_dyn_smem(k_hs_sweep<N>, h->smem_optin);
     set_max_dyn_smem(k_hs_fused<N>, h->smem_optin);
+    set_max_dyn_smem(k_hs_tile<N>, h->smem_optin);
+    choose_tile(h, k_hs_tile<N>, N, stab_bytes(h->meta, false), h->tile_tb, h->tile_smem, h->tile_bps);
+    if (N > 8 || h->tile_tb == 0) h->hs_tile = false;  // n > 8: one box per warp, the three kernels win
     if ((int)h->fused_smem > h->smem_optin) h->hs_fused = false;
     int nb = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_filter<N>, h->filter_threads, h->filter_smem), "occ");
@@ -83,14 +86,16 @@ void AllParentsK<N>::run(rb_handle* h) {
 }
 
 template <int N>
-void FilterK<N>::run(rb_handle* h, int64_t max_parents, int64_t* tags) {
+void FilterK<N>::run(rb_handle* h, int64_t max_parents, int64_t* tags, int64_t p0, int64_t pcount) {
+    // parents [p0, p0 + pcount) of the round's list (a streamed chunk), or all of them (pcount < 0)
+    const uint32_t* par = h->parents + p0;
     if (h->meta.ftab && h->use_ftab) {
         using Sh = FtabShape<N>;
         const int64_t units = N >= 8 ? (max_parents << Sh::CHLOG) : ((max_parents + Sh::PPB - 1) >> Sh::LOGPPB);
         const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)h->sms * h->ftab_blocks_per_sm));
         h->launches++;
-        klaunch(h, k_filter_tab<N>, blocks, 256, h->ftab_smem, h->meta, h->d_tab, h->F[h->cur].f, h->parents,
-                                                             h->d_ctr, h->S, tags, h->d_order);
+        klaunch(h, k_filter_tab<N>, blocks, 256, h->ftab_smem, h->meta, h->d_tab, h->F[h->cur].f, par,
+                                                             h->d_ctr, h->S, tags, h->d_order, pcount);
         ck(cudaGetLastError(), "filter_tab launch");
         return;
     }
@@ -99,13 +104,13 @@ void FilterK<N>::run(rb_handle* h, int64_t max_parents, int64_t* tags) {
     if (gen_on(h)) {
         const int blocks = grid_for(work, h->filter_threads, h->sms * h->gen_filter_bps);
         klaunch_k(h, h->gen.filter, blocks, h->filter_threads, h->filter_smem, h->meta, (const uint8_t*)h->d_tab,
-                  h->F[h->cur].f, (const uint32_t*)h->parents, h->d_ctr, h->S, tags, (const int*)h->d_order);
+                  h->F[h->cur].f, par, h->d_ctr, h->S, tags, (const int*)h->d_order, pcount);
         ck(cudaGetLastError(), "filter launch");
         return;
     }
     const int blocks = grid_for(work, h->filter_threads, h->sms * h->filter_blocks_per_sm);
     klaunch(h, k_filter<N>, blocks, h->filter_threads, h->filter_smem, h->meta, h->d_tab, h->F[h->cur].f,
-                                                                     h->parents, h->d_ctr, h->S, tags, h->d_order);
+                                                                     par, h->d_ctr, h->S, tags, h->d_order, pcount);
     ck(cudaGetLastError(), "filter launch");
 }
 
@@ -130,6 +135,24 @@ void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* 
     klaunch(h, k_hs_sweep<N>, grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem,
         h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
     ck(cudaGetLastError(), "hs launch");
+}
+
+template <int N>
+void HsTileK<N>::run(rb_handle* h, int64_t n_in, HsParams prm, int64_t* tags, int64_t bound) {
+    prm.force_exact = h->force_exact ? 1 : 0;
+    h->launches++;
+    Front out = h->F[h->cur ^ 1].f;
+    const int64_t rows = std::max<int64_t>(1, bound);
+    if (gen_on(h) && h->gen_tile_tb > 0) {
+        const int tb = h->gen_tile_tb;
+        klaunch_k(h, h->gen.hs_tile, grid_for(rows, tb, h->sms * h->gen_tile_bps), tb, h->gen_tile_smem, h->meta,
+                  (const uint8_t*)h->d_tab, h->S, n_in, prm, out, h->d_ctr, tags);
+    } else {
+        const int tb = h->tile_tb;
+        klaunch(h, k_hs_tile<N>, grid_for(rows, tb, h->sms * h->tile_bps), tb, h->tile_smem, h->meta, h->d_tab,
+                h->S, n_in, prm, out, h->d_ctr, tags);
+    }
+    ck(cudaGetLastError(), "hs tile launch");
 }
 
 template <int N>

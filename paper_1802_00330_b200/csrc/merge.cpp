@@ -378,10 +378,81 @@ int snap_fast(const std::vector<i128>& A, const std::vector<i128>& W, const std:
     return 0;
 }
 
+// |a| * |b| with the sign of a * b
+Big mul_big(const Big& a, const Big& b) {
+    Big r;
+    if (a.n == 0 || b.n == 0) return r;
+    const int rn = a.n + b.n;
+    if (rn > LIMBS) throw std::string("integer too large");
+    for (int i = 0; i < rn; i++) r.w[i] = 0;
+    for (int i = 0; i < a.n; i++) {
+        unsigned __int128 c = 0;
+        for (int j = 0; j < b.n; j++) {
+            c += (unsigned __int128)a.w[i] * b.w[j] + r.w[i + j];
+            r.w[i + j] = (uint64_t)c;
+            c >>= 64;
+        }
+        r.w[i + b.n] = (uint64_t)c;
+    }
+    r.n = rn;
+    r.neg = a.neg != b.neg;
+    norm(r);
+    return r;
+}
+
+// ---- cell indices: 128-bit while every snapped level is at most 120, else wide keys
+// (snap_to_grid has no level limit: a box of width ~1e-300 snaps to a level near 1000)
+constexpr int KW = 18;  // 1152 bits: indices below 2^L for any level a double box can reach
+struct KeyW {
+    uint64_t w[KW];
+};
+inline bool operator<(const KeyW& a, const KeyW& b) {
+    for (int i = KW - 1; i >= 0; i--)
+        if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+    return false;
+}
+inline bool operator==(const KeyW& a, const KeyW& b) {
+    for (int i = 0; i < KW; i++)
+        if (a.w[i] != b.w[i]) return false;
+    return true;
+}
+inline bool operator!=(const KeyW& a, const KeyW& b) { return !(a == b); }
+inline KeyW operator>>(const KeyW& a, int s) {
+    KeyW r{};
+    const int q = s / 64, b = s % 64;
+    for (int i = q; i < KW; i++) {
+        uint64_t v = a.w[i] >> b;
+        if (b && i + 1 < KW) v |= a.w[i + 1] << (64 - b);
+        r.w[i - q] = v;
+    }
+    return r;
+}
+KeyW keyw_of(const Big& b) {
+    if (b.neg || b.n > KW) throw std::string("cell index beyond the wide key range");
+    KeyW k{};
+    for (int i = 0; i < b.n; i++) k.w[i] = b.w[i];
+    return k;
+}
+KeyW keyw_of(u128 v) {
+    KeyW k{};
+    k.w[0] = (uint64_t)v;
+    k.w[1] = (uint64_t)(v >> 64);
+    return k;
+}
+Big big_of(u128 v) { return from_u128(v); }
+Big big_of(const KeyW& k) {
+    Big b;
+    int n = KW;
+    while (n > 0 && k.w[n - 1] == 0) n--;
+    for (int i = 0; i < n; i++) b.w[i] = k.w[i];
+    b.n = n;
+    return b;
+}
+
 // _float_down / _float_up of (A + k W / 2^L) / 2^S
-double cell_bound(const Grid& g, int i, int L, unsigned __int128 k, bool up) {
+double cell_bound(const Grid& g, int i, int L, const Big& k, bool up) {
     // value * 2^(S+L) = A 2^L + k W
-    const Big num = add(shl(g.A[i], L), mul_u128(g.W[i], k));
+    const Big num = add(shl(g.A[i], L), mul_big(g.W[i], k));
     const int S2 = g.S[i] + L;
     double f = to_double_rn(num, S2);
     // exact comparison of f with the rational
@@ -396,31 +467,32 @@ double cell_bound(const Grid& g, int i, int L, unsigned __int128 k, bool up) {
 // Cells of one level: flat keys (n indices per cell) + flags; sorted and unique
 // after norm_level().  Cells keep a uniform level per box (snap_to_grid), as in
 // the reference, so a cell is (L, k_0 .. k_{n-1}).
+template <typename K>
 struct LevelVec {
-    std::vector<u128> keys;
+    std::vector<K> keys;
     std::vector<uint8_t> flags;
 };
-using Cells = std::map<int, LevelVec>;
-
-int g_n = 1;  // key width for the comparators below (set per rb_merge call)
+template <typename K>
+using Cells = std::map<int, LevelVec<K>>;
 
 // sort + unique with flag OR (dict assignment `cells[key] = cells.get(key) or flag`)
-void norm_level(LevelVec& v, int n) {
+template <typename K>
+void norm_level(LevelVec<K>& v, int n) {
     const size_t m = v.flags.size();
     std::vector<uint32_t> ord(m);
     for (size_t i = 0; i < m; i++) ord[i] = (uint32_t)i;
     std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) {
-        const u128* x = &v.keys[(size_t)a * n];
-        const u128* y = &v.keys[(size_t)b * n];
+        const K* x = &v.keys[(size_t)a * n];
+        const K* y = &v.keys[(size_t)b * n];
         for (int i = 0; i < n; i++)
             if (x[i] != y[i]) return x[i] < y[i];
         return false;
     });
-    LevelVec o;
+    LevelVec<K> o;
     o.keys.reserve(v.keys.size());
     o.flags.reserve(m);
     for (size_t j = 0; j < m; j++) {
-        const u128* x = &v.keys[(size_t)ord[j] * n];
+        const K* x = &v.keys[(size_t)ord[j] * n];
         if (!o.flags.empty() && std::equal(x, x + n, &o.keys[o.keys.size() - n])) {
             o.flags.back() |= v.flags[ord[j]];
             continue;
@@ -432,13 +504,14 @@ void norm_level(LevelVec& v, int n) {
 }
 
 // index of key in a normalised level, or -1
-int64_t find_key(const LevelVec& v, const u128* key, int n) {
+template <typename K>
+int64_t find_key(const LevelVec<K>& v, const K* key, int n) {
     int64_t lo = 0, hi = (int64_t)v.flags.size() - 1;
     while (lo <= hi) {
         const int64_t mid = (lo + hi) / 2;
-        const u128* x = &v.keys[(size_t)mid * n];
+        const K* x = &v.keys[(size_t)mid * n];
         int c = 0;
-        for (int i = 0; i < n && c == 0; i++) c = x[i] < key[i] ? -1 : (x[i] > key[i] ? 1 : 0);
+        for (int i = 0; i < n && c == 0; i++) c = x[i] < key[i] ? -1 : (key[i] < x[i] ? 1 : 0);
         if (c == 0) return mid;
         if (c < 0) lo = mid + 1;
         else hi = mid - 1;
@@ -448,15 +521,16 @@ int64_t find_key(const LevelVec& v, const u128* key, int n) {
 
 // _drop_nested (backtrack.py:168-191) for uniform-level cells: a cell inside a
 // kept coarser cell is absorbed (flag OR into the coarsest such ancestor).
-Cells drop_nested(Cells cells, int n) {
+template <typename K>
+Cells<K> drop_nested(Cells<K> cells, int n) {
     for (auto& kv : cells) norm_level(kv.second, n);
     if (cells.size() <= 1) return cells;
-    Cells kept;
-    std::vector<u128> anc(n);
+    Cells<K> kept;
+    std::vector<K> anc(n);
     for (auto& [L, v] : cells) {  // coarse (small L) first
-        LevelVec out;
+        LevelVec<K> out;
         for (size_t c = 0; c < v.flags.size(); c++) {
-            const u128* k = &v.keys[c * n];
+            const K* k = &v.keys[c * n];
             bool absorbed = false;
             for (auto& [L2, v2] : kept) {
                 if (L2 >= L) break;
@@ -478,13 +552,15 @@ Cells drop_nested(Cells cells, int n) {
     return kept;
 }
 
-size_t count(const Cells& c) {
+template <typename K>
+size_t count(const Cells<K>& c) {
     size_t s = 0;
     for (auto& kv : c) s += kv.second.flags.size();
     return s;
 }
 
-double cur_width(const Grid& g, const Cells& cells) {
+template <typename K>
+double cur_width(const Grid& g, const Cells<K>& cells) {
     double w = 0.0;
     bool any = false;
     for (auto& [L, m] : cells) {
@@ -496,6 +572,57 @@ double cur_width(const Grid& g, const Cells& cells) {
         }
     }
     return any ? w : 0.0;
+}
+
+struct OutBox {
+    std::vector<double> lo, hi;
+    bool flag;
+};
+
+// merge_to_width (backtrack.py:194-242) of snapped cells, materialised in canonical
+// order (Box.sort_key: lows then highs)
+template <typename K>
+void merge_levels(const Grid& g, Cells<K> cells, double stop_width, int stop_on_plateau, std::vector<OutBox>& out,
+                  std::vector<std::pair<double, int64_t>>& log) {
+    const int n = g.n;
+    cells = drop_nested(std::move(cells), n);
+    log.push_back({cur_width(g, cells), (int64_t)count(cells)});
+    const bool has_stop = stop_width >= 0 && !std::isnan(stop_width);
+    while (count(cells) > 0) {
+        if (stop_on_plateau && log.size() >= 2 && log[log.size() - 1].second == log[log.size() - 2].second) break;
+        if (has_stop && log.back().first >= stop_width) break;
+        if (cells.count(0) && !cells[0].flags.empty()) break;
+        Cells<K> parents;
+        for (auto& [L, m] : cells) {
+            auto& pv = parents[L - 1];
+            pv.keys.resize(m.keys.size());
+            for (size_t i = 0; i < m.keys.size(); i++) pv.keys[i] = m.keys[i] >> 1;
+            pv.flags = m.flags;
+        }
+        cells = drop_nested(std::move(parents), n);
+        log.push_back({cur_width(g, cells), (int64_t)count(cells)});
+    }
+    for (auto& [L, m] : cells)
+        for (size_t c = 0; c < m.flags.size(); c++) {
+            const K* k = &m.keys[c * n];
+            OutBox b;
+            b.lo.resize(n);
+            b.hi.resize(n);
+            for (int i = 0; i < n; i++) {
+                const Big kb = big_of(k[i]);
+                b.lo[i] = cell_bound(g, i, L, kb, false);
+                b.hi[i] = cell_bound(g, i, L, add(kb, from_u128(1)), true);
+            }
+            b.flag = m.flags[c] != 0;
+            out.push_back(std::move(b));
+        }
+    std::sort(out.begin(), out.end(), [&](const OutBox& x, const OutBox& y) {
+        for (int i = 0; i < n; i++)
+            if (x.lo[i] != y.lo[i]) return x.lo[i] < y.lo[i];
+        for (int i = 0; i < n; i++)
+            if (x.hi[i] != y.hi[i]) return x.hi[i] < y.hi[i];
+        return false;
+    });
 }
 
 }  // namespace
@@ -540,13 +667,16 @@ int rb_merge(int n, const double* init_lo, const double* init_hi, const double* 
             g.A.push_back(from_double(init_lo[i], s));
             g.W.push_back(sub(from_double(init_hi[i], s), g.A.back()));
         }
-        // ---- snap_to_grid per box
-        Cells cells;
-        g_n = n;
+        // ---- snap_to_grid per box: 128-bit indices (fast path) or big ones, then the merge
+        // runs on 128-bit keys when every level is at most 120, else on wide keys
+        Cells<u128> cells;
+        std::vector<std::pair<int, std::vector<Big>>> deep;  // (level, indices) of boxes snapped beyond 120
+        std::vector<uint8_t> deep_flags;
         std::vector<i128> fA(n), fW(n);
         bool fast = true;
         for (int i = 0; i < n; i++) fast = fast && big_to_i128(g.A[i], fA[i]) && big_to_i128(g.W[i], fW[i]);
         for (int64_t r = 0; r < N; r++) {
+            const uint8_t flag = cert && cert[r] ? 1 : 0;
             if (fast) {
                 std::vector<u128> fidx(n, 0);
                 int fL = 0;
@@ -556,7 +686,7 @@ int rb_merge(int n, const double* init_lo, const double* init_hi, const double* 
                 if (rc == 0) {
                     auto& lv = cells[fL];
                     lv.keys.insert(lv.keys.end(), fidx.begin(), fidx.end());
-                    lv.flags.push_back(cert && cert[r] ? 1 : 0);
+                    lv.flags.push_back(flag);
                     continue;
                 }
             }
@@ -573,88 +703,67 @@ int rb_merge(int n, const double* init_lo, const double* init_hi, const double* 
                 level = level < 0 ? li : std::min(level, li);
             }
             if (level < 0) level = 52;  // a point box: snap to a deep cell
-            if (level > 120) return fail("snap level beyond the native index range");
-            std::vector<unsigned __int128> idx(n, 0);
+            std::vector<Big> idx(n);
             int L = level;
             for (; L > 0; L--) {
                 bool ok = true;
                 for (int i = 0; i < n && ok; i++) {
                     // k = floor((lo - a) / cw), cw = W / 2^L;  k = min(k, 2^L - 1)
                     Big kb = div_floor(shl(dlo[i], L), g.W[i]);
-                    unsigned __int128 k = to_u128(kb);
-                    const unsigned __int128 kmax = (((unsigned __int128)1) << L) - 1;
-                    if (k > kmax) k = kmax;
+                    const Big kmax = sub(shl(from_u128(1), L), from_u128(1));
+                    if (cmp(kb, kmax) > 0) kb = kmax;
                     // straddles when hi > a + (k+1) cw  <=>  (hi - a) 2^L > (k+1) W
-                    if (cmp(shl(dhi[i], L), mul_u128(g.W[i], k + 1)) > 0) ok = false;
-                    idx[i] = k;
+                    if (cmp(shl(dhi[i], L), mul_big(g.W[i], add(kb, from_u128(1)))) > 0) ok = false;
+                    idx[i] = kb;
                 }
                 if (ok) break;
             }
-            if (L == 0) std::fill(idx.begin(), idx.end(), 0);
+            if (L == 0) std::fill(idx.begin(), idx.end(), Big());
             // merge_to_width: locate() of the snapped cell box is exact only when its
             // materialised bounds are exact (dyadic initial box, backtrack.py:1-9)
             for (int i = 0; i < n; i++) {
-                const Big num_lo = add(shl(g.A[i], L), mul_u128(g.W[i], idx[i]));
+                const Big num_lo = add(shl(g.A[i], L), mul_big(g.W[i], idx[i]));
                 const Big num_hi = add(num_lo, g.W[i]);
-                const double flo = cell_bound(g, i, L, idx[i], false), fhi = cell_bound(g, i, L, idx[i] + 1, true);
+                const double flo = cell_bound(g, i, L, idx[i], false);
+                const double fhi = cell_bound(g, i, L, add(idx[i], from_u128(1)), true);
                 const int S2 = g.S[i] + L;
                 if ((flo != 0.0 && S2 < -low_exp(flo)) || (fhi != 0.0 && S2 < -low_exp(fhi)) ||
                     cmp(from_double(flo, S2), num_lo) != 0 || cmp(from_double(fhi, S2), num_hi) != 0)
-                    return fail("snapped cell is not exactly representable (non-dyadic initial box)");
+                    return fail(L > 120 ? "snapped cell is not exactly representable at its level: the reference's "
+                                          "locate() would give it per-component levels, which rb_merge does not handle"
+                                        : "snapped cell is not exactly representable (non-dyadic initial box)");
             }
-            auto& lv = cells[L];
-            lv.keys.insert(lv.keys.end(), idx.begin(), idx.end());
-            lv.flags.push_back(cert && cert[r] ? 1 : 0);
+            if (L <= 120) {
+                auto& lv = cells[L];
+                for (int i = 0; i < n; i++) lv.keys.push_back(to_u128(idx[i]));
+                lv.flags.push_back(flag);
+            } else {
+                deep.emplace_back(L, std::move(idx));
+                deep_flags.push_back(flag);
+            }
         }
         const bool timing = std::getenv("RB_MERGE_TIMING") != nullptr;
         auto tnow = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
         double t_snap = tnow();
-        cells = drop_nested(std::move(cells), n);
-        // ---- merge levels
         std::vector<std::pair<double, int64_t>> log;
-        log.push_back({cur_width(g, cells), (int64_t)count(cells)});
-        const bool has_stop = stop_width >= 0 && !std::isnan(stop_width);
-        while (count(cells) > 0) {
-            if (stop_on_plateau && log.size() >= 2 && log[log.size() - 1].second == log[log.size() - 2].second) break;
-            if (has_stop && log.back().first >= stop_width) break;
-            if (cells.count(0) && !cells[0].flags.empty()) break;
-            Cells parents;
+        std::vector<OutBox> out;
+        if (deep.empty()) {
+            merge_levels(g, std::move(cells), stop_width, stop_on_plateau, out, log);
+        } else {  // some box snapped beyond level 120: every key goes wide
+            Cells<KeyW> wide;
             for (auto& [L, m] : cells) {
-                auto& pv = parents[L - 1];
-                pv.keys.resize(m.keys.size());
-                for (size_t i = 0; i < m.keys.size(); i++) pv.keys[i] = m.keys[i] >> 1;
-                pv.flags = m.flags;
+                auto& lv = wide[L];
+                for (const u128 k : m.keys) lv.keys.push_back(keyw_of(k));
+                lv.flags = m.flags;
             }
-            cells = drop_nested(std::move(parents), n);
-            log.push_back({cur_width(g, cells), (int64_t)count(cells)});
+            for (size_t d = 0; d < deep.size(); d++) {
+                auto& lv = wide[deep[d].first];
+                for (const Big& k : deep[d].second) lv.keys.push_back(keyw_of(k));
+                lv.flags.push_back(deep_flags[d]);
+            }
+            merge_levels(g, std::move(wide), stop_width, stop_on_plateau, out, log);
         }
         if (timing) std::fprintf(stderr, "rb_merge: merge levels %.3fs\n", tnow() - t_snap);
-        // ---- materialise in canonical order (Box.sort_key: lows then highs)
-        struct OutBox {
-            std::vector<double> lo, hi;
-            bool flag;
-        };
-        std::vector<OutBox> out;
-        for (auto& [L, m] : cells)
-            for (size_t c = 0; c < m.flags.size(); c++) {
-                const u128* k = &m.keys[c * n];
-                OutBox b;
-                b.lo.resize(n);
-                b.hi.resize(n);
-                for (int i = 0; i < n; i++) {
-                    b.lo[i] = cell_bound(g, i, L, k[i], false);
-                    b.hi[i] = cell_bound(g, i, L, k[i] + 1, true);
-                }
-                b.flag = m.flags[c] != 0;
-                out.push_back(std::move(b));
-            }
-        std::sort(out.begin(), out.end(), [&](const OutBox& x, const OutBox& y) {
-            for (int i = 0; i < n; i++)
-                if (x.lo[i] != y.lo[i]) return x.lo[i] < y.lo[i];
-            for (int i = 0; i < n; i++)
-                if (x.hi[i] != y.hi[i]) return x.hi[i] < y.hi[i];
-            return false;
-        });
         *M = (int64_t)out.size();
         for (int64_t r = 0; r < (int64_t)out.size() && r < cap; r++) {
             for (int i = 0; i < n; i++) {

@@ -252,11 +252,14 @@ def _exchange(torch, dist, backend, rank, world, send, group):
     return rows, sc, keep
 
 
-def solve_sharded(s, cfg=None, backend=None, group=None, device: int | None = None, force_protocol=False):
+def solve_sharded(s, cfg=None, backend=None, group=None, device: int | None = None, force_protocol=False,
+                  arrays=False):
     """bnb.solve over the ranks of `group` (default: the world).  Every rank calls
     it; rank 0 returns the SolveResult (canonical order), the others None.  The
     boxes and statistics are those of the single-process solve, bit for bit.
-    force_protocol: run the exchange protocol even at world size 1 (tests)."""
+    force_protocol: run the exchange protocol even at world size 1 (tests).  arrays:
+    return the engine arrays and per-round statistics (with children and hs_calls)
+    instead of SolveResult objects."""
     import torch
     import torch.distributed as dist
     cfg = cfg or SolverConfig()
@@ -270,6 +273,8 @@ def solve_sharded(s, cfg=None, backend=None, group=None, device: int | None = No
         nccl = on and dist.get_backend(group) == "nccl"
         backend = CudaShardBackend(spec, dev, device_exchange=nccl or not on)
     if world == 1 and hasattr(backend, "solve_single") and not force_protocol:
+        if arrays:
+            return backend.eng.solve(native_config(cfg))
         return _result(s, backend.solve_single(cfg))
     comm_dev = (torch.device("cuda", backend.device) if getattr(backend, "device_exchange", False)
                 else torch.device("cpu"))
@@ -318,15 +323,16 @@ def solve_sharded(s, cfg=None, backend=None, group=None, device: int | None = No
                 hs_on = True
             if cfg.hs_enable_width is not None and g_cw <= cfg.hs_enable_width:
                 hs_on = True
-        size, width, _calls = backend.round_hs(hs_on, cfg.hs_contract)
+        size, width, calls = backend.round_hs(hs_on, cfg.hs_contract)
         thin, other = backend.route_count(world)
         stop = 1.0 if (rank == 0 and cfg.max_seconds is not None and
                        time.perf_counter() - t_start > cfg.max_seconds) else 0.0
-        g2 = gather([float(size), width if size else 0.0, float(other), stop, float(carried + surv)]
-                    + [float(v) for v in thin])                              # exchange 2
+        g2 = gather([float(size), width if size else 0.0, float(other), stop, float(carried + surv),
+                     float(children), float(calls)] + [float(v) for v in thin])  # exchange 2
         sizes, g_width = g2[:, 0].astype(np.int64), float(g2[:, 1].max())
         g_after_filter = int(g2[:, 4].sum())
-        thin_m = g2[:, 5:5 + world].astype(np.int64)            # thin_m[r][d]: thin rows r -> d
+        g_children, g_calls = int(g2[:, 5].sum()), int(g2[:, 6].sum())
+        thin_m = g2[:, 7:7 + world].astype(np.int64)            # thin_m[r][d]: thin rows r -> d
         movable = g2[:, 2].astype(np.int64)
         stay = np.array([movable[r] + thin_m[r][r] for r in range(world)])
         after_thin = stay + np.array([thin_m[:, d].sum() - thin_m[d][d] for d in range(world)])
@@ -342,7 +348,7 @@ def solve_sharded(s, cfg=None, backend=None, group=None, device: int | None = No
         backend.dedup()
         pre_total = int(sizes.sum())  # before dedup: duplicates are thin rows now on one shard
         rows_stats.append([round_no, g_in, g_after_filter, pre_total, g_width if pre_total else 0.0,
-                           time.perf_counter() - t0])
+                           time.perf_counter() - t0, g_children, g_calls])
         if pre_total == 0:  # dedup never empties a non-empty frontier
             status = NO_REAL_SOLUTION
             break
@@ -371,11 +377,10 @@ def solve_sharded(s, cfg=None, backend=None, group=None, device: int | None = No
             return None
         backend.import_packed(torch, 0, got)
     lo, hi, c, u = backend.finalize()
-    stats = [tuple(r) for r in rows_stats]
     out = {"status": status, "lo": lo, "hi": hi, "cert": c, "unsplit": u,
            "stats": [dict(round=r[0], boxes_in=r[1], boxes_after_filter=r[2], boxes_after_hs=r[3], width=r[4],
-                          elapsed_seconds=r[5]) for r in stats]}
-    return _result(s, out)
+                          elapsed_seconds=r[5], children=r[6], hs_calls=r[7]) for r in rows_stats]}
+    return out if arrays else _result(s, out)
 
 
 def _result(s, out):

@@ -586,6 +586,23 @@ def part_merge():
         for sw in (None, 0.5):
             cases.append({"name": f"synthetic{t}_sw{sw}", "init_lo": ilo, "init_hi": ihi, "lo": lo, "hi": hi,
                           "cert": cert, "stop_width": sw})
+    # deep levels: boxes far narrower than 2^-120 of the initial width (an HS-contracted box
+    # around a root at the origin) -- snap_to_grid has no level limit (backtrack.py:118-158)
+    ilo = np.array([-2.0, -2.0]); ihi = np.array([2.0, 2.0])
+    deep = [([0.0, -1e-300], [1e-40, 0.0]), ([1.0, 1.0], [1.0 + 2.0 ** -30, 1.0 + 2.0 ** -30]),
+            ([2.0 ** -200, -2.0 ** -180], [2.0 ** -199, -2.0 ** -181]), ([0.25, 0.25], [0.25, 0.25]),
+            ([-1.0, 0.5], [-0.5, 1.0]), ([-0.75, 0.5], [-0.75 + 2.0 ** -300, 0.5 + 2.0 ** -300])]
+    lo = np.array([d[0] for d in deep]); hi = np.array([d[1] for d in deep])
+    for sw in (None, 0.5):
+        cases.append({"name": f"deep_levels_sw{sw}", "init_lo": ilo, "init_hi": ihi, "lo": lo, "hi": hi,
+                      "cert": np.array([1, 0, 1, 0, 0, 1], bool), "stop_width": sw})
+        cases.append({"name": f"deep_levels_advice_sw{sw}", "init_lo": ilo, "init_hi": ihi, "lo": lo[:2],
+                      "hi": hi[:2], "cert": np.array([0, 1], bool), "stop_width": sw})
+    # a deep cell whose other component (a point at -0.5) cannot be materialised exactly
+    # at that level: locate() then gives per-component levels (rb_merge: uniform levels only)
+    cases.append({"name": "deep_levels_mixed_swNone", "init_lo": ilo, "init_hi": ihi,
+                  "lo": np.array([[2.0 ** -200, -0.5]]), "hi": np.array([[2.0 ** -199, -0.5]]),
+                  "cert": np.array([1], bool), "stop_width": None})
     out = []
     for c in cases:
         r = _merge_case(c["init_lo"], c["init_hi"], c["lo"], c["hi"], c["cert"], c["stop_width"])
