@@ -287,6 +287,15 @@ int rb_interval_kat(int device, int op, int policy, int64_t m, const double* xl,
                     const double* yl, const double* yh, double* o0, double* o1, double* o2, double* o3,
                     int8_t* kind);
 
+/* ---- report writer ---------------------------------------
+ * The raw-box sections of the reference's reports for N boxes (lo/hi [N x n],
+ * cert [N]): fmt 0 = the elements of RunReport.to_json's "roots" list exactly as
+ * json.dumps(indent=2) lays them out inside the report object (cli.py:54-86),
+ * fmt 1 = RunReport.to_csv's rows (cli.py:88-100); floats as Python's repr().
+ * Writes at most cap bytes to out (may be null); *len receives the full length. */
+int rb_format_boxes(int n, const double* lo, const double* hi, const uint8_t* cert, int64_t N, int fmt, char* out,
+                    int64_t cap, int64_t* len);
+
 /* ---- measurement utility ----------------------------------------------------
  * Measured throughput of the FP64 pipe on `device` for the directed-rounding
  * instructions the engine issues (DMUL.RM/RP, DADD.RM/RP; one op each), in

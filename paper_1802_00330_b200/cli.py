@@ -4,9 +4,10 @@
 
 Rebinds ``rootbox.bnb.solve`` / ``rootbox.cli.solve`` / ``rootbox.solve`` (the
 three import-time bindings: __init__.py:12, cli.py:26-34) to
-``paper_1802_00330_b200.solve``, and ``rootbox.cli.run_pipeline`` to the native
-pipeline (B200 solve + exact native backtracking merge, pipeline.py), then calls
-``rootbox.cli.main``.  Report formats and exit codes are the reference's own.
+``paper_1802_00330_b200.solve``, ``rootbox.cli.run_pipeline`` to the native
+pipeline (B200 solve + exact native backtracking merge, pipeline.py) and the
+report writers RunReport.to_json / to_csv to the native ones (byte-identical),
+then calls ``rootbox.cli.main``.  Report formats and exit codes are the reference's own.
 Requires the reference package to be importable.
 """
 from __future__ import annotations
@@ -21,11 +22,14 @@ def install():
     import rootbox.cli
 
     from .bnb import solve
-    from .pipeline import run_pipeline
+    from .pipeline import report_to_csv, report_to_json, run_pipeline
     rootbox.bnb.solve = solve
     rootbox.cli.solve = solve
     rootbox.solve = solve
     rootbox.cli.run_pipeline = run_pipeline
+    # the report writers: same bytes, roots section written natively (rb_format_boxes)
+    rootbox.cli.RunReport.to_json = report_to_json
+    rootbox.cli.RunReport.to_csv = report_to_csv
     return rootbox
 
 

@@ -1194,6 +1194,7 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
     key.push_back((uintptr_t)h->trace);
     key.push_back((uintptr_t)h->force_exact);
     key.push_back((uintptr_t)h->hs_tile);
+    key.push_back((uintptr_t)h->lin_tpb);
     if (key != h->graph_key || !h->graph_exec) build_round_graph(h, prm, dedup, scap, key);
     DevState st{};
     st.n_cur = 1;
@@ -2227,6 +2228,10 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     }
     if (k == "mem_budget_mb") {  // engine memory budget (tests of the streamed rounds at small budgets)
         h->mem_budget = value > 0 ? (size_t)value << 20 : h->mem_budget_default;  // 0: the default
+        return RB_OK;
+    }
+    if (k == "lin_tpb") {  // three-kernel HS, n <= 8: 1 = thread-per-box Gauss-Jordan, 0 = G lanes per box
+        h->lin_tpb = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         return RB_OK;
     }
     if (k == "hs_tile") {  // large HS batches: 1 = k_hs_tile (n <= 8), 0 = eval/lin/sweep

@@ -212,8 +212,12 @@ struct rb_handle {
     bool force_exact = false;
     // k_hs_tile (throughput HS, n <= 8): boxes per tile (= threads per block), shared memory,
     // blocks per SM; table-evaluator and specialised builds
-    bool hs_tile = true;
-    int64_t stream_parents = 0;  // > 0: host-driven rounds stream parents in chunks of this size (tests)
+    bool hs_tile = false;  // k_hs_tile measured slower than eval/lin/sweep (6 vs 19 warps per SM): off
+    int64_t stream_parents = 0;
+    // k_hs_lin_tpb (thread per box Gauss-Jordan, n <= 8) in the three-kernel HS
+    int lin_tpb = 1;  // 1: registers (k_hs_lin_tpb), 2: shared memory (k_hs_lin_tps), 0: G lanes per box
+    int lin_tpb_threads = 0, lin_tpb_bps = 1, lin_tps_bps = 1;
+    size_t lin_tpb_smem = 0, lin_tps_smem = 0;  // > 0: host-driven rounds stream parents in chunks of this size (tests)
     int tile_tb = 0, gen_tile_tb = 0;
     size_t tile_smem = 0, gen_tile_smem = 0;
     int tile_bps = 1, gen_tile_bps = 1;

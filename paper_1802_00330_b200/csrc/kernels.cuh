@@ -1695,6 +1695,320 @@ __global__ void __launch_bounds__(128, RB_LIN_MINB) k_hs_lin(SBuf S, int64_t n_i
     }
 }
 
+// K2b, thread per box (n <= 8): the Gauss-Jordan inverse of lin_group with the same
+// operations in the same order, run by one thread in registers -- with G lanes per
+// box (k_hs_lin) every group re-executes the pivot search, row-swap selects and
+// pivot-column shuffles on all of its lanes (ncu, katsura6 round 5: ~1,080 warp
+// instructions per box for k_hs_lin<7>); here they are one thread's scalar work, and
+// the J / F(x) scratch is read and M / g written with coalesced thread-per-box
+// accesses.  The tableau is kept in place (n x n instead of [mid J | I], n x 2n):
+//   slot s < k holds the column of the right half that became non-trivial at step s
+//   (label e_s = original row of the step-s pivot row), slot s >= k the left column s.
+// Every non-trivial operation of linalg.py:137-172 is performed with the same operands;
+// the skipped ones act on exact zeros / ones of the identity half (x - f*0 = x,
+// 1 * inv = inv, 0 - f*inv = -(f*inv)), so the inverse is bit-identical (zero signs
+// aside, which no later operation can observe).  Row swaps are predicated selects.
+template <int N, class A, class AM>
+__device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int64_t t);
+
+template <int N, class A>
+__device__ __forceinline__ void lin_products_reg(const double (&a)[N][N], HsScratch& W, int64_t t) {
+    lin_products_acc<N, A>([&](int i, int u) { return a[i][u]; }, W, t);
+}
+
+// M = A J and g = A F(x) with A given by an accessor am(i, u)
+template <int N, class A, class AM>
+__device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int64_t t) {
+    // M = A J, column by column in place (linalg.py:102-114), u ascending
+#pragma unroll 1
+    for (int j = 0; j < N; j++) {
+        ival jc[N];
+#pragma unroll
+        for (int u = 0; u < N; u++) jc[u] = mk(W.jl[(u * N + j) * W.B + t], W.jh[(u * N + j) * W.B + t]);
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            ival acc = mk(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A, N>(am(i, u), jc[u]));
+            W.jl[(i * N + j) * W.B + t] = acc.lo;
+            W.jh[(i * N + j) * W.B + t] = acc.hi;
+        }
+    }
+    // g = A F(x) (linalg.py:117-129)
+    ival fx[N];
+#pragma unroll
+    for (int u = 0; u < N; u++) fx[u] = mk(W.fl[u * W.B + t], W.fh[u * W.B + t]);
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        ival acc = mk(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A, N>(am(i, u), fx[u]));
+        W.fl[i * W.B + t] = acc.lo;
+        W.fh[i * W.B + t] = acc.hi;
+    }
+}
+
+template <int N>
+static __device__ __noinline__ void lin_products_reg_exact(const double (&a)[N][N], HsScratch& W, int64_t t) {
+    lin_products_reg<N, Exact>(a, W, t);
+}
+
+#ifndef RB_LIN_REG_MINB
+#define RB_LIN_REG_MINB 2
+#endif
+template <int N>
+__global__ void __launch_bounds__(128, RB_LIN_REG_MINB) k_hs_lin_tpb(SBuf S, int64_t n_in_arg, int64_t b0,
+                                                                     HsParams prm, HsScratch W, Counters* ctr) {
+    pdl_enter();
+    static_assert(N <= 8, "k_hs_lin_tpb: one thread holds a box's n x n Gauss-Jordan tableau in registers");
+    bool hs_on;
+    const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
+    if (n_in < 0 || !hs_on || n_in <= prm.fused_max) return;
+    const int64_t b_end = min(n_in, b0 + W.B);
+    for (int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < b_end;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = b - b0;
+        // mid(J) (mid_matrix, linalg.py:132-134) with the exponent range of J
+        ExpRange rj, ra, rf;
+        rj.init();
+        ra.init();
+        rf.init();
+        double c[N][N];
+        double scale = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; i++)
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                const double lo = W.jl[(i * N + j) * W.B + t], hi = W.jh[(i * N + j) * W.B + t];
+                rj.add(lo);
+                rj.add(hi);
+                c[i][j] = mid_of(lo, hi);
+                scale = fmax(scale, fabs(c[i][j]));
+            }
+        // Gauss-Jordan (linalg.py:137-172): threshold 1e-12 scale, first-max pivot,
+        // inv = RN(1/pivot), pivot row scaled, other rows eliminated, no FMA
+        bool singular = scale == 0.0;
+        const double threshold = __dmul_rn(1e-12, scale);
+        uint32_t orig = 0, label = 0;  // 4-bit fields: original row at each position; e_s per slot
+#pragma unroll
+        for (int r = 0; r < N; r++) orig |= (uint32_t)r << (4 * r);
+#pragma unroll
+        for (int k = 0; k < N; k++) {
+            // no early exit (a break would keep the compiler from unrolling the steps, and
+            // with them every register index of c): a singular tableau skips its steps
+            int pr = k;
+            double best = fabs(c[k][k]), pv = c[k][k];
+#pragma unroll
+            for (int r = k + 1; r < N; r++)
+                if (fabs(c[r][k]) > best) {
+                    best = fabs(c[r][k]);
+                    pv = c[r][k];
+                    pr = r;
+                }
+            singular = singular || fabs(pv) < threshold;
+            if (!singular) {
+                // swap rows k and pr (every slot: left columns >= k and the stored right columns)
+#pragma unroll
+                for (int r = k + 1; r < N; r++)
+                    if (r == pr) {
+#pragma unroll
+                        for (int s2 = 0; s2 < N; s2++) {
+                            const double tmp = c[k][s2];
+                            c[k][s2] = c[r][s2];
+                            c[r][s2] = tmp;
+                        }
+                    }
+                const uint32_t ok = (orig >> (4 * k)) & 15u, op = (orig >> (4 * pr)) & 15u;
+                orig = (orig & ~((15u << (4 * k)) | (15u << (4 * pr)))) | (op << (4 * k)) | (ok << (4 * pr));
+                label |= op << (4 * k);  // e_k: original row of the pivot row
+                const double inv = __drcp_rn(pv);  // RN(1/pivot) == 1.0 / pivot (linalg.py:162)
+                // c[k][j] *= inv (linalg.py:163-164): left j > k and the stored right columns;
+                // the right column e_k becomes 1 * inv = inv (slot k; left column k is dead)
+#pragma unroll
+                for (int s2 = 0; s2 < N; s2++) c[k][s2] = s2 == k ? inv : __dmul_rn(c[k][s2], inv);
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    if (i == k) continue;
+                    const double f = c[i][k];
+                    if (f != 0.0) {  // linalg.py:168
+#pragma unroll
+                        for (int s2 = 0; s2 < N; s2++)
+                            c[i][s2] = s2 == k ? __dsub_rn(0.0, __dmul_rn(f, inv))  // 0 - f * inv
+                                               : __dsub_rn(c[i][s2], __dmul_rn(f, c[k][s2]));
+                    }
+                }
+            }
+        }
+        uint8_t fl = 0;
+        if (singular) {
+            fl = HSF_SINGULAR;
+        } else {
+            // unscramble in place, row by row: A[i][e_s] = slot s (predicated selects)
+            double (&a)[N][N] = c;
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                double row[N];
+#pragma unroll
+                for (int u = 0; u < N; u++) {
+                    row[u] = c[i][0];
+#pragma unroll
+                    for (int s2 = 1; s2 < N; s2++)
+                        if (((label >> (4 * s2)) & 15u) == (uint32_t)u) row[u] = c[i][s2];
+                }
+#pragma unroll
+                for (int u = 0; u < N; u++) c[i][u] = row[u];
+            }
+#pragma unroll
+            for (int i = 0; i < N; i++)
+#pragma unroll
+                for (int u = 0; u < N; u++) ra.add(a[i][u]);
+#pragma unroll
+            for (int u = 0; u < N; u++) {
+                rf.add(W.fl[u * W.B + t]);
+                rf.add(W.fh[u * W.B + t]);
+            }
+            rj.emin = min(rj.emin, rf.emin);
+            rj.emax = max(rj.emax, rf.emax);
+            if (!prm.force_exact && prod_guard_ok(ra, rj)) {
+                lin_products_reg<N, Fast>(a, W, t);
+            } else {  // rare: the Exact policy on a memory copy (keeps `a` itself in registers)
+                double ax[N][N];
+#pragma unroll
+                for (int i = 0; i < N; i++)
+#pragma unroll
+                    for (int u = 0; u < N; u++) ax[i][u] = a[i][u];
+                lin_products_reg_exact<N>(ax, W, t);
+                fl = HSF_EXACT_LIN;
+            }
+        }
+        W.flags[t] |= fl;
+    }
+}
+
+// k_hs_lin_tpb with the in-place tableau in shared memory (this thread's column:
+// element (i, s) at C[(i * n + s) * T], conflict-free) instead of registers: n^2 doubles
+// per thread, so more threads stay resident and no register limit is reached at n = 8.
+// Same operations in the same order; the row swap and the unscrambling index memory.
+template <int N>
+#ifndef RB_TPS_MINB7
+#define RB_TPS_MINB7 4
+#endif
+#ifndef RB_TPS_MINB8
+#define RB_TPS_MINB8 3
+#endif
+__global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k_hs_lin_tps(SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
+                                                    Counters* ctr) {
+    pdl_enter();
+    extern __shared__ __align__(16) uint8_t smem[];
+    bool hs_on;
+    const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
+    if (n_in < 0 || !hs_on || n_in <= prm.fused_max) return;
+    const int64_t b_end = min(n_in, b0 + W.B);
+    const int T = blockDim.x;
+    double* C = reinterpret_cast<double*>(smem) + threadIdx.x;
+    auto c = [&](int i, int s2) -> double& { return C[(i * N + s2) * T]; };
+    for (int64_t b = b0 + (int64_t)blockIdx.x * T + threadIdx.x; b < b_end; b += (int64_t)gridDim.x * T) {
+        const int64_t t = b - b0;
+        ExpRange rj, ra, rf;
+        rj.init();
+        ra.init();
+        rf.init();
+        double scale = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; i++)
+#pragma unroll
+            for (int j = 0; j < N; j++) {
+                const double lo = W.jl[(i * N + j) * W.B + t], hi = W.jh[(i * N + j) * W.B + t];
+                rj.add(lo);
+                rj.add(hi);
+                const double m = mid_of(lo, hi);
+                c(i, j) = m;
+                scale = fmax(scale, fabs(m));
+            }
+        bool singular = scale == 0.0;
+        const double threshold = __dmul_rn(1e-12, scale);
+        uint32_t orig = 0, label = 0;
+#pragma unroll
+        for (int r = 0; r < N; r++) orig |= (uint32_t)r << (4 * r);
+#pragma unroll
+        for (int k = 0; k < N; k++) {
+            int pr = k;
+            double best = fabs(c(k, k)), pv = c(k, k);
+#pragma unroll
+            for (int r = k + 1; r < N; r++) {
+                const double v = c(r, k);
+                if (fabs(v) > best) {
+                    best = fabs(v);
+                    pv = v;
+                    pr = r;
+                }
+            }
+            singular = singular || fabs(pv) < threshold;
+            if (!singular) {
+                const uint32_t ok = (orig >> (4 * k)) & 15u, op = (orig >> (4 * pr)) & 15u;
+                orig = (orig & ~((15u << (4 * k)) | (15u << (4 * pr)))) | (op << (4 * k)) | (ok << (4 * pr));
+                label |= op << (4 * k);
+                const double inv = __drcp_rn(pv);  // RN(1/pivot) == 1.0 / pivot (linalg.py:162)
+                double rowk[N];
+#pragma unroll
+                for (int s2 = 0; s2 < N; s2++) {  // swap (row pr <- old row k) and scale row k
+                    const double vk = c(k, s2), vp = c(pr, s2);
+                    c(pr, s2) = vk;
+                    rowk[s2] = s2 == k ? inv : __dmul_rn(vp, inv);
+                    c(k, s2) = rowk[s2];
+                }
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    if (i == k) continue;
+                    const double f = c(i, k);
+                    if (f != 0.0) {  // linalg.py:168
+#pragma unroll
+                        for (int s2 = 0; s2 < N; s2++)
+                            c(i, s2) = s2 == k ? __dsub_rn(0.0, __dmul_rn(f, inv))
+                                               : __dsub_rn(c(i, s2), __dmul_rn(f, rowk[s2]));
+                    }
+                }
+            }
+        }
+        uint8_t fl = 0;
+        if (singular) {
+            fl = HSF_SINGULAR;
+        } else {
+            int slot[N];  // slot[u] = s with e_s = u (unrolled: registers)
+#pragma unroll
+            for (int u = 0; u < N; u++) {
+                slot[u] = 0;
+#pragma unroll
+                for (int s2 = 0; s2 < N; s2++)
+                    if (((label >> (4 * s2)) & 15u) == (uint32_t)u) slot[u] = s2;
+            }
+#pragma unroll
+            for (int i = 0; i < N; i++)
+#pragma unroll
+                for (int u = 0; u < N; u++) ra.add(c(i, u));  // same values, another order
+#pragma unroll
+            for (int u = 0; u < N; u++) {
+                rf.add(W.fl[u * W.B + t]);
+                rf.add(W.fh[u * W.B + t]);
+            }
+            rj.emin = min(rj.emin, rf.emin);
+            rj.emax = max(rj.emax, rf.emax);
+            if (!prm.force_exact && prod_guard_ok(ra, rj)) {
+                lin_products_acc<N, Fast>([&](int i, int u) { return c(i, slot[u]); }, W, t);
+            } else {
+                double ax[N][N];
+#pragma unroll
+                for (int i = 0; i < N; i++)
+#pragma unroll
+                    for (int u = 0; u < N; u++) ax[i][u] = c(i, slot[u]);
+                lin_products_reg_exact<N>(ax, W, t);
+                fl = HSF_EXACT_LIN;
+            }
+        }
+        W.flags[t] |= fl;
+    }
+}
+
 // K2k: the Krawczyk operator (hansen.py:141-170) on the K2a/K2b scratch (x, M, g),
 // thread per box.  Row i: acc = [x_i,x_i] - g_i + sum_{j, (I - M)_ij != [0,0]}
 // (I - M)_ij (X_j - [x_j,x_j]), left to right, then acc intersected with X_i.

@@ -27,6 +27,17 @@ void SetupK<N>::run(rb_handle* h) {
     set_max_dyn_smem(k_hs_sweep<N>, h->smem_optin);
     set_max_dyn_smem(k_hs_fused<N>, h->smem_optin);
     set_max_dyn_smem(k_hs_tile<N>, h->smem_optin);
+    if constexpr (N <= 8) {  // thread-per-box Gauss-Jordan: registers (k_hs_lin_tpb) / shared (k_hs_lin_tps)
+        int nb = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_lin_tpb<N>, 128, 0), "occ lin tpb");
+        h->lin_tpb_threads = 128;
+        h->lin_tpb_smem = 0;
+        h->lin_tpb_bps = std::max(1, nb);
+        set_max_dyn_smem(k_hs_lin_tps<N>, h->smem_optin);
+        h->lin_tps_smem = (size_t)N * N * 128 * sizeof(double);
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_lin_tps<N>, 128, h->lin_tps_smem), "occ lin tps");
+        h->lin_tps_bps = std::max(1, nb);
+    }
     choose_tile(h, k_hs_tile<N>, N, stab_bytes(h->meta, false), h->tile_tb, h->tile_smem, h->tile_bps);
     if (N > 8 || h->tile_tb == 0) h->hs_tile = false;  // n > 8: one box per warp, the three kernels win
     if ((int)h->fused_smem > h->smem_optin) h->hs_fused = false;
@@ -131,7 +142,22 @@ void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* 
     else
         klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
             h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags, R);
-    klaunch(h, k_hs_lin<N>, grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T, h->lin_smem, h->S, n_in, b0, prm, h->W, h->d_ctr);
+    bool tpb = false;
+    if constexpr (N <= 8) {
+        if (h->lin_tpb == 1 && h->lin_tpb_threads > 0) {
+            tpb = true;
+            const int tl = h->lin_tpb_threads;
+            klaunch(h, k_hs_lin_tpb<N>, grid_for(bound, tl, h->sms * h->lin_tpb_bps), tl, h->lin_tpb_smem, h->S, n_in,
+                    b0, prm, h->W, h->d_ctr);
+        } else if (h->lin_tpb == 2) {
+            tpb = true;
+            klaunch(h, k_hs_lin_tps<N>, grid_for(bound, 128, h->sms * h->lin_tps_bps), 128, h->lin_tps_smem, h->S,
+                    n_in, b0, prm, h->W, h->d_ctr);
+        }
+    }
+    if (!tpb)
+        klaunch(h, k_hs_lin<N>, grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T,
+                h->lin_smem, h->S, n_in, b0, prm, h->W, h->d_ctr);
     klaunch(h, k_hs_sweep<N>, grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem,
         h->meta, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags);
     ck(cudaGetLastError(), "hs launch");

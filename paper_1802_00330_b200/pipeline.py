@@ -84,21 +84,82 @@ class RunReport:
         }
 
     def to_json(self) -> str:
-        return json.dumps(self.to_json_dict(), indent=2)
+        return report_to_json(self)
 
     def to_csv(self, var_names) -> str:
-        header = []
-        for nm in var_names:
-            header += [f"{nm}_lo", f"{nm}_hi"]
-        header.append("certified")
-        lines = [",".join(header)]
-        for rb in self.roots:
-            row = []
-            for iv in rb.box:
-                row += [repr(iv.lo), repr(iv.hi)]
-            row.append("true" if rb.certified else "false")
-            lines.append(",".join(row))
-        return "\n".join(lines) + "\n"
+        return report_to_csv(self, var_names)
+
+
+def format_boxes(lo, hi, cert, fmt: str) -> str:
+    """rb_format_boxes: the "roots" elements of RunReport.to_json (fmt "json") or the
+    rows of RunReport.to_csv (fmt "csv") for row-major boxes, written natively with
+    Python's float repr (cli.py:54-100)."""
+    L = _native.lib()
+    lo = np.ascontiguousarray(lo, np.float64)
+    hi = np.ascontiguousarray(hi, np.float64)
+    N = lo.shape[0]
+    n = lo.shape[1] if lo.ndim == 2 else 1
+    c = np.ascontiguousarray(cert, np.uint8).reshape(-1)
+    code = {"json": 0, "csv": 1}[fmt]
+    ln = C.c_int64()
+    p = _native._p
+    rc = L.rb_format_boxes(n, p(lo), p(hi), p(c), N, code, None, 0, C.byref(ln))
+    if rc != 0:
+        raise ValueError("rb_format_boxes: bad arguments")
+    buf = C.create_string_buffer(max(1, ln.value))
+    rc = L.rb_format_boxes(n, p(lo), p(hi), p(c), N, code, buf, ln.value, C.byref(ln))
+    if rc != 0:
+        raise ValueError("rb_format_boxes: bad arguments")
+    return buf.raw[:ln.value].decode("ascii")
+
+
+def _root_arrays(roots):
+    if isinstance(roots, RootBoxes):
+        return roots.lo, roots.hi, roots.cert
+    n = len(roots[0].box) if roots else 1
+    lo = np.array([[iv.lo for iv in rb.box] for rb in roots], np.float64).reshape(-1, n)
+    hi = np.array([[iv.hi for iv in rb.box] for rb in roots], np.float64).reshape(-1, n)
+    return lo, hi, np.array([rb.certified for rb in roots], bool)
+
+
+_ROOTS_MARK = "\x00roots\x00"
+
+
+def report_to_json(rep) -> str:
+    """RunReport.to_json() (cli.py:54-86) with the roots section from rb_format_boxes:
+    byte-identical, for this package's RunReport or the reference's."""
+    d = {
+        "schema_version": SCHEMA_VERSION,
+        "solver_version": "0.1.0",
+        "system": rep.system,
+        "config": rep.config,
+        "status": rep.status,
+        "rounds": [{"round": st.round, "boxes_in": st.boxes_in, "boxes_after_filter": st.boxes_after_filter,
+                    "boxes_after_hs": st.boxes_after_hs, "width": st.width,
+                    "elapsed_seconds": st.elapsed_seconds} for st in rep.result.stats],
+        "roots": _ROOTS_MARK,
+        "merge_levels": [{"width": w, "count": c} for w, c in rep.merge_levels],
+        "wall_seconds": rep.wall_seconds,
+    }
+    text = json.dumps(d, indent=2)
+    if len(rep.roots) == 0:
+        body = "[]"
+    else:
+        lo, hi, cert = _root_arrays(rep.roots)
+        body = "[\n" + format_boxes(lo, hi, cert, "json") + "\n  ]"
+    return text.replace(json.dumps(_ROOTS_MARK), body, 1)
+
+
+def report_to_csv(rep, var_names) -> str:
+    """RunReport.to_csv (cli.py:88-100) with the rows from rb_format_boxes."""
+    header = []
+    for nm in var_names:
+        header += [f"{nm}_lo", f"{nm}_hi"]
+    header.append("certified")
+    if len(rep.roots) == 0:
+        return ",".join(header) + "\n"
+    lo, hi, cert = _root_arrays(rep.roots)
+    return ",".join(header) + "\n" + format_boxes(lo, hi, cert, "csv")
 
 
 def config_echo(cfg, merge: bool) -> dict:
