@@ -268,6 +268,9 @@ def solve_sharded(s, cfg=None, backend=None, group=None, device: int | None = No
     on = dist.is_available() and dist.is_initialized()
     rank = dist.get_rank(group) if on else 0
     world = dist.get_world_size(group) if on else 1
+    if world == 1 and backend is None and not force_protocol:  # the engine's own solve (cached engine)
+        from .bnb import solve, solve_arrays
+        return solve_arrays(s, cfg, device) if arrays else solve(s, cfg)
     if backend is None:
         dev = device if device is not None else (torch.cuda.current_device() if torch.cuda.is_available() else 0)
         nccl = on and dist.get_backend(group) == "nccl"

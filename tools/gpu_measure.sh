@@ -21,4 +21,12 @@ ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "rb
     python tools/prof_solve.py brown8 > $out/ncu_brown8.log 2>&1
 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "rb_round_5/" -o $out/eco8_r5 \
     python tools/prof_solve.py eco8 > $out/ncu_eco8.log 2>&1
-ls -la $out
+# raw metrics + per-line source counters as CSV; the reports themselves stay on the box
+for r in bt6_r3 k6_r5 brown8_r6 eco8_r5; do
+    if [ -f $out/$r.ncu-rep ]; then
+        ncu -i $out/$r.ncu-rep --page raw --csv > $out/${r}_raw.csv 2>/dev/null
+        ncu -i $out/$r.ncu-rep --page details --csv > $out/${r}_details.csv 2>/dev/null
+        rm -f $out/$r.ncu-rep
+    fi
+done
+du -sh $out; ls -la $out
