@@ -39,6 +39,7 @@ struct Compiled {
     std::string name_hs_fused;
     std::string name_hs_eval;
     std::string name_hs_tile;
+    std::string name_filter_tab;
 };
 
 // CUDA source of the specialised translation unit
@@ -57,6 +58,7 @@ struct Loaded {
     cudaKernel_t hs_fused = nullptr;  // k_hs_fused<N, GenEval>
     cudaKernel_t hs_eval = nullptr;   // k_hs_eval<N, GenEval>
     cudaKernel_t hs_tile = nullptr;   // k_hs_tile<N, GenEval>
+    cudaKernel_t filter_tab = nullptr;  // k_filter_tab<N, GenEval>
 };
 
 // load the compiled kernels into the current device's context (process-wide cache)

@@ -167,7 +167,7 @@ struct rb_handle {
     bool gen_pending = false;                              // compiling in the background
     std::future<std::pair<bool, rbg::Compiled>> gen_job;
     std::string gen_err;
-    int gen_cf_bps = 1, gen_filter_bps = 1, gen_hsf_bps = 1, gen_hse_bps = 1;
+    int gen_cf_bps = 1, gen_filter_bps = 1, gen_hsf_bps = 1, gen_hse_bps = 1, gen_ftab_bps = 1;
     bool append_dedup = true;    // round graph: exact dedup at append time instead of k_dedup_insert
     // sharded protocol state
     double shard_target = 0.0;
@@ -342,7 +342,7 @@ static void choose_tile(rb_handle* h, K kernel, int n, int tab_bytes, int& tb_ou
 // table kernels, whose sizes SetupK computed)
 static inline void gen_configure(rb_handle* h) {
     if (!h->gen.ok) return;
-    for (cudaKernel_t k : {h->gen.cf, h->gen.filter, h->gen.hs_fused, h->gen.hs_eval, h->gen.hs_tile}) {
+    for (cudaKernel_t k : {h->gen.cf, h->gen.filter, h->gen.hs_fused, h->gen.hs_eval, h->gen.hs_tile, h->gen.filter_tab}) {
         cudaFuncAttributes fa;
         ck(cudaFuncGetAttributes(&fa, (const void*)k), "gen attrs");
         ck(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -362,7 +362,14 @@ static inline void gen_configure(rb_handle* h) {
         h->gen_hsf_bps = std::max(1, nb);
     }
     choose_tile(h, (const void*)h->gen.hs_tile, h->n, 0, h->gen_tile_tb, h->gen_tile_smem, h->gen_tile_bps);
-    h->use_ftab = false;  // the specialised direct filter beats the tabulated one (eco8 47.9 vs 54.6 ms)
+    if (h->meta.ftab && h->ftab_smem <= (size_t)h->smem_optin) {
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)h->gen.filter_tab, 256, h->ftab_smem), "occ");
+        h->gen_ftab_bps = std::max(1, nb);
+    }
+    // the specialised direct filter beats the tabulated one up to n = 8 (katsura6 6.7 vs 9.3 ms, brown8
+    // 4.7 vs 6.2, eco8 26.2 vs 25.8 ms); with 2^n >= 1024 children per parent the tables pay
+    // (broyden_banded12 3.25 -> 2.35 ms, tools/hs_bench.py --opt filter_tab=1)
+    h->use_ftab = h->n >= 10 && h->meta.ftab;
 }
 
 template <int N>

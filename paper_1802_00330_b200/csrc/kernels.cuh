@@ -672,6 +672,24 @@ struct TabEval {
     __device__ __forceinline__ static ival feq(const TermP* tp, const STab& t, int e, const double2* xs2, int stride) {
         return A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride) : eval_poly_packed<A>(tp, t, e, xs2, stride);
     }
+    // k_filter_tab: equation e of child c as the canonical-order sum of its terms' table
+    // entries tb[tbase[q] + combo], combo = the child's half bits of the term's factors
+    template <int N, class A>
+    __device__ __forceinline__ static ival tsum(const STab& t, const uint16_t* tbase, int e, uint32_t c,
+                                                const double2* tb) {
+        ival acc = mk(0.0, 0.0);
+        const int t0 = t.poly_off[e], t1 = t.poly_off[e + 1];
+        for (int q = t0; q < t1; q++) {
+            int combo = 0;
+            for (int f = t.fac_off[q]; f < t.fac_off[q + 1]; f++) {
+                const int v = t.fac[f] & 0xff;
+                combo = (combo << 1) | (int)((c >> (N - 1 - v)) & 1u);
+            }
+            const double2 tv = tb[tbase[q] + combo];
+            acc = A::add(acc, mk(tv.x, tv.y));
+        }
+        return acc;
+    }
 };
 
 template <int N, class A, class EV = TabEval>
@@ -1049,7 +1067,7 @@ static __device__ __noinline__ ival term_value_exact(const STab& t, int q, int c
     return term_value<Exact>(t, q, combo, plo, phi, pmid);
 }
 
-template <int N>
+template <int N, class EV = TabEval>
 __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                     const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
                                                     int64_t* tags, const int* __restrict__ eq_order, int64_t pcount) {
@@ -1134,17 +1152,8 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
             __syncthreads();
             if (alive) {
                 const double2* tb = table + lp * meta.e_max;
-                ival acc = mk(0.0, 0.0);
-                const int t0 = tab.poly_off[e], t1 = tab.poly_off[e + 1];
-                for (int q = t0; q < t1; q++) {
-                    int combo = 0;
-                    for (int f = tab.fac_off[q]; f < tab.fac_off[q + 1]; f++) {
-                        const int v = tab.fac[f] & 0xff;
-                        combo = (combo << 1) | (int)((c >> (N - 1 - v)) & 1u);
-                    }
-                    const double2 tv = tb[tbase[q] + combo];
-                    acc = exact ? Exact::add(acc, mk(tv.x, tv.y)) : Fast::add(acc, mk(tv.x, tv.y));
-                }
+                const ival acc = exact ? EV::template tsum<N, Exact>(tab, tbase, e, c, tb)
+                                       : EV::template tsum<N, Fast>(tab, tbase, e, c, tb);
                 ops += meta.ops_eq[e];
                 alive = acc.lo <= 0.0 && 0.0 <= acc.hi;
                 if (!alive) atomicAdd(&s_rej[e], 1u);

@@ -105,8 +105,13 @@ void FilterK<N>::run(rb_handle* h, int64_t max_parents, int64_t* tags, int64_t p
         const int64_t units = N >= 8 ? (max_parents << Sh::CHLOG) : ((max_parents + Sh::PPB - 1) >> Sh::LOGPPB);
         const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)h->sms * h->ftab_blocks_per_sm));
         h->launches++;
-        klaunch(h, k_filter_tab<N>, blocks, 256, h->ftab_smem, h->meta, h->d_tab, h->F[h->cur].f, par,
-                                                             h->d_ctr, h->S, tags, h->d_order, pcount);
+        if (gen_on(h))  // specialised sums of table entries (codegen.cpp fts*)
+            klaunch_k(h, h->gen.filter_tab, (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)h->sms * h->gen_ftab_bps)),
+                      256, h->ftab_smem, h->meta, (const uint8_t*)h->d_tab, h->F[h->cur].f, par, h->d_ctr, h->S, tags,
+                      (const int*)h->d_order, pcount);
+        else
+            klaunch(h, k_filter_tab<N>, blocks, 256, h->ftab_smem, h->meta, h->d_tab, h->F[h->cur].f, par,
+                    h->d_ctr, h->S, tags, h->d_order, pcount);
         ck(cudaGetLastError(), "filter_tab launch");
         return;
     }

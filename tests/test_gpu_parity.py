@@ -93,8 +93,8 @@ def _set_codegen(eng, on):
     eng.set_option("codegen", int(on))
 
 
-@pytest.mark.parametrize("mode,codegen", [(1, 0), (0, 0), (0, 1)],
-                         ids=["tabulated", "direct_tables", "direct_specialised"])
+@pytest.mark.parametrize("mode,codegen", [(1, 0), (0, 0), (0, 1), (1, 1)],
+                         ids=["tabulated", "direct_tables", "direct_specialised", "tabulated_specialised"])
 @pytest.mark.parametrize("name", FILTER_SYSTEMS)
 def test_filter_random_cells_vs_oracle(native, name, mode, codegen):
     spec = golden_spec(name)
@@ -273,6 +273,24 @@ def test_solve_vs_reference_golden(native, case, graph, fused, codegen, pingpong
         eng.set_option("hs_fused", 1)
         eng.set_option("codegen", 1)
         eng.set_option("pingpong", 1)
+    check_against_golden(case, out, meta)
+
+
+@pytest.mark.parametrize("case", solve_cases())
+def test_solve_host_loop_tabulated_specialised_filter(native, case):
+    """Host-driven rounds with the tabulated filter on the specialised table sums."""
+    from paper_1802_00330_b200 import bnb
+    meta = load_solve(case)
+    spec = golden_spec(meta["system"])
+    eng = bnb.engine_for(spec)
+    _set_codegen(eng, 1)
+    eng.set_option("graph", 0)
+    eng.set_option("filter_tab", 1)
+    try:
+        out = eng.solve(bnb.native_config(bnb.SolverConfig(**meta["config"])))
+    finally:
+        eng.set_option("graph", 1)
+        eng.set_option("filter_tab", 0)
     check_against_golden(case, out, meta)
 
 
