@@ -267,6 +267,17 @@ int rb_merge(int n, const double* init_lo, const double* init_hi, const double* 
              double* out_hi, uint8_t* out_cert, int64_t cap, int64_t* M, double* levels, int64_t cap_levels,
              int64_t* K, char* err, int64_t err_len);
 
+/* The same merge on `device`: snapping per box in 128-bit
+ * integers, then per merge level a radix sort of the (level, index) keys, exact-duplicate
+ * merge with flag OR, nested-cell absorption and parent index halving on the GPU.
+ * Same arguments and results as rb_merge.  Applies when every initial width is a power of
+ * two and every snapped level is at most 53; otherwise returns RB_ERR_LIMIT (message in
+ * err) and the caller runs rb_merge. */
+int rb_merge_device(int device, int n, const double* init_lo, const double* init_hi, const double* lo,
+                    const double* hi, const uint8_t* cert, int64_t N, double stop_width, int stop_on_plateau,
+                    double* out_lo, double* out_hi, uint8_t* out_cert, int64_t cap, int64_t* M, double* levels,
+                    int64_t cap_levels, int64_t* K, char* err, int64_t err_len);
+
 /* ---- interval-layer known-answer hook (tests) --------------------------------
  * m operand pairs through one device operation of interval.cuh on `device`
  * (host arrays in and out).  x = [xl, xh], y = [yl, yh]; policy 0 = Fast (IEEE

@@ -134,6 +134,8 @@ def lib():
     L.rb_shard_route.restype = i32
     L.rb_shard_finalize.argtypes = [P, C.POINTER(i64)]
     L.rb_shard_finalize.restype = i32
+    L.rb_merge_device.argtypes = [i32] + L.rb_merge.argtypes
+    L.rb_merge_device.restype = i32
     L.rb_format_boxes.argtypes = [i32, P, P, P, i64, i32, P, i64, C.POINTER(i64)]
     L.rb_format_boxes.restype = i32
     L.rb_interval_kat.argtypes = [i32, i32, i32, i64, P, P, P, P, P, P, P, P, P]
@@ -147,7 +149,7 @@ EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch"
             "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak", "rb_set_option",
             "rb_shard_partition", "rb_shard_dedup", "rb_shard_export_device", "rb_shard_import_device",
             "rb_merge", "rb_krawczyk", "rb_codegen_prepare", "rb_codegen_active", "rb_interval_kat",
-            "rb_shard_route_count", "rb_shard_route", "rb_shard_finalize", "rb_format_boxes"]
+            "rb_shard_route_count", "rb_shard_route", "rb_shard_finalize", "rb_format_boxes", "rb_merge_device"]
 
 
 def _p(a):

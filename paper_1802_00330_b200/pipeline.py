@@ -24,9 +24,14 @@ from .system import as_spec
 SCHEMA_VERSION = 1
 
 
-def merge_arrays(init_lo, init_hi, lo, hi, cert, stop_width=None, stop_on_plateau=True):
-    """rb_merge: merged boxes (canonical order), certified flags and the merge
-    levels [(width, count), ...] of merge_to_width(snap_to_grid(boxes))."""
+DEVICE_MERGE_MIN = 20000  # result sets at least this large merge on the device when it applies
+
+
+def merge_arrays(init_lo, init_hi, lo, hi, cert, stop_width=None, stop_on_plateau=True, device=None):
+    """rb_merge / rb_merge_device: merged boxes (canonical order), certified flags and
+    the merge levels [(width, count), ...] of merge_to_width(snap_to_grid(boxes)).
+    device: run on that GPU when the set is on its fast path (power-of-two initial
+    widths, levels <= 53), else on the host; None = the host."""
     L = _native.lib()
     ilo = np.ascontiguousarray(init_lo, np.float64)
     ihi = np.ascontiguousarray(init_hi, np.float64)
@@ -42,9 +47,18 @@ def merge_arrays(init_lo, init_hi, lo, hi, cert, stop_width=None, stop_on_platea
         lv = np.empty((cap_lv, 2))
         M = C.c_int64(); K = C.c_int64()
         p = _native._p
-        rc = L.rb_merge(n, p(ilo), p(ihi), p(lo), p(hi), p(c), N,
-                        -1.0 if stop_width is None else float(stop_width), int(bool(stop_on_plateau)),
-                        p(olo), p(ohi), p(oc), cap, C.byref(M), p(lv), cap_lv, C.byref(K), err, 512)
+        args = (n, p(ilo), p(ihi), p(lo), p(hi), p(c), N, -1.0 if stop_width is None else float(stop_width),
+                int(bool(stop_on_plateau)), p(olo), p(ohi), p(oc), cap, C.byref(M), p(lv), cap_lv, C.byref(K),
+                err, 512)
+        rc = -1
+        if device is not None:
+            rc = L.rb_merge_device(int(device), *args)
+            if rc == _native.RB_ERR_LIMIT:  # not on the device fast path: the host merge decides
+                device = None
+            elif rc != 0:
+                raise _native.NativeError(f"rb_merge_device: {err.value.decode()}")
+        if device is None:
+            rc = L.rb_merge(*args)
         if rc != 0:
             raise ValueError(f"rb_merge: {err.value.decode()}")
         if M.value <= cap and K.value <= cap_lv:
@@ -195,7 +209,10 @@ def run_pipeline(s, cfg=None, merge: bool = True, merge_width=None):
             lo = np.array([[iv.lo for iv in rb.box] for rb in result.boxes]).reshape(-1, n)
             hi = np.array([[iv.hi for iv in rb.box] for rb in result.boxes]).reshape(-1, n)
             cert = np.array([rb.certified for rb in result.boxes], bool)
-        mlo, mhi, mc, levels = merge_arrays(spec.init_lo, spec.init_hi, lo, hi, cert, stop_width=merge_width)
+        from .bnb import default_device
+        dev = default_device() if lo.shape[0] >= DEVICE_MERGE_MIN else None
+        mlo, mhi, mc, levels = merge_arrays(spec.init_lo, spec.init_hi, lo, hi, cert, stop_width=merge_width,
+                                            device=dev)
         roots = tuple(RB(BX(tuple(IV(a, b) for a, b in zip(mlo[r].tolist(), mhi[r].tolist()))), bool(mc[r]))
                       for r in range(mlo.shape[0]))
     wall = time.perf_counter() - t0
