@@ -692,6 +692,12 @@ struct TabEval {
     }
 };
 
+// Filter policy.  A sign-selected 2-product multiply (branch on "no operand straddles
+// zero", warp-uniform for bisection cells) measured slower than the branch-free 8-product
+// tree: katsura6 filter 6.7 -> 11.1 ms, eco8 26.2 -> 33.6 ms (tools/hs_bench.py).
+#ifndef RB_FILTER_FAST
+#define RB_FILTER_FAST Fast
+#endif
 template <int N, class A, class EV = TabEval>
 __device__ __forceinline__ bool feasible(const TabMeta& meta, const TermP* tp, const STab& t, const double2* xs2,
                                          int stride, const int* order, unsigned* s_eval, unsigned* s_rej,
@@ -791,7 +797,7 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
                 w = j == 0 ? d : (d > w ? d : w);
             }
             const bool sample = (blockIdx.x & 3) == 0;  // statistics from a quarter of the blocks
-            if (!exact) keep = feasible<N, Fast, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
+            if (!exact) keep = feasible<N, RB_FILTER_FAST, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
             else {
                 keep = feasible<N, Exact, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
                 exact_acc++;
@@ -924,7 +930,7 @@ __global__ void __launch_bounds__(256) k_classify_filter(TabMeta meta, const uin
             if (parent) {
                 const bool exact = !poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, r);
                 const bool sample = (blockIdx.x & 3) == 0;  // statistics from a quarter of the blocks
-                if (!exact) keep = feasible<N, Fast, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
+                if (!exact) keep = feasible<N, RB_FILTER_FAST, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
                 else {
                     keep = feasible<N, Exact, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
                     exact_acc++;
@@ -1146,7 +1152,7 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
                 const uint32_t en = ent[e0 + i];
                 const double* q = sp + l2 * (3 * N + 1);
                 const ival v = (q[3 * N] != 0.0) ? term_value_exact(tab, en & 0xffff, en >> 16, q, q + N, q + 2 * N)
-                                                 : term_value<Fast>(tab, en & 0xffff, en >> 16, q, q + N, q + 2 * N);
+                                                 : term_value<RB_FILTER_FAST>(tab, en & 0xffff, en >> 16, q, q + N, q + 2 * N);
                 table[l2 * meta.e_max + i] = make_double2(v.lo, v.hi);
             }
             __syncthreads();
@@ -1209,8 +1215,11 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
 //   K2c k_hs_sweep  thread per box: Gauss-Seidel sweep with extended division,
 //                   fork / certification, compaction of 0-2 outputs into F_next
 //
-// The scratch costs (2n^2 + 3n) x 8 B of HBM traffic per box and pass, small
-// against the O(n^3) FP64 work; every phase gets the parallel shape that suits it.
+// The scratch costs ~2 x (2n^2 + 3n) x 8 B of HBM traffic per box (written by K2a, read
+// and rewritten by K2b, read by K2c): ~2.8 KB per box at n = 8 against 0.3 KB of frontier
+// I/O (ncu, brown8 round 6: 8.2 GB for 2.96M boxes in k_hs_lin_tps).  It is not what
+// bounds these kernels (k_hs_lin_tps runs at 1.6 TB/s, ~25 % of HBM): keeping the
+// operands on chip (k_hs_tile) cost more residency than the traffic it saved.
 
 struct HsParams {
     int round_no;
