@@ -775,26 +775,45 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
     __syncthreads();
     const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
     unsigned long long ops_acc = 0, exact_acc = 0;
+    // the block's parents of an iteration (blockDim / 2^N of them, or one parent's slice of
+    // children for 2^N >= blockDim): (lo, mid, hi) per component staged once in shared
+    // memory, so a child picks its halves with one 16-byte load per component instead of
+    // every child re-reading the parent and recomputing the midpoints
+    __shared__ double s_par[384];  // max over N of (256 >> N) * N * 3 (N = 1, 2), and 3N for N >= 8
+    __shared__ uint8_t s_pex[128];
+    const int log_bd = 31 - __clz((int)blockDim.x);
+    const int np = N >= log_bd ? 1 : (int)(blockDim.x >> N);
     for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < total; base += gstride) {
         const unsigned long long idx = base + threadIdx.x;
         const bool valid = idx < total;
+        const unsigned long long p_first = base >> N;
+        __syncthreads();  // the previous iteration's children are done with s_par
+        for (int k = threadIdx.x; k < np * N; k += blockDim.x) {
+            const int lp = k / N, j = k - lp * N;
+            if (((p_first + lp) << N) < total) {
+                const uint32_t pe = parents[p_first + lp];
+                const uint32_t p = pe & 0x7fffffffu;
+                const double lo = cur.lo[j * cur.cap + p], hi = cur.hi[j * cur.cap + p];
+                double* q = s_par + 3 * (lp * N + j);
+                q[0] = lo;
+                q[1] = mid_of(lo, hi);
+                q[2] = hi;
+                if (j == 0) s_pex[lp] = (uint8_t)(pe >> 31);
+            }
+        }
+        __syncthreads();
         bool keep = false;
         double w = 0.0;
         unsigned ops = 0;
         if (valid) {
-            const uint32_t pe = parents[idx >> N];
-            const uint32_t p = pe & 0x7fffffffu;
-            const bool exact = pe >> 31;
+            const int lp = (int)((idx >> N) - p_first);
+            const bool exact = s_pex[lp] != 0;
             const uint32_t c = (uint32_t)(idx & ((1ull << N) - 1));
 #pragma unroll
             for (int j = 0; j < N; j++) {
-                const double lo = cur.lo[j * cur.cap + p], hi = cur.hi[j * cur.cap + p];
-                const double m = mid_of(lo, hi);
                 const bool up = (c >> (N - 1 - j)) & 1u;
-                const double cl = up ? m : lo, ch = up ? hi : m;
-                xs2[j * stride] = make_double2(cl, ch);
-                const double d = __dsub_rn(ch, cl);
-                w = j == 0 ? d : (d > w ? d : w);
+                const double* q = s_par + 3 * (lp * N + j) + (up ? 1 : 0);
+                xs2[j * stride] = make_double2(q[0], q[1]);
             }
             const bool sample = (blockIdx.x & 3) == 0;  // statistics from a quarter of the blocks
             if (!exact) keep = feasible<N, RB_FILTER_FAST, EV>(meta, tp, tab, xs2, stride, s_order, s_eval, s_rej, sample, ops);
@@ -803,6 +822,14 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
                 exact_acc++;
             }
             ops_acc += ops;
+            if (keep) {  // child width (bnb.py:290) only for survivors
+#pragma unroll
+                for (int j = 0; j < N; j++) {
+                    const double2 x = xs2[j * stride];
+                    const double d = __dsub_rn(x.y, x.x);
+                    w = j == 0 ? d : (d > w ? d : w);
+                }
+            }
         }
         const unsigned long long slot = warp_append(keep, &ctr->n_surv);
         if (keep && slot < (unsigned long long)S.cap) {
