@@ -474,15 +474,22 @@ def sharded_solve(args, world, rank, local, config="brown8", steps=None):
     for _ in range(max(1, min(args.warmup, 3))):
         out = solve_sharded(spec, cfg, backend=backend, arrays=True)  # warm: buffers, kernels
     ts = []
+    from paper_1802_00330_b200 import _native
+    launches = 0
     for _ in range(steps):
         barrier(world)
         torch.cuda.synchronize()
+        l0 = _native.lib().rb_kernel_launches(backend.eng.h)
         t0 = time.perf_counter()
         out = solve_sharded(spec, cfg, backend=backend, arrays=True)
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
+        # world 1 runs rb_solve (its own count); otherwise the protocol's calls accumulate
+        launches += int(out["kernel_launches"]) if world == 1 else \
+            int(_native.lib().rb_kernel_launches(backend.eng.h) - l0)
     barrier(world)
     t = allreduce_max(world, sum(ts), local)
+    launches = int(allreduce_sum(world, launches, local))
     boxes = None
     if rank == 0:
         boxes = int(sum(st["children"] + st["hs_calls"] for st in out["stats"]))
@@ -504,6 +511,7 @@ def sharded_solve(args, world, rank, local, config="brown8", steps=None):
             "rounds": len(out["stats"]), "final_boxes": int(out["lo"].shape[0]), "boxes_per_step": boxes,
             "time_to_solution_ms": 1e3 * t / steps, "boxes_per_s": boxes * steps / t,
             "e2e_time_to_solution_ms": 1e3 * te / len(e2e_t), "e2e_boxes_per_s": boxes * len(e2e_t) / te,
+            "gpu_launches": launches,
             "timing": "host clock between barrier+synchronize, max over ranks",
             "path": "dist.solve_sharded (world 1: the engine's own solve)",
             "final_result_type": type(res.boxes).__name__}
@@ -536,7 +544,7 @@ def run_scaling(args, world, rank, local):
                 "d2h_bytes_per_step": int(sh["final_boxes"] * (16 * spec.n + 2)),
                 "time_to_solution_ms": sh["e2e_time_to_solution_ms"],
                 "path": "paper_1802_00330_b200.dist.solve_sharded(spec, cfg) -> SolveResult on rank 0"},
-        "gpu_launches": None,
+        "gpu_launches": sh["gpu_launches"],
         "clocks": clocks,
         "timing": sh["timing"],
     }

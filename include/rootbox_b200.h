@@ -225,6 +225,10 @@ int rb_shard_route(rb_handle* h, int32_t world, int32_t rank, const int64_t* mov
  * a sharded solve, bnb.py:322-326); *nboxes receives the row count. */
 int rb_shard_finalize(rb_handle* h, int64_t* nboxes);
 
+/* Kernels launched by the handle since its last rb_solve (the shard protocol's calls
+ * accumulate): the launch count of a sharded solve, for the bench record. */
+int64_t rb_kernel_launches(rb_handle* h);
+
 /* Engine tuning knobs (results never depend on them):
  *   "filter_tab"  1: tabulated per-parent term filter (k_filter_tab) when the tables
  *                 fit; 0: direct per-child evaluation (k_filter).  Default: the direct

@@ -134,6 +134,8 @@ def lib():
     L.rb_shard_route.restype = i32
     L.rb_shard_finalize.argtypes = [P, C.POINTER(i64)]
     L.rb_shard_finalize.restype = i32
+    L.rb_kernel_launches.argtypes = [P]
+    L.rb_kernel_launches.restype = i64
     L.rb_merge_device.argtypes = [i32] + L.rb_merge.argtypes
     L.rb_merge_device.restype = i32
     L.rb_format_boxes.argtypes = [i32, P, P, P, i64, i32, P, i64, C.POINTER(i64)]
@@ -149,7 +151,8 @@ EXPORTED = ["rb_version", "rb_device_count", "rb_create", "rb_solve", "rb_fetch"
             "rb_shard_export", "rb_shard_import", "rb_shard_size", "rb_fp64_peak", "rb_set_option",
             "rb_shard_partition", "rb_shard_dedup", "rb_shard_export_device", "rb_shard_import_device",
             "rb_merge", "rb_krawczyk", "rb_codegen_prepare", "rb_codegen_active", "rb_interval_kat",
-            "rb_shard_route_count", "rb_shard_route", "rb_shard_finalize", "rb_format_boxes", "rb_merge_device"]
+            "rb_shard_route_count", "rb_shard_route", "rb_shard_finalize", "rb_format_boxes", "rb_merge_device",
+            "rb_kernel_launches"]
 
 
 def _p(a):
@@ -206,6 +209,14 @@ class Engine:
         # unit per engine: ctypes releases the GIL, and the engine cache hands the
         # same Engine to every thread solving the same system.
         self._lock = threading.RLock()
+        self._info = RbResultInfo()  # reused under the lock
+        self._info_ref = C.byref(self._info)
+        self._cfg_cache = (None, None)
+
+    def _cfg_ref(self, cfg):
+        if self._cfg_cache[0] is not cfg:
+            self._cfg_cache = (cfg, C.byref(cfg))
+        return self._cfg_cache[1]
 
     def codegen_active(self):
         """(True, '') when the system-specialised kernels run, else (False, reason)."""
@@ -251,14 +262,22 @@ class Engine:
             if device_timing != self._device_timing:
                 self.set_option("device_timing", 1 if device_timing else 0)
                 self._device_timing = device_timing
-            info = RbResultInfo()
-            _check(L.rb_solve(self.h, C.byref(cfg), C.byref(info)), self.h, "rb_solve")
+            info = self._info
+            _check(L.rb_solve(self.h, self._cfg_ref(cfg), self._info_ref), self.h, "rb_solve")
             N, n, nr = int(info.nboxes), self.n, int(info.nrounds)
-            lo = np.empty((N, n)); hi = np.empty((N, n))
-            flags = np.empty((2, N), np.uint8)  # cert, unsplit
-            stats = np.empty(max(1, nr), _STATS_DTYPE)
-            _check(L.rb_fetch(self.h, lo.ctypes.data, hi.ctypes.data, flags.ctypes.data, flags[1].ctypes.data,
-                              stats.ctypes.data), self.h, "rb_fetch")
+            # one host buffer for rows, flags and statistics: a single address lookup
+            # (ndarray.ctypes costs ~1 us per access on this per-solve path)
+            sb = _STATS_DTYPE.itemsize * max(1, nr)
+            rb = 8 * N * n
+            buf = np.empty(2 * rb + 2 * N + sb + 8, np.uint8)
+            a0 = buf.ctypes.data
+            a_st = (a0 + 2 * rb + 2 * N + 7) & ~7
+            _check(L.rb_fetch(self.h, a0, a0 + rb, a0 + 2 * rb, a0 + 2 * rb + N, a_st), self.h, "rb_fetch")
+            lo = buf[:rb].view(np.float64).reshape(N, n)
+            hi = buf[rb:2 * rb].view(np.float64).reshape(N, n)
+            flags = buf[2 * rb:2 * rb + 2 * N].reshape(2, N)
+            o = a_st - a0
+            stats = buf[o:o + sb].view(_STATS_DTYPE)
         rows = stats[:nr].tolist()
         fb = flags.view(np.bool_)
         return {"status": STATUS_NAMES[info.status], "lo": lo, "hi": hi, "cert": fb[0], "unsplit": fb[1],

@@ -214,7 +214,25 @@ def engine_for(spec: SystemSpec, device: int | None = None) -> _native.Engine:
         return e
 
 
+_NCFG: dict = {}
+
+
 def native_config(cfg, exact_round_dedup: bool = True) -> _native.RbConfig:
+    """rb_config of a (frozen) SolverConfig, cached per config value."""
+    try:
+        key = (cfg, exact_round_dedup)
+        hit = _NCFG.get(key)
+    except TypeError:  # an unhashable config-like object
+        key, hit = None, None
+    if hit is not None:
+        return hit
+    out = _native_config(cfg, exact_round_dedup)
+    if key is not None and len(_NCFG) < 256:
+        _NCFG[key] = out
+    return out
+
+
+def _native_config(cfg, exact_round_dedup: bool) -> _native.RbConfig:
     return _native.RbConfig(
         target_width=-1.0 if cfg.target_width is None else float(cfg.target_width),
         hs_enable_round=-1 if cfg.hs_enable_round is None else int(cfg.hs_enable_round),

@@ -2010,6 +2010,10 @@ int rb_shard_import(rb_handle* h, int64_t keep, const double* lo, const double* 
 
 int64_t rb_shard_size(rb_handle* h) { return h ? h->n_cur : -1; }
 
+// kernels launched by this handle since its last rb_solve (the shard protocol's calls
+// accumulate; rb_solve reports its own count in rb_result_info.kernel_launches)
+int64_t rb_kernel_launches(rb_handle* h) { return h ? h->launches : -1; }
+
 int rb_shard_partition(rb_handle* h, int32_t world, int64_t* counts) {
     if (!h || world < 1 || !counts) return RB_ERR_ARG;
     std::lock_guard<std::mutex> lk(h->mu);
