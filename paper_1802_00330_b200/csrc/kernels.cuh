@@ -3642,6 +3642,11 @@ __global__ void k_solve_finish(const DevState* st, const DevRoundStats* rs, cons
     const Front f0 = s.cur ? fb : fa;  // frontier in F[cur]
     const long long N = (long long)s.n_cur;
     const bool gather = s.done && N <= max_rows;
+    // only the blocks with rows to gather take part (block 0 always: state + statistics);
+    // the rest leave at once instead of each fencing and counting itself
+    const long long rows = gather ? N : 0;
+    const unsigned active = (unsigned)max(1ll, min((long long)gridDim.x, (rows + blockDim.x - 1) / blockDim.x));
+    if (blockIdx.x >= active) return;
     if (blockIdx.x == 0) {
         const int first = s.round0 - 1;  // device copy: no PCIe read of hx->start
         for (int r = first + (int)threadIdx.x; r < s.nrounds; r += blockDim.x) hstats[r] = rs[r];
@@ -3653,7 +3658,7 @@ __global__ void k_solve_finish(const DevState* st, const DevRoundStats* rs, cons
     }
     if (gather) {
         for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N;
-             i += (long long)gridDim.x * blockDim.x) {
+             i += (long long)active * blockDim.x) {
             for (int j = 0; j < n; j++) {
                 hlo[i * n + j] = canon0(f0.lo[j * f0.cap + i]);
                 hhi[i * n + j] = canon0(f0.hi[j * f0.cap + i]);
@@ -3669,7 +3674,7 @@ __global__ void k_solve_finish(const DevState* st, const DevRoundStats* rs, cons
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned prev = atomicAdd(&const_cast<DevState*>(st)->finish_blocks, 1u);
-        if (prev == gridDim.x - 1) {
+        if (prev == active - 1) {
             __threadfence_system();
             *reinterpret_cast<volatile unsigned long long*>(&hx->done_seq) = s.seq;
         }
