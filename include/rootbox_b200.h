@@ -230,10 +230,12 @@ int rb_shard_finalize(rb_handle* h, int64_t* nboxes);
 int64_t rb_kernel_launches(rb_handle* h);
 
 /* Engine tuning knobs (results never depend on them):
- *   "filter_tab"  1: tabulated per-parent term filter (k_filter_tab) when the tables
- *                 fit; 0: direct per-child evaluation (k_filter).  Default: the direct
- *                 filter when the system-specialised kernels are loaded (they beat the
- *                 tables), else the tables when the F terms multiply several variables.
+ *   "filter_tab"  1: tabulated per-parent term filter (k_filter_tab, a block per
+ *                 parent) when the tables fit; 0: direct per-child evaluation (k_filter).
+ *                 Default: on for n >= 10 (2^n >= 1024 children per parent).
+ *   "filter_wt"   1: warp-tabulated filter (k_filter_wt, a warp per parent, 5 <= n <= 10),
+ *                 ahead of "filter_tab"; 0: off; -1: the default, on when every
+ *                 equation's table has at most 2^(n-2) entries.
  *   "force_exact" 0 (default): exponent guards pick IEEE directed rounding wherever it
  *                 provably equals the reference; 1: every guard fails, so every box
  *                 runs the Exact policy (the reference's error-free transformations,

@@ -40,6 +40,7 @@ struct Compiled {
     std::string name_hs_eval;
     std::string name_hs_tile;
     std::string name_filter_tab;
+    std::string name_filter_wt;
 };
 
 // CUDA source of the specialised translation unit
@@ -59,6 +60,7 @@ struct Loaded {
     cudaKernel_t hs_eval = nullptr;   // k_hs_eval<N, GenEval>
     cudaKernel_t hs_tile = nullptr;   // k_hs_tile<N, GenEval>
     cudaKernel_t filter_tab = nullptr;  // k_filter_tab<N, GenEval>
+    cudaKernel_t filter_wt = nullptr;   // k_filter_wt<N, GenEval>
 };
 
 // load the compiled kernels into the current device's context (process-wide cache)

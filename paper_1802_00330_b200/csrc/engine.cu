@@ -1175,7 +1175,8 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         (uintptr_t)h->table_slots, (uintptr_t)h->d_slot, (uintptr_t)h->d_dead, (uintptr_t)h->d_rstats,
         (uintptr_t)h->d_state, (uintptr_t)scap, (uintptr_t)dedup, (uintptr_t)prm.hs_enable_round,
         (uintptr_t)prm.hs_possible, (uintptr_t)hw_bits, (uintptr_t)prm.contract_output,
-        (uintptr_t)(h->use_ftab ? 1 : 0), (uintptr_t)(h->hs_fused ? 1 : 0), (uintptr_t)h->fused_rows};
+        (uintptr_t)(h->use_ftab ? 1 : 0), (uintptr_t)(h->hs_fused ? 1 : 0), (uintptr_t)h->fused_rows,
+        (uintptr_t)(h->use_fwt ? 1 : 0)};
     key.push_back((uintptr_t)h->hs_cond);
     key.push_back((uintptr_t)h->graph_unroll);
     key.push_back((uintptr_t)h->graph_fused_only);
@@ -2153,6 +2154,10 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     const std::string k(key);
     if (k == "filter_tab") {
         h->use_ftab = value != 0;
+        return RB_OK;
+    }
+    if (k == "filter_wt") {  // warp-tabulated filter where it applies (5 <= n <= 10, tables fit); -1: auto
+        h->use_fwt = value < 0 ? h->fwt_auto : value != 0;
         return RB_OK;
     }
     if (k == "hs_fused") {  // 0: eval/lin/sweep only, 1: by batch size, 2: fused only

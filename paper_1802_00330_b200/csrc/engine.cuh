@@ -183,6 +183,10 @@ struct rb_handle {
     size_t filter_smem = 0, eval_smem = 0, lin_smem = 0, sweep_smem = 0, ftab_smem = 0;
     int ftab_blocks_per_sm = 1;
     bool use_ftab = true;
+    // warp-tabulated filter (k_filter_wt, 5 <= n <= 10): shared memory, blocks per SM (table / specialised)
+    bool use_fwt = false, fwt_auto = false;
+    size_t fwt_smem = 0;
+    int fwt_bps = 0, gen_fwt_bps = 0;
     bool hs_fused = true;        // k_hs_fused (tile in shared memory) for small HS batches
     int64_t fused_rows = 0;      // largest HS batch k_hs_fused takes (set from the SM count)
     cudaStream_t st_side = nullptr;  // captures the IF branch of the round graph
@@ -342,7 +346,7 @@ static void choose_tile(rb_handle* h, K kernel, int n, int tab_bytes, int& tb_ou
 // table kernels, whose sizes SetupK computed)
 static inline void gen_configure(rb_handle* h) {
     if (!h->gen.ok) return;
-    for (cudaKernel_t k : {h->gen.cf, h->gen.filter, h->gen.hs_fused, h->gen.hs_eval, h->gen.hs_tile, h->gen.filter_tab}) {
+    for (cudaKernel_t k : {h->gen.cf, h->gen.filter, h->gen.hs_fused, h->gen.hs_eval, h->gen.hs_tile, h->gen.filter_tab, h->gen.filter_wt}) {
         cudaFuncAttributes fa;
         ck(cudaFuncGetAttributes(&fa, (const void*)k), "gen attrs");
         ck(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -365,6 +369,11 @@ static inline void gen_configure(rb_handle* h) {
     if (h->meta.ftab && h->ftab_smem <= (size_t)h->smem_optin) {
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)h->gen.filter_tab, 256, h->ftab_smem), "occ");
         h->gen_ftab_bps = std::max(1, nb);
+    }
+    h->gen_fwt_bps = 0;
+    if (h->fwt_bps > 0) {
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)h->gen.filter_wt, 256, h->fwt_smem), "occ");
+        h->gen_fwt_bps = nb;
     }
     // the specialised direct filter beats the tabulated one up to n = 8 (katsura6 6.7 vs 9.3 ms, brown8
     // 4.7 vs 6.2, eco8 26.2 vs 25.8 ms); with 2^n >= 1024 children per parent the tables pay

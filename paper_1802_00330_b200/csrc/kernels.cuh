@@ -698,6 +698,10 @@ struct TabEval {
 #ifndef RB_FILTER_FAST
 #define RB_FILTER_FAST Fast
 #endif
+#ifndef RB_FILTER_WARPSTAGE
+#define RB_FILTER_WARPSTAGE 1  // k_filter: parents staged per warp, no block barrier per iteration
+                               // (filter katsura6 6.7 -> 6.2 ms, brown8 5.1 -> 4.3, eco8 23.5 -> 22.7)
+#endif
 template <int N, class A, class EV = TabEval>
 __device__ __forceinline__ bool feasible(const TabMeta& meta, const TermP* tp, const STab& t, const double2* xs2,
                                          int stride, const int* order, unsigned* s_eval, unsigned* s_rej,
@@ -781,38 +785,61 @@ __device__ __forceinline__ void k_filter_body(TabMeta meta, const uint8_t* __res
     // every child re-reading the parent and recomputing the midpoints
     __shared__ double s_par[384];  // max over N of (256 >> N) * N * 3 (N = 1, 2), and 3N for N >= 8
     __shared__ uint8_t s_pex[128];
+#if RB_FILTER_WARPSTAGE
+    // per warp: its 32 children belong to one parent (n >= 5) or to 32 / 2^n parents,
+    // whose (lo, mid, hi) lanes 0 .. np*n-1 stage in the warp's own slice (no block barrier)
+    constexpr int np = N >= 5 ? 1 : (32 >> N);
+    double* par = s_par + (threadIdx.x >> 5) * 48;
+    uint8_t* pex = s_pex + (threadIdx.x >> 5) * 16;
+    const int lane_f = threadIdx.x & 31;
+#else
     const int log_bd = 31 - __clz((int)blockDim.x);
     const int np = N >= log_bd ? 1 : (int)(blockDim.x >> N);
+    double* par = s_par;
+    uint8_t* pex = s_pex;
+#endif
     for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < total; base += gstride) {
         const unsigned long long idx = base + threadIdx.x;
         const bool valid = idx < total;
+#if RB_FILTER_WARPSTAGE
+        const unsigned long long p_first = (base + (threadIdx.x & ~31u)) >> N;
+        __syncwarp();  // the warp's previous children are done with its slice
+        if (lane_f < np * N) {
+            const int lp = lane_f / N, j = lane_f - lp * N;
+            if (((p_first + lp) << N) < total) {
+#else
         const unsigned long long p_first = base >> N;
         __syncthreads();  // the previous iteration's children are done with s_par
         for (int k = threadIdx.x; k < np * N; k += blockDim.x) {
             const int lp = k / N, j = k - lp * N;
             if (((p_first + lp) << N) < total) {
+#endif
                 const uint32_t pe = parents[p_first + lp];
                 const uint32_t p = pe & 0x7fffffffu;
                 const double lo = cur.lo[j * cur.cap + p], hi = cur.hi[j * cur.cap + p];
-                double* q = s_par + 3 * (lp * N + j);
+                double* q = par + 3 * (lp * N + j);
                 q[0] = lo;
                 q[1] = mid_of(lo, hi);
                 q[2] = hi;
-                if (j == 0) s_pex[lp] = (uint8_t)(pe >> 31);
+                if (j == 0) pex[lp] = (uint8_t)(pe >> 31);
             }
         }
+#if RB_FILTER_WARPSTAGE
+        __syncwarp();
+#else
         __syncthreads();
+#endif
         bool keep = false;
         double w = 0.0;
         unsigned ops = 0;
         if (valid) {
             const int lp = (int)((idx >> N) - p_first);
-            const bool exact = s_pex[lp] != 0;
+            const bool exact = pex[lp] != 0;
             const uint32_t c = (uint32_t)(idx & ((1ull << N) - 1));
 #pragma unroll
             for (int j = 0; j < N; j++) {
                 const bool up = (c >> (N - 1 - j)) & 1u;
-                const double* q = s_par + 3 * (lp * N + j) + (up ? 1 : 0);
+                const double* q = par + 3 * (lp * N + j) + (up ? 1 : 0);
                 xs2[j * stride] = make_double2(q[0], q[1]);
             }
             const bool sample = (blockIdx.x & 3) == 0;  // statistics from a quarter of the blocks
@@ -1230,6 +1257,146 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
     }
 }
 
+// K1'' warp-tabulated filter: the tables of k_filter_tab, one warp per parent (n >= 5:
+// 2^n / 32 children per lane).  The warp stages its parent, builds equation e's table
+// (entries over the 32 lanes) only while one of its children is alive, and sums the
+// table entries for its live children: no block barrier, and the 8 warps of a block
+// work on 8 parents independently.  Same term values and summation order as
+// k_filter / k_filter_tab (bit-identical); survivors compacted per child bit.
+template <int N>
+__host__ __device__ inline int fwt_warp_doubles(const TabMeta& m) {
+    return ((3 * N + 1 + 1) & ~1) + 2 * m.e_max;  // parent (lo, hi, mid, exact) + table (double2)
+}
+template <int N>
+__host__ __device__ inline int fwt_smem_bytes(const TabMeta& m, int threads) {
+    return ftab_off_sp<N>(m) + (threads / 32) * fwt_warp_doubles<N>(m) * 8;
+}
+
+template <int N, class EV = TabEval>
+__global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
+                                                   const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
+                                                   int64_t* tags, const int* __restrict__ eq_order, int64_t pcount) {
+    pdl_enter();
+    if constexpr (N >= 5 && N <= 10) {
+        constexpr int K = (1 << N) / 32;  // children per lane: c = 32 i + lane
+        __shared__ int s_order[16];
+        __shared__ unsigned s_eval[16], s_rej[16];
+        if (threadIdx.x < 16) {
+            s_order[threadIdx.x] = (eq_order && threadIdx.x < N) ? eq_order[threadIdx.x] : (int)threadIdx.x;
+            s_eval[threadIdx.x] = 0;
+            s_rej[threadIdx.x] = 0;
+        }
+        extern __shared__ __align__(16) uint8_t smem[];
+        const STab tab = issue_stab(meta, gtab, smem, true);
+        uint8_t* p8 = smem + stab_bytes(meta, true);
+        uint16_t* tbase = reinterpret_cast<uint16_t*>(p8);
+        uint16_t* ent_off = reinterpret_cast<uint16_t*>(p8 + align8(2 * meta.TF));
+        uint32_t* ent = reinterpret_cast<uint32_t*>(p8 + align8(2 * meta.TF) + align8(2 * (N + 1)));
+        copy_async<4>(tbase, gtab + meta.off_tbase, 2 * meta.TF);
+        copy_async<4>(ent_off, gtab + meta.off_ent_off, 2 * (N + 1));
+        copy_async<4>(ent, gtab + meta.off_ent, 4 * meta.ent_total);
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        double* sp = reinterpret_cast<double*>(smem + ftab_off_sp<N>(meta)) + wid * fwt_warp_doubles<N>(meta);
+        double2* table = reinterpret_cast<double2*>(sp + ((3 * N + 1 + 1) & ~1));
+        const unsigned long long n_par = pcount >= 0 ? (unsigned long long)pcount : ctr->n_par;
+        cp_async_wait();
+        __syncthreads();
+        unsigned long long ops_acc = 0, exact_acc = 0;
+        for (unsigned long long pidx = (unsigned long long)blockIdx.x * nw + wid; pidx < n_par;
+             pidx += (unsigned long long)gridDim.x * nw) {
+            __syncwarp();  // the previous parent's children are done with sp / table
+            if (lane < N) {
+                const uint32_t pe = parents[pidx];
+                const uint32_t row = pe & 0x7fffffffu;
+                const double lo = cur.lo[lane * cur.cap + row], hi = cur.hi[lane * cur.cap + row];
+                sp[lane] = lo;
+                sp[N + lane] = hi;
+                sp[2 * N + lane] = mid_of(lo, hi);
+                if (lane == 0) sp[3 * N] = (pe >> 31) ? 1.0 : 0.0;
+            }
+            __syncwarp();
+            const bool exact = sp[3 * N] != 0.0;
+            uint32_t alive = K >= 32 ? 0xffffffffu : ((1u << K) - 1u);
+            unsigned ops = 0;
+#pragma unroll 1
+            for (int k = 0; k < N; k++) {
+                if (__ballot_sync(0xffffffffu, alive != 0) == 0) break;
+                const int e = s_order[k];
+                const int e0 = ent_off[e], E = ent_off[e + 1] - e0;
+                for (int i = lane; i < E; i += 32) {
+                    const uint32_t en = ent[e0 + i];
+                    const ival v = exact ? term_value_exact(tab, en & 0xffff, en >> 16, sp, sp + N, sp + 2 * N)
+                                         : term_value<RB_FILTER_FAST>(tab, en & 0xffff, en >> 16, sp, sp + N, sp + 2 * N);
+                    table[i] = make_double2(v.lo, v.hi);
+                }
+                __syncwarp();
+                unsigned ne = 0, nr = 0;
+#pragma unroll
+                for (int i = 0; i < K; i++) {
+                    if ((alive >> i) & 1u) {
+                        const uint32_t c = (uint32_t)(32 * i + lane);
+                        const ival acc = exact ? EV::template tsum<N, Exact>(tab, tbase, e, c, table)
+                                               : EV::template tsum<N, Fast>(tab, tbase, e, c, table);
+                        ne++;
+                        if (!(acc.lo <= 0.0 && 0.0 <= acc.hi)) {
+                            alive &= ~(1u << i);
+                            nr++;
+                        }
+                    }
+                }
+                ops += ne * (unsigned)meta.ops_eq[e];
+                ne = __reduce_add_sync(0xffffffffu, ne);
+                nr = __reduce_add_sync(0xffffffffu, nr);
+                if (lane == 0) {
+                    atomicAdd(&s_eval[e], ne);
+                    if (nr) atomicAdd(&s_rej[e], nr);
+                }
+                __syncwarp();  // the table is rebuilt for the next equation
+            }
+            ops_acc += ops;
+            if (lane == 0 && exact) exact_acc += 1u << N;
+            // survivors -> S, one child bit at a time (ballot + one atomic per non-empty bit)
+            double w = 0.0;
+#pragma unroll 1
+            for (int i = 0; i < K; i++) {
+                if (__ballot_sync(0xffffffffu, alive != 0) == 0) break;
+                const bool keep = (alive >> i) & 1u;
+                const unsigned long long slot = warp_append(keep, &ctr->n_surv);
+                if (keep) {
+                    const uint32_t c = (uint32_t)(32 * i + lane);
+#pragma unroll
+                    for (int j = 0; j < N; j++) {
+                        const bool up = (c >> (N - 1 - j)) & 1u;
+                        const double cl = up ? sp[2 * N + j] : sp[j];
+                        const double ch = up ? sp[N + j] : sp[2 * N + j];
+                        const double d = __dsub_rn(ch, cl);
+                        w = (d > w) ? d : w;
+                        if (slot < (unsigned long long)S.cap) {
+                            S.lo[j * S.cap + slot] = cl;
+                            S.hi[j * S.cap + slot] = ch;
+                        }
+                    }
+                    if (tags && slot < (unsigned long long)S.cap) tags[slot] = (int64_t)((pidx << N) | c);
+                }
+                alive &= ~(1u << i);
+            }
+            unsigned long long wb = (unsigned long long)__double_as_longlong(w);
+            wb = warp_max(wb);
+            if (lane == 0 && wb) atomicMax(&ctr->child_wmax, wb);
+        }
+        ops_acc = warp_sum(ops_acc);
+        if (lane == 0) {
+            if (ops_acc) atomicAdd(&ctr->filter_ops, ops_acc);
+            if (exact_acc) atomicAdd(&ctr->exact_boxes, exact_acc);
+        }
+        __syncthreads();
+        if (threadIdx.x < N) {
+            if (s_eval[threadIdx.x]) atomicAdd(&ctr->f_eval[threadIdx.x], (unsigned long long)s_eval[threadIdx.x]);
+            if (s_rej[threadIdx.x]) atomicAdd(&ctr->f_rej[threadIdx.x], (unsigned long long)s_rej[threadIdx.x]);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ K2 Hansen-Sengupta
 //
 // hansen.contract (hansen.py:56-138) over a batch of boxes as a three-kernel
@@ -1494,6 +1661,14 @@ __device__ __forceinline__ ival pmul_sign(double a, ival y) {
 #ifndef RB_PMUL_SIGN_MIN_N
 #define RB_PMUL_SIGN_MIN_N 9  // sign-bit point products from this n up (A/B: tools/hs_bench.py)
 #endif
+// The thread-per-box products (lin_products_acc: k_hs_lin_tps / tpb, n <= 8) take the
+// sign-bit form at every n (brown8 HS 23.8 -> 21.9 ms, katsura6 10.6 -> 10.3 ms); an L1
+// prefetch of the next J column there measured slower (brown8 HS 24.4 ms).
+template <class A>
+__device__ __forceinline__ ival pmul_tpb(double a, ival y) {
+    if constexpr (A::exact) return A::mul_point(a, y);
+    else return pmul_sign(a, y);
+}
 template <class A, int N>
 __device__ __forceinline__ ival pmul(double a, ival y) {
     if constexpr (A::exact) return A::mul_point(a, y);
@@ -1774,7 +1949,7 @@ __device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int
         for (int i = 0; i < N; i++) {
             ival acc = mk(0.0, 0.0);
 #pragma unroll
-            for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A, N>(am(i, u), jc[u]));
+            for (int u = 0; u < N; u++) acc = A::add(acc, pmul_tpb<A>(am(i, u), jc[u]));
             W.jl[(i * N + j) * W.B + t] = acc.lo;
             W.jh[(i * N + j) * W.B + t] = acc.hi;
         }
@@ -1787,7 +1962,7 @@ __device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int
     for (int i = 0; i < N; i++) {
         ival acc = mk(0.0, 0.0);
 #pragma unroll
-        for (int u = 0; u < N; u++) acc = A::add(acc, pmul<A, N>(am(i, u), fx[u]));
+        for (int u = 0; u < N; u++) acc = A::add(acc, pmul_tpb<A>(am(i, u), fx[u]));
         W.fl[i * W.B + t] = acc.lo;
         W.fh[i * W.B + t] = acc.hi;
     }

@@ -93,8 +93,9 @@ def _set_codegen(eng, on):
     eng.set_option("codegen", int(on))
 
 
-@pytest.mark.parametrize("mode,codegen", [(1, 0), (0, 0), (0, 1), (1, 1)],
-                         ids=["tabulated", "direct_tables", "direct_specialised", "tabulated_specialised"])
+@pytest.mark.parametrize("mode,codegen", [(1, 0), (0, 0), (0, 1), (1, 1), (2, 0), (2, 1)],
+                         ids=["tabulated", "direct_tables", "direct_specialised", "tabulated_specialised",
+                              "warp_tabulated", "warp_tabulated_specialised"])
 @pytest.mark.parametrize("name", FILTER_SYSTEMS)
 def test_filter_random_cells_vs_oracle(native, name, mode, codegen):
     spec = golden_spec(name)
@@ -102,7 +103,8 @@ def test_filter_random_cells_vs_oracle(native, name, mode, codegen):
     from paper_1802_00330_b200.system import compile_tables
     eng = _native.Engine(compile_tables(spec), 0)
     _set_codegen(eng, codegen)
-    eng.set_option("filter_tab", mode)
+    eng.set_option("filter_tab", int(mode == 1))
+    eng.set_option("filter_wt", int(mode == 2))  # k_filter_wt where 5 <= n <= 10, else the direct filter
     osys = oracle_sys(name)
     for depth, seed in ((1, 1), (3, 2), (7, 3), (30, 4)):
         P = max(1, min(2048, (1 << 16) >> spec.n))
@@ -291,6 +293,26 @@ def test_solve_host_loop_tabulated_specialised_filter(native, case):
     finally:
         eng.set_option("graph", 1)
         eng.set_option("filter_tab", 0)
+    check_against_golden(case, out, meta)
+
+
+@pytest.mark.parametrize("codegen", [0, 1], ids=["tables", "specialised"])
+@pytest.mark.parametrize("case", solve_cases())
+def test_solve_host_loop_warp_tabulated_filter(native, case, codegen):
+    """Host-driven rounds with the warp-tabulated filter forced on (k_filter_wt, 5 <= n <= 10)."""
+    from paper_1802_00330_b200 import bnb
+    meta = load_solve(case)
+    spec = golden_spec(meta["system"])
+    eng = bnb.engine_for(spec)
+    _set_codegen(eng, codegen)
+    eng.set_option("graph", 0)
+    eng.set_option("filter_wt", 1)
+    try:
+        out = eng.solve(bnb.native_config(bnb.SolverConfig(**meta["config"])))
+    finally:
+        eng.set_option("graph", 1)
+        eng.set_option("filter_wt", -1)
+        eng.set_option("codegen", 1)
     check_against_golden(case, out, meta)
 
 

@@ -54,4 +54,4 @@ def test_codegen_prepare_without_gpu(tmp_path, monkeypatch):
     files = sorted(os.listdir(tmp_path))
     assert files == sorted([f"{k1}.cubin", f"{k1}.names", f"{k3}.cubin", f"{k3}.names"])
     names = (tmp_path / f"{k1}.names").read_text().split()
-    assert len(names) == 6 and all("GenEval" in n or "rbg" in n for n in names)
+    assert len(names) == 7 and all("GenEval" in n or "rbg" in n for n in names)
