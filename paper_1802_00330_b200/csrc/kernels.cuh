@@ -1928,7 +1928,7 @@ __global__ void __launch_bounds__(128, RB_LIN_MINB) k_hs_lin(SBuf S, int64_t n_i
 // the skipped ones act on exact zeros / ones of the identity half (x - f*0 = x,
 // 1 * inv = inv, 0 - f*inv = -(f*inv)), so the inverse is bit-identical (zero signs
 // aside, which no later operation can observe).  Row swaps are predicated selects.
-template <int N, class A, class AM>
+template <int N, class A, class AM, int IU = N>
 __device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int64_t t);
 
 template <int N, class A>
@@ -1936,8 +1936,9 @@ __device__ __forceinline__ void lin_products_reg(const double (&a)[N][N], HsScra
     lin_products_acc<N, A>([&](int i, int u) { return a[i][u]; }, W, t);
 }
 
-// M = A J and g = A F(x) with A given by an accessor am(i, u)
-template <int N, class A, class AM>
+// M = A J and g = A F(x) with A given by an accessor am(i, u); IU = unrolling of the row
+// loop (N for A in registers; small for A in shared memory, bounding the loads in flight)
+template <int N, class A, class AM, int IU>
 __device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int64_t t) {
     // M = A J, column by column in place (linalg.py:102-114), u ascending
 #pragma unroll 1
@@ -1945,7 +1946,7 @@ __device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int
         ival jc[N];
 #pragma unroll
         for (int u = 0; u < N; u++) jc[u] = mk(W.jl[(u * N + j) * W.B + t], W.jh[(u * N + j) * W.B + t]);
-#pragma unroll
+#pragma unroll IU
         for (int i = 0; i < N; i++) {
             ival acc = mk(0.0, 0.0);
 #pragma unroll
@@ -2105,17 +2106,36 @@ __global__ void __launch_bounds__(128, RB_LIN_REG_MINB) k_hs_lin_tpb(SBuf S, int
     }
 }
 
+__device__ __forceinline__ double lds_volatile(const double* p) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+
+template <int N>
+static __device__ __noinline__ void lin_products_tps_exact(const double* C, HsScratch W, int64_t t) {
+    lin_products_acc<N, Exact>([&](int i, int u) { return C[(i * N + u) * 128]; }, W, t);
+}
+
 // k_hs_lin_tpb with the in-place tableau in shared memory (this thread's column:
 // element (i, s) at C[(i * n + s) * T], conflict-free) instead of registers: n^2 doubles
 // per thread, so more threads stay resident and no register limit is reached at n = 8.
 // Same operations in the same order; the row swap and the unscrambling index memory.
-template <int N>
 #ifndef RB_TPS_MINB7
 #define RB_TPS_MINB7 4
 #endif
 #ifndef RB_TPS_MINB8
 #define RB_TPS_MINB8 3
 #endif
+#ifndef RB_TPS_MID_UNROLL
+#define RB_TPS_MID_UNROLL 1
+#endif
+constexpr int kTpsMidUnroll = RB_TPS_MID_UNROLL;
+#ifndef RB_TPS_ROW_UNROLL
+#define RB_TPS_ROW_UNROLL 1
+#endif
+constexpr int kTpsRowUnroll = RB_TPS_ROW_UNROLL;
+template <int N>
 __global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k_hs_lin_tps(SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
                                                     Counters* ctr) {
     pdl_enter();
@@ -2124,7 +2144,7 @@ __global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
     if (n_in < 0 || !hs_on || n_in <= prm.fused_max) return;
     const int64_t b_end = min(n_in, b0 + W.B);
-    const int T = blockDim.x;
+    constexpr int T = 128;  // launched with 128 threads: tableau offsets are immediates
     double* C = reinterpret_cast<double*>(smem) + threadIdx.x;
     auto c = [&](int i, int s2) -> double& { return C[(i * N + s2) * T]; };
     for (int64_t b = b0 + (int64_t)blockIdx.x * T + threadIdx.x; b < b_end; b += (int64_t)gridDim.x * T) {
@@ -2134,7 +2154,7 @@ __global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k
         ra.init();
         rf.init();
         double scale = 0.0;
-#pragma unroll
+#pragma unroll kTpsMidUnroll  // a row of J per step: full unrolling hoisted every load and spilled
         for (int i = 0; i < N; i++)
 #pragma unroll
             for (int j = 0; j < N; j++) {
@@ -2194,18 +2214,19 @@ __global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k
         if (singular) {
             fl = HSF_SINGULAR;
         } else {
-            int slot[N];  // slot[u] = s with e_s = u (unrolled: registers)
+            // unscramble in place, row by row: slot s holds A[i][e_s] (a permutation), so the
+            // products read A at fixed offsets
+#pragma unroll 1
+            for (int i = 0; i < N; i++) {
+                double row[N];
 #pragma unroll
-            for (int u = 0; u < N; u++) {
-                slot[u] = 0;
+                for (int s2 = 0; s2 < N; s2++) row[s2] = c(i, s2);
 #pragma unroll
-                for (int s2 = 0; s2 < N; s2++)
-                    if (((label >> (4 * s2)) & 15u) == (uint32_t)u) slot[u] = s2;
+                for (int s2 = 0; s2 < N; s2++) {
+                    c(i, (int)((label >> (4 * s2)) & 15u)) = row[s2];
+                    ra.add(row[s2]);
+                }
             }
-#pragma unroll
-            for (int i = 0; i < N; i++)
-#pragma unroll
-                for (int u = 0; u < N; u++) ra.add(c(i, u));  // same values, another order
 #pragma unroll
             for (int u = 0; u < N; u++) {
                 rf.add(W.fl[u * W.B + t]);
@@ -2214,14 +2235,12 @@ __global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k
             rj.emin = min(rj.emin, rf.emin);
             rj.emax = max(rj.emax, rf.emax);
             if (!prm.force_exact && prod_guard_ok(ra, rj)) {
-                lin_products_acc<N, Fast>([&](int i, int u) { return c(i, slot[u]); }, W, t);
-            } else {
-                double ax[N][N];
-#pragma unroll
-                for (int i = 0; i < N; i++)
-#pragma unroll
-                    for (int u = 0; u < N; u++) ax[i][u] = c(i, slot[u]);
-                lin_products_reg_exact<N>(ax, W, t);
+                auto am_tps = [&](int i, int u) { return lds_volatile(&c(i, u)); };
+                // volatile shared loads: kept inside the column loop (hoisting all n^2 of A out
+                // of it is what spilled)
+                lin_products_acc<N, Fast, decltype(am_tps), kTpsRowUnroll>(am_tps, W, t);
+            } else {  // rare: out of line, A read from the tableau (no local copy in this frame)
+                lin_products_tps_exact<N>(C, W, t);
                 fl = HSF_EXACT_LIN;
             }
         }
