@@ -1519,8 +1519,11 @@ __device__ void hs_passthrough(const SBuf& S, int64_t n_in, const Front& out, Co
 
 // K2a: thread per box.  Rows [b0, b0 + B) of S.  When HS is off for this round the
 // first batch launch copies S into F_next instead (bnb.py:580-581).
+#ifndef RB_EVAL_MINB
+#define RB_EVAL_MINB 1  // k_hs_eval min blocks per SM (register cap)
+#endif
 template <int N, class EV = TabEval>
-__global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
+__global__ void __launch_bounds__(128, RB_EVAL_MINB) k_hs_eval(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
                                                  int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
                                                  Front out, Counters* ctr, int64_t* tags, int R) {
     pdl_enter();
@@ -1550,10 +1553,8 @@ __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __
     const int64_t nb = b_end - b0;
     const int64_t items = nb * R;
     unsigned long long exact_acc = 0;
-    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = it % nb;
-        const int r = (int)(it / nb);
-        const int64_t b = b0 + t;
+    // stage box b (components at xlo / xhi / xmid [j * stride]); guards of J(X) and F(x)
+    auto stage = [&](int64_t b, int64_t t, bool write_x, bool& fastJ, bool& fastF) {
         ExpRange rx, rm;
         rx.init();
         rm.init();
@@ -1564,18 +1565,30 @@ __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __
             xlo[j * stride] = lo;
             xhi[j * stride] = hi;
             xmid[j * stride] = m;
-            if (r == 0) W.x[j * W.B + t] = m;
+            if (write_x) W.x[j * W.B + t] = m;
             rx.add(lo);
             rx.add(hi);
             rm.add(m);
         }
-        const bool fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
-        const bool fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
+        fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
+        fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
+    };
+    bool deferred = false;
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = it % nb;
+        const int r = (int)(it / nb);
+        const int64_t b = b0 + t;
+        bool fastJ, fastF;
+        stage(b, t, r == 0, fastJ, fastF);
         if constexpr (EV::whole_box) {  // specialised evaluator: all of J(X) and F(x) by this thread (R = 1)
-            if (fastJ) EV::template J<Fast>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
-            else EV::template J<Exact>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
-            if (fastF) EV::template F<Fast>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
-            else EV::template F<Exact>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
+            // a box needing the Exact policy is evaluated after the loop: no out-of-line call
+            // in the hot loop (its calling convention spilled the loop state to the stack)
+            if (fastJ && fastF) {
+                EV::template J<Fast>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
+                EV::template F<Fast>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
+            } else {
+                deferred = true;
+            }
         }
         const int p0 = EV::whole_box ? P : (int)((int64_t)r * P / R), p1 = (int)((int64_t)(r + 1) * P / R);
 #pragma unroll 1
@@ -1599,6 +1612,19 @@ __global__ void __launch_bounds__(128) k_hs_eval(TabMeta meta, const uint8_t* __
             const bool ex = !(fastJ && fastF);
             W.flags[t] = ex ? HSF_EXACT_EVAL : 0;
             exact_acc += ex;
+        }
+    }
+    if constexpr (EV::whole_box) {
+        if (__syncthreads_or(deferred)) {  // rare: this block's Exact-policy boxes (R = 1: t = it)
+            for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += (int64_t)gridDim.x * blockDim.x) {
+                if (!(W.flags[t] & HSF_EXACT_EVAL)) continue;
+                bool fastJ, fastF;
+                stage(b0 + t, t, false, fastJ, fastF);
+                if (fastJ) EV::template J<Fast>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
+                else EV::template J<Exact>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
+                if (fastF) EV::template F<Fast>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
+                else EV::template F<Exact>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
+            }
         }
     }
     exact_acc = warp_sum(exact_acc);
