@@ -672,6 +672,11 @@ struct TabEval {
     __device__ __forceinline__ static ival feq(const TermP* tp, const STab& t, int e, const double2* xs2, int stride) {
         return A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride) : eval_poly_packed<A>(tp, t, e, xs2, stride);
     }
+    // k_filter_wt: f(sum) with sum(c, tb) = tsum of equation e (selected once)
+    template <int N, class A, class F>
+    __device__ __forceinline__ static void with_tsum(const STab& t, const uint16_t* tbase, int e, F&& f) {
+        f([&](uint32_t c, const double2* tb) { return tsum<N, A>(t, tbase, e, c, tb); });
+    }
     // k_filter_tab: equation e of child c as the canonical-order sum of its terms' table
     // entries tb[tbase[q] + combo], combo = the child's half bits of the term's factors
     template <int N, class A>
@@ -1330,26 +1335,38 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
                     table[i] = make_double2(v.lo, v.hi);
                 }
                 __syncwarp();
-                unsigned ne = 0, nr = 0;
+                const uint32_t before = alive;
+                // the equation's sum is selected once (not per child); with every child of the
+                // lane alive the K sums are independent chains, evaluated without branches
+                auto sweep = [&](auto fts) {
+                    if (alive == (K >= 32 ? 0xffffffffu : ((1u << K) - 1u))) {
+                        uint32_t keep = 0;
 #pragma unroll
-                for (int i = 0; i < K; i++) {
-                    if ((alive >> i) & 1u) {
-                        const uint32_t c = (uint32_t)(32 * i + lane);
-                        const ival acc = exact ? EV::template tsum<N, Exact>(tab, tbase, e, c, table)
-                                               : EV::template tsum<N, Fast>(tab, tbase, e, c, table);
-                        ne++;
-                        if (!(acc.lo <= 0.0 && 0.0 <= acc.hi)) {
-                            alive &= ~(1u << i);
-                            nr++;
+                        for (int i = 0; i < K; i++) {
+                            const ival acc = fts((uint32_t)(32 * i + lane), table);
+                            keep |= (uint32_t)(acc.lo <= 0.0 && 0.0 <= acc.hi) << i;
+                        }
+                        alive = keep;
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < K; i++) {
+                            if ((alive >> i) & 1u) {
+                                const ival acc = fts((uint32_t)(32 * i + lane), table);
+                                if (!(acc.lo <= 0.0 && 0.0 <= acc.hi)) alive &= ~(1u << i);
+                            }
                         }
                     }
-                }
+                };
+                if (exact) EV::template with_tsum<N, Exact>(tab, tbase, e, sweep);
+                else EV::template with_tsum<N, Fast>(tab, tbase, e, sweep);
+                const unsigned ne = (unsigned)__popc(before), nr = ne - (unsigned)__popc(alive);
                 ops += ne * (unsigned)meta.ops_eq[e];
-                ne = __reduce_add_sync(0xffffffffu, ne);
-                nr = __reduce_add_sync(0xffffffffu, nr);
-                if (lane == 0) {
-                    atomicAdd(&s_eval[e], ne);
-                    if (nr) atomicAdd(&s_rej[e], nr);
+                if ((blockIdx.x & 3) == 0) {  // statistics from a quarter of the blocks (as k_filter)
+                    const unsigned se = __reduce_add_sync(0xffffffffu, ne), sr = __reduce_add_sync(0xffffffffu, nr);
+                    if (lane == 0) {
+                        atomicAdd(&s_eval[e], se);
+                        if (sr) atomicAdd(&s_rej[e], sr);
+                    }
                 }
                 __syncwarp();  // the table is rebuilt for the next equation
             }
@@ -2138,21 +2155,40 @@ __device__ __forceinline__ double lds_volatile(const double* p) {
     return v;
 }
 
+template <bool B, class T, class F>
+struct pick_t {
+    using type = T;
+};
+template <class T, class F>
+struct pick_t<false, T, F> {
+    using type = F;
+};
+#ifndef RB_TPS_MINB7
+#define RB_TPS_MINB7 4
+#endif
+#ifndef RB_TPS_MINB12
+#define RB_TPS_MINB12 3
+#endif
+#ifndef RB_TPS_MINB8
+#define RB_TPS_MINB8 3
+#endif
+// k_hs_lin_tps shape: n^2 doubles of shared memory per thread; 128 threads per block up to
+// n = 8, 64 above (n = 12: 72 KB per block, 3 blocks per SM)
+template <int N>
+struct TpsShape {
+    static constexpr int T = N <= 8 ? 128 : 64;
+    static constexpr int MINB = N <= 7 ? RB_TPS_MINB7 : (N <= 8 ? RB_TPS_MINB8 : RB_TPS_MINB12);
+    using Lbl = typename pick_t<(N > 8), unsigned long long, uint32_t>::type;
+};
 template <int N>
 static __device__ __noinline__ void lin_products_tps_exact(const double* C, HsScratch W, int64_t t) {
-    lin_products_acc<N, Exact>([&](int i, int u) { return C[(i * N + u) * 128]; }, W, t);
+    lin_products_acc<N, Exact>([&](int i, int u) { return C[(i * N + u) * TpsShape<N>::T]; }, W, t);
 }
 
 // k_hs_lin_tpb with the in-place tableau in shared memory (this thread's column:
 // element (i, s) at C[(i * n + s) * T], conflict-free) instead of registers: n^2 doubles
 // per thread, so more threads stay resident and no register limit is reached at n = 8.
 // Same operations in the same order; the row swap and the unscrambling index memory.
-#ifndef RB_TPS_MINB7
-#define RB_TPS_MINB7 4
-#endif
-#ifndef RB_TPS_MINB8
-#define RB_TPS_MINB8 3
-#endif
 #ifndef RB_TPS_MID_UNROLL
 #define RB_TPS_MID_UNROLL 1
 #endif
@@ -2162,7 +2198,7 @@ constexpr int kTpsMidUnroll = RB_TPS_MID_UNROLL;
 #endif
 constexpr int kTpsRowUnroll = RB_TPS_ROW_UNROLL;
 template <int N>
-__global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k_hs_lin_tps(SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
+__global__ void __launch_bounds__(TpsShape<N>::T, TpsShape<N>::MINB) k_hs_lin_tps(SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
                                                     Counters* ctr) {
     pdl_enter();
     extern __shared__ __align__(16) uint8_t smem[];
@@ -2170,7 +2206,7 @@ __global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k
     const int64_t n_in = hs_count(prm, ctr, n_in_arg, S.cap, hs_on);
     if (n_in < 0 || !hs_on || n_in <= prm.fused_max) return;
     const int64_t b_end = min(n_in, b0 + W.B);
-    constexpr int T = 128;  // launched with 128 threads: tableau offsets are immediates
+    constexpr int T = TpsShape<N>::T;  // the launch's block size: tableau offsets are immediates
     double* C = reinterpret_cast<double*>(smem) + threadIdx.x;
     auto c = [&](int i, int s2) -> double& { return C[(i * N + s2) * T]; };
     for (int64_t b = b0 + (int64_t)blockIdx.x * T + threadIdx.x; b < b_end; b += (int64_t)gridDim.x * T) {
@@ -2193,9 +2229,10 @@ __global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k
             }
         bool singular = scale == 0.0;
         const double threshold = __dmul_rn(1e-12, scale);
-        uint32_t orig = 0, label = 0;
+        using Lbl = typename TpsShape<N>::Lbl;  // 4-bit fields: n <= 8 in 32 bits, else 64
+        Lbl orig = 0, label = 0;
 #pragma unroll
-        for (int r = 0; r < N; r++) orig |= (uint32_t)r << (4 * r);
+        for (int r = 0; r < N; r++) orig |= (Lbl)r << (4 * r);
 #pragma unroll
         for (int k = 0; k < N; k++) {
             int pr = k;
@@ -2211,8 +2248,8 @@ __global__ void __launch_bounds__(128, (N <= 7 ? RB_TPS_MINB7 : RB_TPS_MINB8)) k
             }
             singular = singular || fabs(pv) < threshold;
             if (!singular) {
-                const uint32_t ok = (orig >> (4 * k)) & 15u, op = (orig >> (4 * pr)) & 15u;
-                orig = (orig & ~((15u << (4 * k)) | (15u << (4 * pr)))) | (op << (4 * k)) | (ok << (4 * pr));
+                const Lbl ok = (orig >> (4 * k)) & 15u, op = (orig >> (4 * pr)) & 15u;
+                orig = (orig & ~(((Lbl)15 << (4 * k)) | ((Lbl)15 << (4 * pr)))) | (op << (4 * k)) | (ok << (4 * pr));
                 label |= op << (4 * k);
                 const double inv = __drcp_rn(pv);  // RN(1/pivot) == 1.0 / pivot (linalg.py:162)
                 double rowk[N];

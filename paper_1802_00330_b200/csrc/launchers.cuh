@@ -48,9 +48,13 @@ void SetupK<N>::run(rb_handle* h) {
         h->lin_tpb_threads = 128;
         h->lin_tpb_smem = 0;
         h->lin_tpb_bps = std::max(1, nb);
+    }
+    if constexpr (N <= 12) {  // thread-per-box Gauss-Jordan with the tableau in shared memory
+        int nb = 0;
         set_max_dyn_smem(k_hs_lin_tps<N>, h->smem_optin);
-        h->lin_tps_smem = (size_t)N * N * 128 * sizeof(double);
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_lin_tps<N>, 128, h->lin_tps_smem), "occ lin tps");
+        h->lin_tps_smem = (size_t)N * N * TpsShape<N>::T * sizeof(double);
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_lin_tps<N>, TpsShape<N>::T, h->lin_tps_smem),
+           "occ lin tps");
         h->lin_tps_bps = std::max(1, nb);
     }
     choose_tile(h, k_hs_tile<N>, N, stab_bytes(h->meta, false), h->tile_tb, h->tile_smem, h->tile_bps);
@@ -183,9 +187,13 @@ void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* 
             const int tl = h->lin_tpb_threads;
             klaunch(h, k_hs_lin_tpb<N>, grid_for(bound, tl, h->sms * h->lin_tpb_bps), tl, h->lin_tpb_smem, h->S, n_in,
                     b0, prm, h->W, h->d_ctr);
-        } else if (h->lin_tpb == 2) {
+        }
+    }
+    if constexpr (N <= 12) {
+        if (!tpb && h->lin_tpb == 2) {
             tpb = true;
-            klaunch(h, k_hs_lin_tps<N>, grid_for(bound, 128, h->sms * h->lin_tps_bps), 128, h->lin_tps_smem, h->S,
+            constexpr int TT = TpsShape<N>::T;
+            klaunch(h, k_hs_lin_tps<N>, grid_for(bound, TT, h->sms * h->lin_tps_bps), TT, h->lin_tps_smem, h->S,
                     n_in, b0, prm, h->W, h->d_ctr);
         }
     }
