@@ -233,9 +233,10 @@ int64_t rb_kernel_launches(rb_handle* h);
  *   "filter_tab"  1: tabulated per-parent term filter (k_filter_tab, a block per
  *                 parent) when the tables fit; 0: direct per-child evaluation (k_filter).
  *                 Default: on for n >= 10 (2^n >= 1024 children per parent).
- *   "filter_wt"   1: warp-tabulated filter (k_filter_wt, a warp per parent, 5 <= n <= 10),
+ *   "filter_wt"   1: warp-tabulated filter (k_filter_wt, a warp per parent or per 1024 of its
+ *                 children, 5 <= n <= 16),
  *                 ahead of "filter_tab"; 0: off; -1: the default, on when every
- *                 equation's table has at most 2^(n-2) entries.
+ *                 equation's table has at most 2^(min(n, 10) - 2) entries.
  *   "force_exact" 0 (default): exponent guards pick IEEE directed rounding wherever it
  *                 provably equals the reference; 1: every guard fails, so every box
  *                 runs the Exact policy (the reference's error-free transformations,

@@ -2156,7 +2156,7 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
         h->use_ftab = value != 0;
         return RB_OK;
     }
-    if (k == "filter_wt") {  // warp-tabulated filter where it applies (5 <= n <= 10, tables fit); -1: auto
+    if (k == "filter_wt") {  // warp-tabulated filter where it applies (5 <= n <= 16, tables fit); -1: auto
         h->use_fwt = value < 0 ? h->fwt_auto : value != 0;
         return RB_OK;
     }

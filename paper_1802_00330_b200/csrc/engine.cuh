@@ -183,7 +183,7 @@ struct rb_handle {
     size_t filter_smem = 0, eval_smem = 0, lin_smem = 0, sweep_smem = 0, ftab_smem = 0;
     int ftab_blocks_per_sm = 1;
     bool use_ftab = true;
-    // warp-tabulated filter (k_filter_wt, 5 <= n <= 10): shared memory, blocks per SM (table / specialised)
+    // warp-tabulated filter (k_filter_wt, 5 <= n <= 16): shared memory, blocks per SM (table / specialised)
     bool use_fwt = false, fwt_auto = false;
     size_t fwt_smem = 0;
     int fwt_bps = 0, gen_fwt_bps = 0;

@@ -1282,8 +1282,11 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
                                                    const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
                                                    int64_t* tags, const int* __restrict__ eq_order, int64_t pcount) {
     pdl_enter();
-    if constexpr (N >= 5 && N <= 10) {
-        constexpr int K = (1 << N) / 32;  // children per lane: c = 32 i + lane
+    if constexpr (N >= 5 && N <= 16) {
+        // a work unit = one parent's 32 K children: K = 2^n / 32 up to n = 10, above that
+        // a parent is CH units of 1024 children (each unit builds the tables it needs)
+        constexpr int K = N <= 10 ? (1 << N) / 32 : 32;  // children per lane: c = c0 + 32 i + lane
+        constexpr int CHLOG = N <= 10 ? 0 : N - 10;
         __shared__ int s_order[16];
         __shared__ unsigned s_eval[16], s_rej[16];
         if (threadIdx.x < 16) {
@@ -1307,9 +1310,12 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
         cp_async_wait();
         __syncthreads();
         unsigned long long ops_acc = 0, exact_acc = 0;
-        for (unsigned long long pidx = (unsigned long long)blockIdx.x * nw + wid; pidx < n_par;
-             pidx += (unsigned long long)gridDim.x * nw) {
-            __syncwarp();  // the previous parent's children are done with sp / table
+        const unsigned long long units = n_par << CHLOG;
+        for (unsigned long long unit = (unsigned long long)blockIdx.x * nw + wid; unit < units;
+             unit += (unsigned long long)gridDim.x * nw) {
+            const unsigned long long pidx = unit >> CHLOG;
+            const uint32_t c0 = (uint32_t)(unit & ((1ull << CHLOG) - 1)) << 10;
+            __syncwarp();  // the previous unit's children are done with sp / table
             if (lane < N) {
                 const uint32_t pe = parents[pidx];
                 const uint32_t row = pe & 0x7fffffffu;
@@ -1343,7 +1349,7 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
                         uint32_t keep = 0;
 #pragma unroll
                         for (int i = 0; i < K; i++) {
-                            const ival acc = fts((uint32_t)(32 * i + lane), table);
+                            const ival acc = fts(c0 + (uint32_t)(32 * i + lane), table);
                             keep |= (uint32_t)(acc.lo <= 0.0 && 0.0 <= acc.hi) << i;
                         }
                         alive = keep;
@@ -1351,7 +1357,7 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
 #pragma unroll
                         for (int i = 0; i < K; i++) {
                             if ((alive >> i) & 1u) {
-                                const ival acc = fts((uint32_t)(32 * i + lane), table);
+                                const ival acc = fts(c0 + (uint32_t)(32 * i + lane), table);
                                 if (!(acc.lo <= 0.0 && 0.0 <= acc.hi)) alive &= ~(1u << i);
                             }
                         }
@@ -1371,7 +1377,7 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
                 __syncwarp();  // the table is rebuilt for the next equation
             }
             ops_acc += ops;
-            if (lane == 0 && exact) exact_acc += 1u << N;
+            if (lane == 0 && exact) exact_acc += 32u * K;
             // survivors -> S, one child bit at a time (ballot + one atomic per non-empty bit)
             double w = 0.0;
 #pragma unroll 1
@@ -1380,7 +1386,7 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
                 const bool keep = (alive >> i) & 1u;
                 const unsigned long long slot = warp_append(keep, &ctr->n_surv);
                 if (keep) {
-                    const uint32_t c = (uint32_t)(32 * i + lane);
+                    const uint32_t c = c0 + (uint32_t)(32 * i + lane);
 #pragma unroll
                     for (int j = 0; j < N; j++) {
                         const bool up = (c >> (N - 1 - j)) & 1u;

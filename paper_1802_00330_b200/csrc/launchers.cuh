@@ -15,7 +15,7 @@ void SetupK<N>::run(rb_handle* h) {
         if (h->ftab_smem > 160 * 1024) h->meta.ftab = 0;  // tables too large: direct evaluation
     }
     h->fwt_bps = 0;
-    if (N >= 5 && N <= 10 && h->meta.ftab) {
+    if (N >= 5 && N <= 16 && h->meta.ftab) {
         h->fwt_smem = fwt_smem_bytes<N>(h->meta, 256);
         if ((int)h->fwt_smem <= h->smem_optin) {
             set_max_dyn_smem(k_filter_wt<N>, h->smem_optin);
@@ -24,10 +24,10 @@ void SetupK<N>::run(rb_handle* h) {
             h->fwt_bps = nbw;
         }
     }
-    // on by default when every equation's table is at most a quarter of a parent's children
+    // on by default when every equation's table is at most a quarter of a work unit's children
     // (building it costs less than evaluating per child): katsura6 filter 6.1 -> 3.3 ms, eco8
     // 22.6 -> 10.0 ms; brown8 (a degree-8 term: 256 entries) stays direct (4.3 vs 5.0 ms)
-    h->fwt_auto = h->fwt_bps > 0 && h->meta.e_max <= (1 << (N - 2));
+    h->fwt_auto = h->fwt_bps > 0 && h->meta.e_max <= (1 << ((N < 10 ? N : 10) - 2));
     h->use_fwt = h->fwt_auto;
     // the attribute is per kernel (shared by every handle of this n): set it to the opt-in maximum
     const size_t mx = std::max({h->filter_smem, h->eval_smem, h->lin_smem, h->sweep_smem});
@@ -122,7 +122,8 @@ void FilterK<N>::run(rb_handle* h, int64_t max_parents, int64_t* tags, int64_t p
     if (h->use_fwt && h->fwt_bps > 0) {  // warp per parent
         const bool g = gen_on(h) && h->gen_fwt_bps > 0;
         const int64_t cap = (int64_t)h->sms * (g ? h->gen_fwt_bps : h->fwt_bps);
-        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((max_parents + 7) / 8, cap));
+        const int64_t units = max_parents << (N > 10 ? N - 10 : 0);  // (parent, 1024-child chunk) above n = 10
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((units + 7) / 8, cap));
         h->launches++;
         if (g)
             klaunch_k(h, h->gen.filter_wt, blocks, 256, h->fwt_smem, h->meta, (const uint8_t*)h->d_tab, h->F[h->cur].f,

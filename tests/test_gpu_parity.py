@@ -104,7 +104,7 @@ def test_filter_random_cells_vs_oracle(native, name, mode, codegen):
     eng = _native.Engine(compile_tables(spec), 0)
     _set_codegen(eng, codegen)
     eng.set_option("filter_tab", int(mode == 1))
-    eng.set_option("filter_wt", int(mode == 2))  # k_filter_wt where 5 <= n <= 10, else the direct filter
+    eng.set_option("filter_wt", int(mode == 2))  # k_filter_wt where 5 <= n <= 16, else the direct filter
     osys = oracle_sys(name)
     for depth, seed in ((1, 1), (3, 2), (7, 3), (30, 4)):
         P = max(1, min(2048, (1 << 16) >> spec.n))
@@ -299,7 +299,7 @@ def test_solve_host_loop_tabulated_specialised_filter(native, case):
 @pytest.mark.parametrize("codegen", [0, 1], ids=["tables", "specialised"])
 @pytest.mark.parametrize("case", solve_cases())
 def test_solve_host_loop_warp_tabulated_filter(native, case, codegen):
-    """Host-driven rounds with the warp-tabulated filter forced on (k_filter_wt, 5 <= n <= 10)."""
+    """Host-driven rounds with the warp-tabulated filter forced on (k_filter_wt, 5 <= n <= 16)."""
     from paper_1802_00330_b200 import bnb
     meta = load_solve(case)
     spec = golden_spec(meta["system"])
