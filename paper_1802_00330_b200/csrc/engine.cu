@@ -363,6 +363,21 @@ static void build_tables(rb_handle* h, const rb_system* sys) {
     h->guard_f_ecmin = m.f_ecmin;
     h->guard_j_ecmin = m.j_ecmin;
     h->meta = m;
+    // constant J entries: no term, or one term without factors -- the value [c, c] that
+    // eval_poly (and the specialised evaluator, codegen.cpp evJ) computes for every box
+    {
+        std::vector<double> jc((size_t)n * n, 0.0);
+        for (int w = 0; w < 4; w++) h->jmask[w] = 0;
+        for (int q = 0; q < n * n; q++) {
+            const int t0 = sys->poly_off[n + q], t1 = sys->poly_off[n + q + 1];
+            const bool cst = t1 == t0 || (t1 - t0 == 1 && sys->fac_off[t0 + 1] == sys->fac_off[t0]);
+            if (!cst) continue;
+            h->jmask[q >> 6] |= 1ull << (q & 63);
+            jc[q] = t1 == t0 ? 0.0 : 0.0 + sys->coeff[t0];  // [0,0] + [c,c] (+0 for a zero c)
+        }
+        dalloc(&h->d_jc, (size_t)n * n);
+        ck(cudaMemcpyAsync(h->d_jc, jc.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, h->st), "jc h2d");
+    }
     dalloc(&h->d_tab, (size_t)m.bytes3);
     ck(cudaMemcpyAsync(h->d_tab, buf.data(), m.bytes3, cudaMemcpyHostToDevice, h->st), "tables h2d");
     ck(cudaStreamSynchronize(h->st), "tables sync");
@@ -833,6 +848,7 @@ static void release_all(rb_handle* h) {
     fr(h->r_cert);
     fr(h->r_uns);
     fr(h->d_tab);
+    fr(h->d_jc);
     fr(h->W.x);
     fr(h->W.jl);
     fr(h->W.jh);
@@ -1176,7 +1192,7 @@ static bool graph_rounds(rb_handle* h, const rb_config* cfg, double target, bool
         (uintptr_t)h->d_state, (uintptr_t)scap, (uintptr_t)dedup, (uintptr_t)prm.hs_enable_round,
         (uintptr_t)prm.hs_possible, (uintptr_t)hw_bits, (uintptr_t)prm.contract_output,
         (uintptr_t)(h->use_ftab ? 1 : 0), (uintptr_t)(h->hs_fused ? 1 : 0), (uintptr_t)h->fused_rows,
-        (uintptr_t)(h->use_fwt ? 1 : 0)};
+        (uintptr_t)(h->use_fwt ? 1 : 0), (uintptr_t)(h->jconst ? 1 : 0)};
     key.push_back((uintptr_t)h->hs_cond);
     key.push_back((uintptr_t)h->graph_unroll);
     key.push_back((uintptr_t)h->graph_fused_only);
@@ -2154,6 +2170,11 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     const std::string k(key);
     if (k == "filter_tab") {
         h->use_ftab = value != 0;
+        return RB_OK;
+    }
+    if (k == "jconst") {  // 1 (default): constant J entries bypass the HS scratch (k_hs_lin_tps)
+        h->jconst = value != 0;
+        graph_release(h);
         return RB_OK;
     }
     if (k == "filter_wt") {  // warp-tabulated filter where it applies (5 <= n <= 16, tables fit); -1: auto

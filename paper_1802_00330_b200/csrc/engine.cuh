@@ -185,6 +185,11 @@ struct rb_handle {
     bool use_ftab = true;
     // warp-tabulated filter (k_filter_wt, 5 <= n <= 16): shared memory, blocks per SM (table / specialised)
     bool use_fwt = false, fwt_auto = false;
+    // constant entries of J (no variable): mask + values (device), used by the three-kernel
+    // HS with k_hs_lin_tps ("jconst" option)
+    unsigned long long jmask[4] = {0, 0, 0, 0};
+    double* d_jc = nullptr;
+    bool jconst = true;
     size_t fwt_smem = 0;
     int fwt_bps = 0, gen_fwt_bps = 0;
     bool hs_fused = true;        // k_hs_fused (tile in shared memory) for small HS batches

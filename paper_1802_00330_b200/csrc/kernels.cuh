@@ -1459,6 +1459,21 @@ struct HsParams {
     int* eq_order;
     int64_t s_cap;
     int force_exact;       // every guard fails: the Exact policy everywhere (parity tests)
+    // constant entries of J (polynomials without variables: [c, c] for every box): with jc
+    // set, k_hs_eval does not store them and k_hs_lin_tps takes c instead of loading
+    const double* jc;      // [n^2] values (null: every entry through the scratch)
+    unsigned long long jm[4];  // bit q: entry q constant
+};
+
+// bit q of the constant-J mask, words held in registers (q may be a runtime index)
+struct JMask {
+    unsigned long long w0, w1, w2, w3;
+    __device__ __forceinline__ explicit JMask(const HsParams& p)
+        : w0(p.jc ? p.jm[0] : 0), w1(p.jc ? p.jm[1] : 0), w2(p.jc ? p.jm[2] : 0), w3(p.jc ? p.jm[3] : 0) {}
+    __device__ __forceinline__ bool operator()(int q) const {
+        const unsigned long long w = q < 64 ? w0 : (q < 128 ? w1 : (q < 192 ? w2 : w3));
+        return (w >> (q & 63)) & 1ull;
+    }
 };
 
 struct HsScratch {         // SoA with stride B (batch capacity)
@@ -1597,6 +1612,10 @@ __global__ void __launch_bounds__(128, RB_EVAL_MINB) k_hs_eval(TabMeta meta, con
         fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
     };
     bool deferred = false;
+    // constant J entries are not stored when k_hs_lin_tps takes them from prm.jc (the
+    // specialised evaluator skips exactly the entries the engine's mask holds)
+    const JMask jskip(prm);
+    const bool skipc = prm.jc != nullptr;
     for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = it % nb;
         const int r = (int)(it / nb);
@@ -1607,7 +1626,7 @@ __global__ void __launch_bounds__(128, RB_EVAL_MINB) k_hs_eval(TabMeta meta, con
             // a box needing the Exact policy is evaluated after the loop: no out-of-line call
             // in the hot loop (its calling convention spilled the loop state to the stack)
             if (fastJ && fastF) {
-                EV::template J<Fast>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
+                EV::template J<Fast>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B, skipc);
                 EV::template F<Fast>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
             } else {
                 deferred = true;
@@ -1617,6 +1636,7 @@ __global__ void __launch_bounds__(128, RB_EVAL_MINB) k_hs_eval(TabMeta meta, con
 #pragma unroll 1
         for (int q = p0; q < p1; q++) {
             if (q < N * N) {
+                if (jskip(q)) continue;  // constant entry: k_hs_lin_tps takes it from prm.jc
                 // J(X) (hansen.py:61-63); zero polynomials evaluate to [0,0]
                 const ival v = fastJ ? eval_poly<Fast>(tab, N + q, xlo, xhi, stride)
                                      : eval_poly_exact(tab, N + q, xlo, xhi, stride);
@@ -1643,8 +1663,8 @@ __global__ void __launch_bounds__(128, RB_EVAL_MINB) k_hs_eval(TabMeta meta, con
                 if (!(W.flags[t] & HSF_EXACT_EVAL)) continue;
                 bool fastJ, fastF;
                 stage(b0 + t, t, false, fastJ, fastF);
-                if (fastJ) EV::template J<Fast>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
-                else EV::template J<Exact>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B);
+                if (fastJ) EV::template J<Fast>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B, skipc);
+                else EV::template J<Exact>(xlo, xhi, stride, W.jl + t, W.jh + t, W.B, skipc);
                 if (fastF) EV::template F<Fast>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
                 else EV::template F<Exact>(xmid, xmid, stride, W.fl + t, W.fh + t, W.B);
             }
@@ -1977,8 +1997,13 @@ __global__ void __launch_bounds__(128, RB_LIN_MINB) k_hs_lin(SBuf S, int64_t n_i
 // the skipped ones act on exact zeros / ones of the identity half (x - f*0 = x,
 // 1 * inv = inv, 0 - f*inv = -(f*inv)), so the inverse is bit-identical (zero signs
 // aside, which no later operation can observe).  Row swaps are predicated selects.
-template <int N, class A, class AM, int IU = N>
-__device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int64_t t);
+struct JLoad {  // J entry q of box t from the scratch
+    const HsScratch& W;
+    int64_t t;
+    __device__ __forceinline__ ival operator()(int q) const { return mk(W.jl[q * W.B + t], W.jh[q * W.B + t]); }
+};
+template <int N, class A, class AM, int IU = N, class JG = JLoad>
+__device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int64_t t, const JG* jg = nullptr);
 
 template <int N, class A>
 __device__ __forceinline__ void lin_products_reg(const double (&a)[N][N], HsScratch& W, int64_t t) {
@@ -1987,14 +2012,15 @@ __device__ __forceinline__ void lin_products_reg(const double (&a)[N][N], HsScra
 
 // M = A J and g = A F(x) with A given by an accessor am(i, u); IU = unrolling of the row
 // loop (N for A in registers; small for A in shared memory, bounding the loads in flight)
-template <int N, class A, class AM, int IU>
-__device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int64_t t) {
+template <int N, class A, class AM, int IU, class JG>
+__device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int64_t t, const JG* jg) {
     // M = A J, column by column in place (linalg.py:102-114), u ascending
 #pragma unroll 1
     for (int j = 0; j < N; j++) {
         ival jc[N];
 #pragma unroll
-        for (int u = 0; u < N; u++) jc[u] = mk(W.jl[(u * N + j) * W.B + t], W.jh[(u * N + j) * W.B + t]);
+        for (int u = 0; u < N; u++)
+            jc[u] = jg ? (*jg)(u * N + j) : mk(W.jl[(u * N + j) * W.B + t], W.jh[(u * N + j) * W.B + t]);
 #pragma unroll IU
         for (int i = 0; i < N; i++) {
             ival acc = mk(0.0, 0.0);
@@ -2186,9 +2212,25 @@ struct TpsShape {
     static constexpr int MINB = N <= 7 ? RB_TPS_MINB7 : (N <= 8 ? RB_TPS_MINB8 : RB_TPS_MINB12);
     using Lbl = typename pick_t<(N > 8), unsigned long long, uint32_t>::type;
 };
+// J entry q: the constant [c, c] where the mask says so, else the scratch
+struct JConst {
+    const HsScratch& W;
+    int64_t t;
+    JMask jm;
+    const double* jc;
+    __device__ __forceinline__ ival operator()(int q) const {
+        if (jm(q)) {
+            const double c = jc[q];
+            return mk(c, c);
+        }
+        return mk(W.jl[q * W.B + t], W.jh[q * W.B + t]);
+    }
+};
 template <int N>
-static __device__ __noinline__ void lin_products_tps_exact(const double* C, HsScratch W, int64_t t) {
-    lin_products_acc<N, Exact>([&](int i, int u) { return C[(i * N + u) * TpsShape<N>::T]; }, W, t);
+static __device__ __noinline__ void lin_products_tps_exact(const double* C, HsScratch W, int64_t t, HsParams prm) {
+    const JConst jg{W, t, JMask(prm), prm.jc};
+    auto am = [&](int i, int u) { return C[(i * N + u) * TpsShape<N>::T]; };
+    lin_products_acc<N, Exact, decltype(am), N, JConst>(am, W, t, &jg);
 }
 
 // k_hs_lin_tpb with the in-place tableau in shared memory (this thread's column:
@@ -2215,8 +2257,10 @@ __global__ void __launch_bounds__(TpsShape<N>::T, TpsShape<N>::MINB) k_hs_lin_tp
     constexpr int T = TpsShape<N>::T;  // the launch's block size: tableau offsets are immediates
     double* C = reinterpret_cast<double*>(smem) + threadIdx.x;
     auto c = [&](int i, int s2) -> double& { return C[(i * N + s2) * T]; };
+    const JMask jmask(prm);
     for (int64_t b = b0 + (int64_t)blockIdx.x * T + threadIdx.x; b < b_end; b += (int64_t)gridDim.x * T) {
         const int64_t t = b - b0;
+        const JConst jg{W, t, jmask, prm.jc};
         ExpRange rj, ra, rf;
         rj.init();
         ra.init();
@@ -2226,7 +2270,8 @@ __global__ void __launch_bounds__(TpsShape<N>::T, TpsShape<N>::MINB) k_hs_lin_tp
         for (int i = 0; i < N; i++)
 #pragma unroll
             for (int j = 0; j < N; j++) {
-                const double lo = W.jl[(i * N + j) * W.B + t], hi = W.jh[(i * N + j) * W.B + t];
+                const ival v = jg(i * N + j);
+                const double lo = v.lo, hi = v.hi;
                 rj.add(lo);
                 rj.add(hi);
                 const double m = mid_of(lo, hi);
@@ -2307,9 +2352,9 @@ __global__ void __launch_bounds__(TpsShape<N>::T, TpsShape<N>::MINB) k_hs_lin_tp
                 auto am_tps = [&](int i, int u) { return lds_volatile(&c(i, u)); };
                 // volatile shared loads: kept inside the column loop (hoisting all n^2 of A out
                 // of it is what spilled)
-                lin_products_acc<N, Fast, decltype(am_tps), kTpsRowUnroll>(am_tps, W, t);
+                lin_products_acc<N, Fast, decltype(am_tps), kTpsRowUnroll, JConst>(am_tps, W, t, &jg);
             } else {  // rare: out of line, A read from the tableau (no local copy in this frame)
-                lin_products_tps_exact<N>(C, W, t);
+                lin_products_tps_exact<N>(C, W, t, prm);
                 fl = HSF_EXACT_LIN;
             }
         }

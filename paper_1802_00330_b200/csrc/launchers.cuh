@@ -171,6 +171,17 @@ void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* 
     const int64_t B = h->W.B;
     Front out = h->F[h->cur ^ 1].f;
     h->launches += 3;
+    // the Gauss-Jordan variant first: with k_hs_lin_tps the constant J entries bypass the scratch
+    int lin = 0;  // 0: G lanes per box (k_hs_lin), 1: registers (k_hs_lin_tpb), 2: shared (k_hs_lin_tps)
+    if constexpr (N <= 8)
+        if (h->lin_tpb == 1 && h->lin_tpb_threads > 0) lin = 1;
+    if constexpr (N <= 12)
+        if (lin == 0 && h->lin_tpb == 2) lin = 2;
+    prm.jc = nullptr;
+    if (lin == 2 && h->jconst && (h->jmask[0] | h->jmask[1] | h->jmask[2] | h->jmask[3])) {
+        prm.jc = h->d_jc;
+        for (int w = 0; w < 4; w++) prm.jm[w] = h->jmask[w];
+    }
     // split each box's n^2 + n polynomials over R threads when the batch is small
     const int64_t bound = std::max<int64_t>(1, std::min<int64_t>(B, batch_bound));
     const int64_t target = (int64_t)h->sms * 1024;
@@ -181,24 +192,21 @@ void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* 
     else
         klaunch(h, k_hs_eval<N>, grid_for(bound * R, T, h->sms * h->eval_blocks_per_sm), T, h->eval_smem,
             h->meta, h->d_tab, h->S, n_in, b0, prm, h->W, out, h->d_ctr, tags, R);
-    bool tpb = false;
     if constexpr (N <= 8) {
-        if (h->lin_tpb == 1 && h->lin_tpb_threads > 0) {
-            tpb = true;
+        if (lin == 1) {
             const int tl = h->lin_tpb_threads;
             klaunch(h, k_hs_lin_tpb<N>, grid_for(bound, tl, h->sms * h->lin_tpb_bps), tl, h->lin_tpb_smem, h->S, n_in,
                     b0, prm, h->W, h->d_ctr);
         }
     }
     if constexpr (N <= 12) {
-        if (!tpb && h->lin_tpb == 2) {
-            tpb = true;
+        if (lin == 2) {
             constexpr int TT = TpsShape<N>::T;
             klaunch(h, k_hs_lin_tps<N>, grid_for(bound, TT, h->sms * h->lin_tps_bps), TT, h->lin_tps_smem, h->S,
                     n_in, b0, prm, h->W, h->d_ctr);
         }
     }
-    if (!tpb)
+    if (lin == 0)
         klaunch(h, k_hs_lin<N>, grid_for(B, (T / 32) * LinLayout<N>::BPW, h->sms * h->lin_blocks_per_sm), T,
                 h->lin_smem, h->S, n_in, b0, prm, h->W, h->d_ctr);
     klaunch(h, k_hs_sweep<N>, grid_for(B, T, h->sms * h->sweep_blocks_per_sm), T, h->sweep_smem,

@@ -316,6 +316,42 @@ def test_solve_host_loop_warp_tabulated_filter(native, case, codegen):
     check_against_golden(case, out, meta)
 
 
+@pytest.mark.parametrize("case", solve_cases())
+def test_solve_host_loop_without_constant_j(native, case):
+    """Host-driven rounds with every J entry through the HS scratch ("jconst" off)."""
+    from paper_1802_00330_b200 import bnb
+    meta = load_solve(case)
+    spec = golden_spec(meta["system"])
+    eng = bnb.engine_for(spec)
+    eng.set_option("graph", 0)
+    eng.set_option("hs_fused", 0)  # every HS round through eval / lin / sweep
+    eng.set_option("jconst", 0)
+    try:
+        out = eng.solve(bnb.native_config(bnb.SolverConfig(**meta["config"])))
+    finally:
+        eng.set_option("graph", 1)
+        eng.set_option("hs_fused", 1)
+        eng.set_option("jconst", 1)
+    check_against_golden(case, out, meta)
+
+
+@pytest.mark.parametrize("case", solve_cases())
+def test_solve_host_loop_three_kernel_hs(native, case):
+    """Host-driven rounds with every HS round through eval / lin / sweep (constant J on)."""
+    from paper_1802_00330_b200 import bnb
+    meta = load_solve(case)
+    spec = golden_spec(meta["system"])
+    eng = bnb.engine_for(spec)
+    eng.set_option("graph", 0)
+    eng.set_option("hs_fused", 0)
+    try:
+        out = eng.solve(bnb.native_config(bnb.SolverConfig(**meta["config"])))
+    finally:
+        eng.set_option("graph", 1)
+        eng.set_option("hs_fused", 1)
+    check_against_golden(case, out, meta)
+
+
 @pytest.mark.parametrize("case", solve_cases()[:12])
 def test_solve_persistent_small_rounds(native, case):
     """The experimental persistent small-round kernel (grid barriers, ping-pong frontier)."""
