@@ -1277,6 +1277,10 @@ __host__ __device__ inline int fwt_smem_bytes(const TabMeta& m, int threads) {
     return ftab_off_sp<N>(m) + (threads / 32) * fwt_warp_doubles<N>(m) * 8;
 }
 
+#ifndef RB_FWT_UNROLL
+#define RB_FWT_UNROLL 2
+#endif
+constexpr int kFwtUnroll = RB_FWT_UNROLL;
 template <int N, class EV = TabEval>
 __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                    const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
@@ -1347,14 +1351,14 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
                 auto sweep = [&](auto fts) {
                     if (alive == (K >= 32 ? 0xffffffffu : ((1u << K) - 1u))) {
                         uint32_t keep = 0;
-#pragma unroll
+#pragma unroll kFwtUnroll  // bounded: the loop is instantiated once per equation (instruction cache)
                         for (int i = 0; i < K; i++) {
                             const ival acc = fts(c0 + (uint32_t)(32 * i + lane), table);
                             keep |= (uint32_t)(acc.lo <= 0.0 && 0.0 <= acc.hi) << i;
                         }
                         alive = keep;
                     } else {
-#pragma unroll
+#pragma unroll 1
                         for (int i = 0; i < K; i++) {
                             if ((alive >> i) & 1u) {
                                 const ival acc = fts(c0 + (uint32_t)(32 * i + lane), table);
@@ -2284,7 +2288,7 @@ __global__ void __launch_bounds__(TpsShape<N>::T, TpsShape<N>::MINB) k_hs_lin_tp
         Lbl orig = 0, label = 0;
 #pragma unroll
         for (int r = 0; r < N; r++) orig |= (Lbl)r << (4 * r);
-#pragma unroll
+#pragma unroll(N <= 8 ? N : 1)  // n > 8: the unrolled steps overflowed the instruction cache
         for (int k = 0; k < N; k++) {
             int pr = k;
             double best = fabs(c(k, k)), pv = c(k, k);
