@@ -235,8 +235,9 @@ int64_t rb_kernel_launches(rb_handle* h);
  *                 Default: on for n >= 10 (2^n >= 1024 children per parent).
  *   "filter_wt"   1: warp-tabulated filter (k_filter_wt, a warp per parent or per 1024 of its
  *                 children, 5 <= n <= 16),
- *                 ahead of "filter_tab"; 0: off; -1: the default, on when every
- *                 equation's table has at most 2^(min(n, 10) - 2) entries.
+ *                 ahead of "filter_tab"; 0: off; -1: the default, on unless more than
+ *                 half of the equations have tables above 2^(min(n, 10) - 2) entries
+ *                 (such equations are evaluated per child inside k_filter_wt).
  *   "force_exact" 0 (default): exponent guards pick IEEE directed rounding wherever it
  *                 provably equals the reference; 1: every guard fails, so every box
  *                 runs the Exact policy (the reference's error-free transformations,

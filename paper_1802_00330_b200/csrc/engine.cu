@@ -268,6 +268,18 @@ static void build_tables(rb_handle* h, const rb_system* sys) {
         std::fill(ent_off.begin(), ent_off.end(), 0);
     }
     m.ent_total = (int)ent.size();
+    // k_filter_wt: an equation whose table exceeds a quarter of a work unit's children
+    // (2^min(n, 10) / 4) is evaluated per child; the table area fits the largest of the others
+    m.fwt_direct = 0;
+    m.fwt_emax = 1;
+    if (m.ftab) {
+        const int lim = 1 << (std::min(n, 10) - 2);
+        for (int e = 0; e < n; e++) {
+            const int E = ent_off[e + 1] - ent_off[e];
+            if (E > lim) m.fwt_direct |= 1 << e;
+            else m.fwt_emax = std::max(m.fwt_emax, E);
+        }
+    }
     // the tables pay off when terms multiply several variables (measured: eco8 1.6x
     // faster filter, linear-term systems slightly slower): mean (d - 1) >= 1
     {

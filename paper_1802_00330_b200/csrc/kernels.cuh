@@ -57,6 +57,9 @@ struct TabMeta {
     int ent_total;                  // total (term, combo) entries over the equations
     int off_tbase, off_ent_off, off_ent, bytes2;  // byte offsets (tbase u16[TF], ent_off u16[n+1], ent u32[])
     int off_termp, bytes3;          // packed F terms (TermP[TF]) for the direct filter
+    // warp-tabulated filter (k_filter_wt): equations whose table would exceed a quarter of a
+    // work unit's children are evaluated per child instead (bit e), the others' largest table
+    int fwt_direct, fwt_emax;
 };
 
 // One F term packed for the direct filter: up to 4 factors of (var < 16,
@@ -1270,11 +1273,21 @@ __global__ void __launch_bounds__(256) k_filter_tab(TabMeta meta, const uint8_t*
 // k_filter / k_filter_tab (bit-identical); survivors compacted per child bit.
 template <int N>
 __host__ __device__ inline int fwt_warp_doubles(const TabMeta& m) {
-    return ((3 * N + 1 + 1) & ~1) + 2 * m.e_max;  // parent (lo, hi, mid, exact) + table (double2)
+    return ((3 * N + 1 + 1) & ~1) + 2 * m.fwt_emax;  // parent (lo, hi, mid, exact) + table (double2)
+}
+// per-child evaluation of the direct equations: packed terms, then a child box per thread
+template <int N>
+__host__ __device__ inline int fwt_off_termp(const TabMeta& m, int threads) {
+    return align16(ftab_off_sp<N>(m) + (threads / 32) * fwt_warp_doubles<N>(m) * 8);
+}
+template <int N>
+__host__ __device__ inline int fwt_off_xs(const TabMeta& m, int threads) {
+    return align16(fwt_off_termp<N>(m, threads) + 16 * m.TF);
 }
 template <int N>
 __host__ __device__ inline int fwt_smem_bytes(const TabMeta& m, int threads) {
-    return ftab_off_sp<N>(m) + (threads / 32) * fwt_warp_doubles<N>(m) * 8;
+    if (!m.fwt_direct) return ftab_off_sp<N>(m) + (threads / 32) * fwt_warp_doubles<N>(m) * 8;
+    return fwt_off_xs<N>(m, threads) + 16 * N * threads;
 }
 
 #ifndef RB_FWT_UNROLL
@@ -1307,6 +1320,9 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
         copy_async<4>(tbase, gtab + meta.off_tbase, 2 * meta.TF);
         copy_async<4>(ent_off, gtab + meta.off_ent_off, 2 * (N + 1));
         copy_async<4>(ent, gtab + meta.off_ent, 4 * meta.ent_total);
+        TermP* tp = reinterpret_cast<TermP*>(smem + fwt_off_termp<N>(meta, blockDim.x));
+        double2* xs2 = reinterpret_cast<double2*>(smem + fwt_off_xs<N>(meta, blockDim.x)) + threadIdx.x;
+        if (meta.fwt_direct) copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
         double* sp = reinterpret_cast<double*>(smem + ftab_off_sp<N>(meta)) + wid * fwt_warp_doubles<N>(meta);
         double2* table = reinterpret_cast<double2*>(sp + ((3 * N + 1 + 1) & ~1));
@@ -1337,6 +1353,33 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
             for (int k = 0; k < N; k++) {
                 if (__ballot_sync(0xffffffffu, alive != 0) == 0) break;
                 const int e = s_order[k];
+                if ((meta.fwt_direct >> e) & 1) {  // per child, as k_filter (same operations)
+                    const uint32_t before = alive;
+#pragma unroll 1
+                    for (int i = 0; i < K; i++) {
+                        if (!((alive >> i) & 1u)) continue;
+                        const uint32_t c = c0 + (uint32_t)(32 * i + lane);
+#pragma unroll
+                        for (int j = 0; j < N; j++) {
+                            const bool up = (c >> (N - 1 - j)) & 1u;
+                            xs2[j * blockDim.x] = up ? make_double2(sp[2 * N + j], sp[N + j])
+                                                     : make_double2(sp[j], sp[2 * N + j]);
+                        }
+                        const ival v = exact ? EV::template feq<Exact>(tp, tab, e, xs2, blockDim.x)
+                                             : EV::template feq<RB_FILTER_FAST>(tp, tab, e, xs2, blockDim.x);
+                        if (!(v.lo <= 0.0 && 0.0 <= v.hi)) alive &= ~(1u << i);
+                    }
+                    const unsigned ne = (unsigned)__popc(before), nr = ne - (unsigned)__popc(alive);
+                    ops += ne * (unsigned)meta.ops_eq[e];
+                    if ((blockIdx.x & 3) == 0) {
+                        const unsigned se = __reduce_add_sync(0xffffffffu, ne), sr = __reduce_add_sync(0xffffffffu, nr);
+                        if (lane == 0) {
+                            atomicAdd(&s_eval[e], se);
+                            if (sr) atomicAdd(&s_rej[e], sr);
+                        }
+                    }
+                    continue;
+                }
                 const int e0 = ent_off[e], E = ent_off[e + 1] - e0;
                 for (int i = lane; i < E; i += 32) {
                     const uint32_t en = ent[e0 + i];

@@ -24,10 +24,10 @@ void SetupK<N>::run(rb_handle* h) {
             h->fwt_bps = nbw;
         }
     }
-    // on by default when every equation's table is at most a quarter of a work unit's children
-    // (building it costs less than evaluating per child): katsura6 filter 6.1 -> 3.3 ms, eco8
-    // 22.6 -> 10.0 ms; brown8 (a degree-8 term: 256 entries) stays direct (4.3 vs 5.0 ms)
-    h->fwt_auto = h->fwt_bps > 0 && h->meta.e_max <= (1 << ((N < 10 ? N : 10) - 2));
+    // on by default when at most half of the equations have tables larger than a quarter of
+    // a work unit's children (those are evaluated per child): katsura6 filter 6.1 -> 3.3 ms,
+    // eco8 22.6 -> 10.0 ms, brown8 (one degree-8 product evaluated per child) 4.2 -> 3.8 ms
+    h->fwt_auto = h->fwt_bps > 0 && 2 * __builtin_popcount((unsigned)h->meta.fwt_direct) <= N;
     h->use_fwt = h->fwt_auto;
     // the attribute is per kernel (shared by every handle of this n): set it to the opt-in maximum
     const size_t mx = std::max({h->filter_smem, h->eval_smem, h->lin_smem, h->sweep_smem});
