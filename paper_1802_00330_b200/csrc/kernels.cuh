@@ -1294,7 +1294,9 @@ __host__ __device__ inline int fwt_smem_bytes(const TabMeta& m, int threads) {
 #define RB_FWT_UNROLL 2
 #endif
 constexpr int kFwtUnroll = RB_FWT_UNROLL;
-template <int N, class EV = TabEval>
+// HYB: some equations evaluated per child (meta.fwt_direct); a separate instantiation, as
+// that path's code in the loop cost the all-table systems ~15 % (instruction fetch)
+template <int N, class EV = TabEval, bool HYB = false>
 __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                    const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
                                                    int64_t* tags, const int* __restrict__ eq_order, int64_t pcount) {
@@ -1322,7 +1324,7 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
         copy_async<4>(ent, gtab + meta.off_ent, 4 * meta.ent_total);
         TermP* tp = reinterpret_cast<TermP*>(smem + fwt_off_termp<N>(meta, blockDim.x));
         double2* xs2 = reinterpret_cast<double2*>(smem + fwt_off_xs<N>(meta, blockDim.x)) + threadIdx.x;
-        if (meta.fwt_direct) copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
+        if (HYB) copy_async<16>(tp, gtab + meta.off_termp, 16 * meta.TF);
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
         double* sp = reinterpret_cast<double*>(smem + ftab_off_sp<N>(meta)) + wid * fwt_warp_doubles<N>(meta);
         double2* table = reinterpret_cast<double2*>(sp + ((3 * N + 1 + 1) & ~1));
@@ -1353,7 +1355,7 @@ __global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* 
             for (int k = 0; k < N; k++) {
                 if (__ballot_sync(0xffffffffu, alive != 0) == 0) break;
                 const int e = s_order[k];
-                if ((meta.fwt_direct >> e) & 1) {  // per child, as k_filter (same operations)
+                if (HYB && ((meta.fwt_direct >> e) & 1)) {  // per child, as k_filter (same operations)
                     const uint32_t before = alive;
 #pragma unroll 1
                     for (int i = 0; i < K; i++) {
@@ -2044,6 +2046,9 @@ __global__ void __launch_bounds__(128, RB_LIN_MINB) k_hs_lin(SBuf S, int64_t n_i
 // the skipped ones act on exact zeros / ones of the identity half (x - f*0 = x,
 // 1 * inv = inv, 0 - f*inv = -(f*inv)), so the inverse is bit-identical (zero signs
 // aside, which no later operation can observe).  Row swaps are predicated selects.
+#ifndef RB_LIN_COLS
+#define RB_LIN_COLS 2  // lin_products_acc: columns of J per pass
+#endif
 struct JLoad {  // J entry q of box t from the scratch
     const HsScratch& W;
     int64_t t;
@@ -2061,33 +2066,45 @@ __device__ __forceinline__ void lin_products_reg(const double (&a)[N][N], HsScra
 // loop (N for A in registers; small for A in shared memory, bounding the loads in flight)
 template <int N, class A, class AM, int IU, class JG>
 __device__ __forceinline__ void lin_products_acc(const AM& am, HsScratch& W, int64_t t, const JG* jg) {
-    // M = A J, column by column in place (linalg.py:102-114), u ascending
+    // M = A J (linalg.py:102-114) and g = A F(x) (linalg.py:117-129), u ascending: the n
+    // columns of J and F(x) as n + 1 columns v, RB_LIN_COLS of them per pass so each A
+    // element read serves several columns; column v of M is written over column v of J
+    constexpr int CP = RB_LIN_COLS;
+    auto ld = [&](int v, int u) -> ival {
+        if (v == N) return mk(W.fl[u * W.B + t], W.fh[u * W.B + t]);
+        return jg ? (*jg)(u * N + v) : mk(W.jl[(u * N + v) * W.B + t], W.jh[(u * N + v) * W.B + t]);
+    };
+    auto st = [&](int v, int i, const ival& r) {
+        if (v == N) {
+            W.fl[i * W.B + t] = r.lo;
+            W.fh[i * W.B + t] = r.hi;
+        } else {
+            W.jl[(i * N + v) * W.B + t] = r.lo;
+            W.jh[(i * N + v) * W.B + t] = r.hi;
+        }
+    };
 #pragma unroll 1
-    for (int j = 0; j < N; j++) {
-        ival jc[N];
+    for (int v0 = 0; v0 <= N; v0 += CP) {
+        ival jc[CP][N];
 #pragma unroll
-        for (int u = 0; u < N; u++)
-            jc[u] = jg ? (*jg)(u * N + j) : mk(W.jl[(u * N + j) * W.B + t], W.jh[(u * N + j) * W.B + t]);
+        for (int c = 0; c < CP; c++)
+#pragma unroll
+            for (int u = 0; u < N; u++) jc[c][u] = v0 + c <= N ? ld(v0 + c, u) : mk(0.0, 0.0);
 #pragma unroll IU
         for (int i = 0; i < N; i++) {
-            ival acc = mk(0.0, 0.0);
+            ival acc[CP];
 #pragma unroll
-            for (int u = 0; u < N; u++) acc = A::add(acc, pmul_tpb<A>(am(i, u), jc[u]));
-            W.jl[(i * N + j) * W.B + t] = acc.lo;
-            W.jh[(i * N + j) * W.B + t] = acc.hi;
+            for (int c = 0; c < CP; c++) acc[c] = mk(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < N; u++) {
+                const double a = am(i, u);
+#pragma unroll
+                for (int c = 0; c < CP; c++) acc[c] = A::add(acc[c], pmul_tpb<A>(a, jc[c][u]));
+            }
+#pragma unroll
+            for (int c = 0; c < CP; c++)
+                if (v0 + c <= N) st(v0 + c, i, acc[c]);
         }
-    }
-    // g = A F(x) (linalg.py:117-129)
-    ival fx[N];
-#pragma unroll
-    for (int u = 0; u < N; u++) fx[u] = mk(W.fl[u * W.B + t], W.fh[u * W.B + t]);
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-        ival acc = mk(0.0, 0.0);
-#pragma unroll
-        for (int u = 0; u < N; u++) acc = A::add(acc, pmul_tpb<A>(am(i, u), fx[u]));
-        W.fl[i * W.B + t] = acc.lo;
-        W.fh[i * W.B + t] = acc.hi;
     }
 }
 

@@ -18,9 +18,11 @@ void SetupK<N>::run(rb_handle* h) {
     if (N >= 5 && N <= 16 && h->meta.ftab) {
         h->fwt_smem = fwt_smem_bytes<N>(h->meta, 256);
         if ((int)h->fwt_smem <= h->smem_optin) {
-            set_max_dyn_smem(k_filter_wt<N>, h->smem_optin);
+            const void* kf = h->meta.fwt_direct ? (const void*)k_filter_wt<N, TabEval, true>
+                                                : (const void*)k_filter_wt<N, TabEval, false>;
+            set_max_dyn_smem(kf, h->smem_optin);
             int nbw = 0;
-            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbw, k_filter_wt<N>, 256, h->fwt_smem), "occ fwt");
+            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbw, kf, 256, h->fwt_smem), "occ fwt");
             h->fwt_bps = nbw;
         }
     }
@@ -128,9 +130,12 @@ void FilterK<N>::run(rb_handle* h, int64_t max_parents, int64_t* tags, int64_t p
         if (g)
             klaunch_k(h, h->gen.filter_wt, blocks, 256, h->fwt_smem, h->meta, (const uint8_t*)h->d_tab, h->F[h->cur].f,
                       par, h->d_ctr, h->S, tags, (const int*)h->d_order, pcount);
+        else if (h->meta.fwt_direct)
+            klaunch(h, k_filter_wt<N, TabEval, true>, blocks, 256, h->fwt_smem, h->meta, h->d_tab, h->F[h->cur].f,
+                    par, h->d_ctr, h->S, tags, h->d_order, pcount);
         else
-            klaunch(h, k_filter_wt<N>, blocks, 256, h->fwt_smem, h->meta, h->d_tab, h->F[h->cur].f, par, h->d_ctr,
-                    h->S, tags, h->d_order, pcount);
+            klaunch(h, k_filter_wt<N, TabEval, false>, blocks, 256, h->fwt_smem, h->meta, h->d_tab, h->F[h->cur].f,
+                    par, h->d_ctr, h->S, tags, h->d_order, pcount);
         ck(cudaGetLastError(), "filter_wt launch");
         return;
     }
