@@ -19,10 +19,12 @@ ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "rb
     python tools/prof_solve.py katsura6 > $out/ncu_k6.log 2>&1
 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "rb_round_6/" -o $out/brown8_r6 \
     python tools/prof_solve.py brown8 > $out/ncu_brown8.log 2>&1
-ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "rb_round_5/" -o $out/eco8_r5 \
-    python tools/prof_solve.py eco8 > $out/ncu_eco8.log 2>&1
+ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "rb_round_4/" --nvtx-include "rb_round_5/" \
+    -o $out/eco8_r4r5 python tools/prof_solve.py eco8 > $out/ncu_eco8.log 2>&1
+ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "rb_round_2/" -o $out/banded12_r2 \
+    python tools/prof_solve.py broyden_banded12 > $out/ncu_banded12.log 2>&1
 # raw metrics + per-line source counters as CSV; the reports themselves stay on the box
-for r in bt6_r3 k6_r5 brown8_r6 eco8_r5; do
+for r in bt6_r3 k6_r5 brown8_r6 eco8_r4r5 banded12_r2; do
     if [ -f $out/$r.ncu-rep ]; then
         ncu -i $out/$r.ncu-rep --page raw --csv > $out/${r}_raw.csv 2>/dev/null
         ncu -i $out/$r.ncu-rep --page details --csv > $out/${r}_details.csv 2>/dev/null
