@@ -1606,6 +1606,9 @@ __device__ void hs_passthrough(const SBuf& S, int64_t n_in, const Front& out, Co
 
 // K2a: thread per box.  Rows [b0, b0 + B) of S.  When HS is off for this round the
 // first batch launch copies S into F_next instead (bnb.py:580-581).
+#ifndef RB_EVAL_PREFETCH
+#define RB_EVAL_PREFETCH 1
+#endif
 #ifndef RB_EVAL_MINB
 #define RB_EVAL_MINB 1  // k_hs_eval min blocks per SM (register cap)
 #endif
@@ -1641,13 +1644,14 @@ __global__ void __launch_bounds__(128, RB_EVAL_MINB) k_hs_eval(TabMeta meta, con
     const int64_t items = nb * R;
     unsigned long long exact_acc = 0;
     // stage box b (components at xlo / xhi / xmid [j * stride]); guards of J(X) and F(x)
-    auto stage = [&](int64_t b, int64_t t, bool write_x, bool& fastJ, bool& fastF) {
+    auto stage_regs = [&](const double (&blo)[N], const double (&bhi)[N], int64_t t, bool write_x, bool& fastJ,
+                          bool& fastF) {
         ExpRange rx, rm;
         rx.init();
         rm.init();
 #pragma unroll
         for (int j = 0; j < N; j++) {
-            const double lo = S.lo[j * S.cap + b], hi = S.hi[j * S.cap + b];
+            const double lo = blo[j], hi = bhi[j];
             const double m = mid_of(lo, hi);  // Box.midpoint, poly.py:114-115
             xlo[j * stride] = lo;
             xhi[j * stride] = hi;
@@ -1660,6 +1664,24 @@ __global__ void __launch_bounds__(128, RB_EVAL_MINB) k_hs_eval(TabMeta meta, con
         fastJ = poly_guard_ok(meta.j_ecmin, meta.j_ecmax, meta.j_deg, rx);
         fastF = poly_guard_ok(meta.f_ecmin, meta.f_ecmax, meta.f_deg, rm);
     };
+    auto stage = [&](int64_t b, int64_t t, bool write_x, bool& fastJ, bool& fastF) {
+        double blo[N], bhi[N];
+#pragma unroll
+        for (int j = 0; j < N; j++) blo[j] = S.lo[j * S.cap + b], bhi[j] = S.hi[j * S.cap + b];
+        stage_regs(blo, bhi, t, write_x, fastJ, fastF);
+    };
+    // the next box's rows are loaded while this one is evaluated (the loads' latency was
+    // the kernel's main stall: long scoreboard ~10 per issue at 12 % occupancy)
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    double nlo[N], nhi[N];
+    auto fetch = [&](int64_t it2) {
+        if (it2 < items) {
+            const int64_t b2 = b0 + it2 % nb;
+#pragma unroll
+            for (int j = 0; j < N; j++) nlo[j] = S.lo[j * S.cap + b2], nhi[j] = S.hi[j * S.cap + b2];
+        }
+    };
+    if (RB_EVAL_PREFETCH) fetch((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     bool deferred = false;
     // constant J entries are not stored when k_hs_lin_tps takes them from prm.jc (the
     // specialised evaluator skips exactly the entries the engine's mask holds)
@@ -1670,7 +1692,15 @@ __global__ void __launch_bounds__(128, RB_EVAL_MINB) k_hs_eval(TabMeta meta, con
         const int r = (int)(it / nb);
         const int64_t b = b0 + t;
         bool fastJ, fastF;
-        stage(b, t, r == 0, fastJ, fastF);
+        if (RB_EVAL_PREFETCH) {
+            double blo[N], bhi[N];
+#pragma unroll
+            for (int j = 0; j < N; j++) blo[j] = nlo[j], bhi[j] = nhi[j];
+            fetch(it + gs);
+            stage_regs(blo, bhi, t, r == 0, fastJ, fastF);
+        } else {
+            stage(b, t, r == 0, fastJ, fastF);
+        }
         if constexpr (EV::whole_box) {  // specialised evaluator: all of J(X) and F(x) by this thread (R = 1)
             // a box needing the Exact policy is evaluated after the loop: no out-of-line call
             // in the hot loop (its calling convention spilled the loop state to the stack)
