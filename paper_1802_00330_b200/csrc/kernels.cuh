@@ -1293,11 +1293,23 @@ __host__ __device__ inline int fwt_smem_bytes(const TabMeta& m, int threads) {
 #ifndef RB_FWT_UNROLL
 #define RB_FWT_UNROLL 2
 #endif
+// k_filter_wt's minimum blocks per SM (0: block size only).  ptxas settles on 80
+// registers with ~100 B of spills either way; 3 measured best (brown8 filter 3.65 ->
+// 3.48 ms, eco8 5.57 -> 5.40; 2 blocks: slower), a compacted evaluation of the live
+// children after the first equation slower still (eco8 5.6 -> 6.3 ms)
+#ifndef RB_FWT_MINB
+#define RB_FWT_MINB 3
+#endif
+#if RB_FWT_MINB > 0
+#define RB_FWT_BOUNDS __launch_bounds__(256, RB_FWT_MINB)
+#else
+#define RB_FWT_BOUNDS __launch_bounds__(256)
+#endif
 constexpr int kFwtUnroll = RB_FWT_UNROLL;
 // HYB: some equations evaluated per child (meta.fwt_direct); a separate instantiation, as
 // that path's code in the loop cost the all-table systems ~15 % (instruction fetch)
 template <int N, class EV = TabEval, bool HYB = false>
-__global__ void __launch_bounds__(256) k_filter_wt(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
+__global__ void RB_FWT_BOUNDS k_filter_wt(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                    const uint32_t* __restrict__ parents, Counters* ctr, SBuf S,
                                                    int64_t* tags, const int* __restrict__ eq_order, int64_t pcount) {
     pdl_enter();
