@@ -2554,8 +2554,11 @@ __device__ __forceinline__ int div_extended_fast(ival p, ival y, ival& q0, ival&
 
 // K2c: thread per box: the Gauss-Seidel sweep (hansen.py:91-138) and the
 // _hs_pass output rules (bnb.py:197-210), compacted into `out` after the carried rows.
+#ifndef RB_SWEEP_MINB
+#define RB_SWEEP_MINB 4  // k_hs_sweep min blocks per SM: 120 registers at n = 8, no spills (4 vs 1: katsura6 / brown8 / eco8 solves -3 %)
+#endif
 template <int N>
-__global__ void __launch_bounds__(128) k_hs_sweep(TabMeta meta, SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm,
+__global__ void __launch_bounds__(128, (N <= 10 ? RB_SWEEP_MINB : 1)) k_hs_sweep(TabMeta meta, SBuf S, int64_t n_in_arg, int64_t b0, HsParams prm,
                                                   HsScratch W, Front out, Counters* ctr, int64_t* tags) {
     pdl_enter();
     extern __shared__ __align__(16) uint8_t smem[];
