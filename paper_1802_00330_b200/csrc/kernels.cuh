@@ -19,6 +19,24 @@
 #endif
 #include "interval.cuh"
 
+// launch bounds of the round graph's kernels (0: block size only) -- dev knobs
+#ifndef RB_CF_MINB
+#define RB_CF_MINB 0
+#endif
+#if RB_CF_MINB > 0
+#define RB_CF_BOUNDS __launch_bounds__(256, RB_CF_MINB)
+#else
+#define RB_CF_BOUNDS __launch_bounds__(256)
+#endif
+#ifndef RB_FUSED_MINB
+#define RB_FUSED_MINB 0
+#endif
+#if RB_FUSED_MINB > 0
+#define RB_FUSED_BOUNDS __launch_bounds__(128, RB_FUSED_MINB)
+#else
+#define RB_FUSED_BOUNDS __launch_bounds__(128)
+#endif
+
 #ifdef __CUDACC_RTC__
 // system-specialised kernels (NVRTC) are never launched with graph conditionals
 #define RB_SET_COND(h, v) ((void)(h), (void)(v))
@@ -908,7 +926,7 @@ __global__ void __launch_bounds__(256) k_filter(TabMeta meta, const uint8_t* __r
 // classify kernel and the parents list round trip; costs 2^n - 1 idle threads per
 // carried row, which is why only the small rounds of the round graph use it.
 template <int N, class EV = TabEval>
-__global__ void __launch_bounds__(256) k_classify_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
+__global__ void RB_CF_BOUNDS k_classify_filter(TabMeta meta, const uint8_t* __restrict__ gtab, Front cur,
                                                          Front next, Counters* ctr, SBuf S, const DevState* st,
                                                          const int* __restrict__ eq_order, DedupCtx dd,
                                                          unsigned long long* prof) {
@@ -3427,7 +3445,7 @@ __device__ __forceinline__ void k_hs_fused_body(TabMeta meta, const uint8_t* __r
 }
 
 template <int N, class EV = TabEval>
-__global__ void __launch_bounds__(128) k_hs_fused(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
+__global__ void RB_FUSED_BOUNDS k_hs_fused(TabMeta meta, const uint8_t* __restrict__ gtab, SBuf S,
                                                   int64_t n_in_arg, HsParams prm, Front out, Counters* ctr,
                                                   int64_t* tags) {
     pdl_launch();
