@@ -248,7 +248,26 @@ int64_t rb_kernel_launches(rb_handle* h);
  *   "device_timing" 1 (default): rb_solve waits for the stream and reports CUDA-event
  *                 device time in rb_result_info.device_ms; 0: a solve the round graph
  *                 finishes returns as soon as its results are visible in mapped host
- *                 memory (completion flag), device_ms = -1. */
+ *                 memory (completion flag), device_ms = -1.
+ *   "jconst"      1 (default): J entries without a variable ([c, c] for every box) are
+ *                 neither stored by k_hs_eval nor loaded by k_hs_lin_tps; 0: every
+ *                 entry through the HS scratch.
+ *   "hs_fused"    1 (default): k_hs_fused (one warp per box) for small survivor counts,
+ *                 k_hs_eval / k_hs_lin_tps / k_hs_sweep above; 0: the three kernels
+ *                 always; 2: k_hs_fused always.
+ *   "lin_tpb"     Gauss-Jordan of the three-kernel HS: 2 (default) one thread per box,
+ *                 tableau in shared memory (n <= 12); 1 tableau in registers (n <= 8);
+ *                 0 G lanes per box.
+ *   "hs_tile"     1: k_hs_tile (a tile's whole HS in shared memory, n <= 8); 0 (default).
+ *   "codegen"     1 (default): system-specialised (NVRTC) kernels once compiled;
+ *                 0: table kernels.  "codegen_wait" 1: block until the compile is done.
+ *   "stream_parents" P > 0: every host-driven round processes its parents in chunks
+ *                 of P (otherwise only rounds whose survivors exceed the buffer do).
+ *   "mem_budget_mb" engine memory budget (0: the default, a share of free memory).
+ *   Round-graph structure (dev knobs, defaults measured best): "pingpong", "graph_cf",
+ *   "append_dedup", "graph_unroll", "graph_prologue", "graph_fused_only", "hs_cond",
+ *   "small_rounds" (persistent small-round kernel, with "mk_bps" / "mk_cap"),
+ *   "tail_blocks_x4", "pdl". */
 int rb_set_option(rb_handle* h, const char* key, int64_t value);
 
 /* ---- system-specialised kernels ----------------------------------------------

@@ -2272,8 +2272,8 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
         h->mem_budget = value > 0 ? (size_t)value << 20 : h->mem_budget_default;  // 0: the default
         return RB_OK;
     }
-    if (k == "lin_tpb") {  // three-kernel HS, n <= 8: thread-per-box Gauss-Jordan in shared memory (2) or
-                           // registers (1); 0 = G lanes per box (k_hs_lin)
+    if (k == "lin_tpb") {  // three-kernel HS: thread-per-box Gauss-Jordan in shared memory (2, n <= 12) or
+                           // registers (1, n <= 8); 0 = G lanes per box (k_hs_lin)
         h->lin_tpb = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         return RB_OK;
     }
