@@ -1792,13 +1792,22 @@ __device__ __forceinline__ int gshfl(unsigned mask, int v, int src) {
     return __shfl_sync(mask, v, src, G);
 }
 
+#ifndef RB_REDUX
+#define RB_REDUX 1
+#endif
 template <int G>
 __device__ __forceinline__ void group_reduce(unsigned mask, ExpRange& r) {
+#if RB_REDUX
+    // one redux.sync per bound (the group's lanes are exactly the mask's)
+    r.emin = __reduce_min_sync(mask, r.emin);
+    r.emax = __reduce_max_sync(mask, r.emax);
+#else
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) {
         r.emin = min(r.emin, __shfl_xor_sync(mask, r.emin, o, G));
         r.emax = max(r.emax, __shfl_xor_sync(mask, r.emax, o, G));
     }
+#endif
 }
 
 template <int G>
