@@ -256,8 +256,9 @@ int64_t rb_kernel_launches(rb_handle* h);
  *                 k_hs_eval / k_hs_lin_tps / k_hs_sweep above; 0: the three kernels
  *                 always; 2: k_hs_fused always.
  *   "lin_tpb"     Gauss-Jordan of the three-kernel HS: 2 (default) one thread per box,
- *                 tableau in shared memory (n <= 12); 1 tableau in registers (n <= 8);
- *                 0 G lanes per box.
+ *                 tableau in shared memory (n <= 8; two threads per box for 8 < n <= 12);
+ *                 3 two threads per box at every n <= 12; 1 tableau in registers
+ *                 (n <= 8); 0 G lanes per box.
  *   "hs_tile"     1: k_hs_tile (a tile's whole HS in shared memory, n <= 8); 0 (default).
  *   "codegen"     1 (default): system-specialised (NVRTC) kernels once compiled;
  *                 0: table kernels.  "codegen_wait" 1: block until the compile is done.

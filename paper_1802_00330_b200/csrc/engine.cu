@@ -2274,7 +2274,7 @@ int rb_set_option(rb_handle* h, const char* key, int64_t value) {
     }
     if (k == "lin_tpb") {  // three-kernel HS: thread-per-box Gauss-Jordan in shared memory (2, n <= 12) or
                            // registers (1, n <= 8); 0 = G lanes per box (k_hs_lin)
-        h->lin_tpb = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
+        h->lin_tpb = (int)std::min<int64_t>(3, std::max<int64_t>(0, value));  // 3: two threads per box
         return RB_OK;
     }
     if (k == "hs_tile") {  // large HS batches: 1 = k_hs_tile (n <= 8), 0 = eval/lin/sweep

@@ -225,6 +225,8 @@ struct rb_handle {
     int64_t stream_parents = 0;
     // k_hs_lin_tpb (thread per box Gauss-Jordan, n <= 8) in the three-kernel HS
     int lin_tpb = 2;  // 2: shared memory (k_hs_lin_tps, measured best), 1: registers (k_hs_lin_tpb), 0: G lanes per box
+    size_t lin_tp2_smem = 0;  // k_hs_lin_tp2 (lin_tpb = 3): two threads per box
+    int lin_tp2_bps = 1;
     int lin_tpb_threads = 0, lin_tpb_bps = 1, lin_tps_bps = 1;
     size_t lin_tpb_smem = 0, lin_tps_smem = 0;  // > 0: host-driven rounds stream parents in chunks of this size (tests)
     int tile_tb = 0, gen_tile_tb = 0;

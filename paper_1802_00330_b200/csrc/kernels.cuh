@@ -2495,6 +2495,203 @@ __global__ void __launch_bounds__(TpsShape<N>::T, TpsShape<N>::MINB) k_hs_lin_tp
     }
 }
 
+// k_hs_lin_tps with two threads per box (lin_tpb = 3): the pair shares the box's
+// tableau in shared memory and splits its columns by parity -- each thread swaps, scales
+// and eliminates its own columns (the pivot search and the bookkeeping are repeated by
+// both, identically), and computes the M / g columns of its parity.  Per element the
+// same operations in the same order as k_hs_lin_tps; twice the threads for the same
+// shared memory per box, so more warps hide the latencies.
+// measured (tools/hs_bench.py): slower than k_hs_lin_tps up to n = 8 (brown8 15.8 -> 18.4 ms
+// per solve), faster above (banded12 3.89 -> 3.61 ms at 4 blocks per SM): the default for
+// 8 < n <= 12
+#ifndef RB_TP2_MINB
+#define RB_TP2_MINB 5
+#endif
+#ifndef RB_TP2_MINB_WIDE
+#define RB_TP2_MINB_WIDE 4
+#endif
+template <int N>
+static __device__ __noinline__ void lin_products_pair_exact(const double* C, int S, HsScratch W, int64_t t, HsParams prm) {
+    const JConst jg{W, t, JMask(prm), prm.jc};
+    auto am = [&](int i, int u) { return C[(i * N + u) * S]; };
+    lin_products_acc<N, Exact, decltype(am), N, JConst>(am, W, t, &jg);
+}
+template <int N>
+__global__ void __launch_bounds__(128, (N > 8 ? RB_TP2_MINB_WIDE : RB_TP2_MINB)) k_hs_lin_tp2(SBuf S_, int64_t n_in_arg, int64_t b0, HsParams prm, HsScratch W,
+                                                    Counters* ctr) {
+    pdl_enter();
+    extern __shared__ __align__(16) uint8_t smem[];
+    bool hs_on;
+    const int64_t n_in = hs_count(prm, ctr, n_in_arg, S_.cap, hs_on);
+    if (n_in < 0 || !hs_on || n_in <= prm.fused_max) return;
+    const int64_t b_end = min(n_in, b0 + W.B);
+    constexpr int T = 128, SL = T / 2;  // 64 boxes per block, slot = tid / 2
+    const int slot = threadIdx.x >> 1, h = threadIdx.x & 1;
+    const unsigned pm = 3u << ((threadIdx.x & 31) & ~1);  // the pair's lanes
+    double* C = reinterpret_cast<double*>(smem) + slot;
+    auto c = [&](int i, int s2) -> double& { return C[(i * N + s2) * SL]; };
+    const JMask jmask(prm);
+    for (int64_t b = b0 + (int64_t)blockIdx.x * SL + slot; b < b_end; b += (int64_t)gridDim.x * SL) {
+        const int64_t t = b - b0;
+        const JConst jg{W, t, jmask, prm.jc};
+        ExpRange rj, ra, rf;
+        rj.init();
+        ra.init();
+        rf.init();
+        double scale = 0.0;
+        // mid(J): this thread's columns (j = h, h + 2, ...)
+#pragma unroll 1
+        for (int i = 0; i < N; i++)
+#pragma unroll
+            for (int q = 0; q < (N + 1) / 2; q++) {
+                const int j = 2 * q + h;
+                if (j >= N) break;
+                const ival v = jg(i * N + j);
+                rj.add(v.lo);
+                rj.add(v.hi);
+                const double m = mid_of(v.lo, v.hi);
+                c(i, j) = m;
+                scale = fmax(scale, fabs(m));
+            }
+        scale = fmax(scale, __shfl_xor_sync(pm, scale, 1));
+        rj.emin = min(rj.emin, __shfl_xor_sync(pm, rj.emin, 1));
+        rj.emax = max(rj.emax, __shfl_xor_sync(pm, rj.emax, 1));
+        __syncwarp(pm);
+        bool singular = scale == 0.0;
+        const double threshold = __dmul_rn(1e-12, scale);
+        using Lbl = typename TpsShape<N>::Lbl;
+        Lbl orig = 0, label = 0;
+#pragma unroll
+        for (int r = 0; r < N; r++) orig |= (Lbl)r << (4 * r);
+#pragma unroll 1
+        for (int k = 0; k < N; k++) {
+            int pr = k;
+            double best = fabs(c(k, k)), pv = c(k, k);
+#pragma unroll
+            for (int r = k + 1; r < N; r++) {
+                const double v = c(r, k);
+                if (fabs(v) > best) {
+                    best = fabs(v);
+                    pv = v;
+                    pr = r;
+                }
+            }
+            singular = singular || fabs(pv) < threshold;
+            if (!singular) {  // pair-uniform (same reads, same decisions)
+                const Lbl ok = (orig >> (4 * k)) & 15u, op = (orig >> (4 * pr)) & 15u;
+                orig = (orig & ~(((Lbl)15 << (4 * k)) | ((Lbl)15 << (4 * pr)))) | (op << (4 * k)) | (ok << (4 * pr));
+                label |= op << (4 * k);
+                const double inv = __drcp_rn(pv);  // RN(1/pivot) == 1.0 / pivot (linalg.py:162)
+                __syncwarp(pm);  // both searched column k before anything is swapped
+                double rowk[(N + 1) / 2];
+#pragma unroll
+                for (int q = 0; q < (N + 1) / 2; q++) {  // swap and scale row k, own columns
+                    const int s2 = 2 * q + h;
+                    if (s2 >= N) break;
+                    const double vk = c(k, s2), vp = c(pr, s2);
+                    c(pr, s2) = vk;
+                    rowk[q] = s2 == k ? inv : __dmul_rn(vp, inv);
+                    c(k, s2) = rowk[q];
+                }
+                __syncwarp(pm);  // column k swapped (by its owner)
+                double fcol[N];
+#pragma unroll
+                for (int i = 0; i < N; i++) fcol[i] = c(i, k);
+                __syncwarp(pm);  // both hold column k before its owner rewrites it
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    if (i == k) continue;
+                    const double f = fcol[i];
+                    if (f != 0.0) {  // linalg.py:168
+#pragma unroll
+                        for (int q = 0; q < (N + 1) / 2; q++) {
+                            const int s2 = 2 * q + h;
+                            if (s2 >= N) break;
+                            c(i, s2) = s2 == k ? __dsub_rn(0.0, __dmul_rn(f, inv))
+                                               : __dsub_rn(c(i, s2), __dmul_rn(f, rowk[q]));
+                        }
+                    }
+                }
+                __syncwarp(pm);
+            }
+        }
+        uint8_t fl = 0;
+        if (singular) {
+            fl = HSF_SINGULAR;
+        } else {
+            // unscramble, row by row: slot s holds A[i][e_s]; a thread writes its
+            // destination columns after both read the row
+#pragma unroll 1
+            for (int i = 0; i < N; i++) {
+                double row[N];
+#pragma unroll
+                for (int s2 = 0; s2 < N; s2++) row[s2] = c(i, s2);
+                __syncwarp(pm);
+#pragma unroll
+                for (int s2 = 0; s2 < N; s2++) {
+                    const int u = (int)((label >> (4 * s2)) & 15u);
+                    if ((u & 1) == h) c(i, u) = row[s2];
+                    ra.add(row[s2]);
+                }
+                __syncwarp(pm);
+            }
+#pragma unroll
+            for (int u = 0; u < N; u++) {
+                rf.add(W.fl[u * W.B + t]);
+                rf.add(W.fh[u * W.B + t]);
+            }
+            rj.emin = min(rj.emin, rf.emin);
+            rj.emax = max(rj.emax, rf.emax);
+            __syncwarp(pm);  // both read F(x) before its owner overwrites it with g
+            if (!prm.force_exact && prod_guard_ok(ra, rj)) {
+                // own columns v = h, h + 2, ... of [J | F(x)] (v = N: F(x) -> g), two per pass
+#pragma unroll 1
+                for (int v0 = h; v0 <= N; v0 += 4) {
+                    const bool two = v0 + 2 <= N;
+                    ival j0[N], j1[N];
+#pragma unroll
+                    for (int u = 0; u < N; u++) {
+                        j0[u] = v0 == N ? mk(W.fl[u * W.B + t], W.fh[u * W.B + t]) : jg(u * N + v0);
+                        j1[u] = !two ? mk(0.0, 0.0)
+                                     : (v0 + 2 == N ? mk(W.fl[u * W.B + t], W.fh[u * W.B + t]) : jg(u * N + v0 + 2));
+                    }
+#pragma unroll 1
+                    for (int i = 0; i < N; i++) {
+                        ival a0 = mk(0.0, 0.0), a1 = mk(0.0, 0.0);
+#pragma unroll
+                        for (int u = 0; u < N; u++) {
+                            const double a = lds_volatile(&c(i, u));
+                            a0 = Fast::add(a0, pmul_tpb<Fast>(a, j0[u]));
+                            a1 = Fast::add(a1, pmul_tpb<Fast>(a, j1[u]));
+                        }
+                        if (v0 == N) {
+                            W.fl[i * W.B + t] = a0.lo;
+                            W.fh[i * W.B + t] = a0.hi;
+                        } else {
+                            W.jl[(i * N + v0) * W.B + t] = a0.lo;
+                            W.jh[(i * N + v0) * W.B + t] = a0.hi;
+                        }
+                        if (two) {
+                            if (v0 + 2 == N) {
+                                W.fl[i * W.B + t] = a1.lo;
+                                W.fh[i * W.B + t] = a1.hi;
+                            } else {
+                                W.jl[(i * N + v0 + 2) * W.B + t] = a1.lo;
+                                W.jh[(i * N + v0 + 2) * W.B + t] = a1.hi;
+                            }
+                        }
+                    }
+                }
+            } else {  // rare: one thread, out of line
+                if (h == 0) lin_products_pair_exact<N>(C, SL, W, t, prm);
+                fl = HSF_EXACT_LIN;
+            }
+        }
+        if (h == 0) W.flags[t] |= fl;
+        __syncwarp(pm);  // the tableau is reused for the next box
+    }
+}
+
 // K2k: the Krawczyk operator (hansen.py:141-170) on the K2a/K2b scratch (x, M, g),
 // thread per box.  Row i: acc = [x_i,x_i] - g_i + sum_{j, (I - M)_ij != [0,0]}
 // (I - M)_ij (X_j - [x_j,x_j]), left to right, then acc intersected with X_i.

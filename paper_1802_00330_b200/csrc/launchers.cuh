@@ -58,6 +58,10 @@ void SetupK<N>::run(rb_handle* h) {
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_lin_tps<N>, TpsShape<N>::T, h->lin_tps_smem),
            "occ lin tps");
         h->lin_tps_bps = std::max(1, nb);
+        set_max_dyn_smem(k_hs_lin_tp2<N>, h->smem_optin);
+        h->lin_tp2_smem = (size_t)N * N * 64 * sizeof(double);
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_hs_lin_tp2<N>, 128, h->lin_tp2_smem), "occ lin tp2");
+        h->lin_tp2_bps = std::max(1, nb);
     }
     choose_tile(h, k_hs_tile<N>, N, stab_bytes(h->meta, false), h->tile_tb, h->tile_smem, h->tile_bps);
     if (N > 8 || h->tile_tb == 0) h->hs_tile = false;  // n > 8: one box per warp, the three kernels win
@@ -183,9 +187,9 @@ void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* 
     if constexpr (N <= 8)
         if (h->lin_tpb == 1 && h->lin_tpb_threads > 0) lin = 1;
     if constexpr (N <= 12)
-        if (lin == 0 && h->lin_tpb == 2) lin = 2;
+        if (lin == 0 && (h->lin_tpb == 2 || h->lin_tpb == 3)) lin = (h->lin_tpb == 2 && N > 8) ? 3 : h->lin_tpb;
     prm.jc = nullptr;
-    if (lin == 2 && h->jconst && (h->jmask[0] | h->jmask[1] | h->jmask[2] | h->jmask[3])) {
+    if ((lin == 2 || lin == 3) && h->jconst && (h->jmask[0] | h->jmask[1] | h->jmask[2] | h->jmask[3])) {
         prm.jc = h->d_jc;
         for (int w = 0; w < 4; w++) prm.jm[w] = h->jmask[w];
     }
@@ -210,6 +214,9 @@ void HsK<N>::run(rb_handle* h, int64_t b0, int64_t n_in, HsParams prm, int64_t* 
         if (lin == 2) {
             constexpr int TT = TpsShape<N>::T;
             klaunch(h, k_hs_lin_tps<N>, grid_for(bound, TT, h->sms * h->lin_tps_bps), TT, h->lin_tps_smem, h->S,
+                    n_in, b0, prm, h->W, h->d_ctr);
+        } else if (lin == 3) {  // two threads per box: 64 boxes per block
+            klaunch(h, k_hs_lin_tp2<N>, grid_for(bound, 64, h->sms * h->lin_tp2_bps), 128, h->lin_tp2_smem, h->S,
                     n_in, b0, prm, h->W, h->d_ctr);
         }
     }

@@ -352,6 +352,27 @@ def test_solve_host_loop_three_kernel_hs(native, case):
     check_against_golden(case, out, meta)
 
 
+@pytest.mark.parametrize("lin", [2, 3], ids=["thread_per_box", "pair_per_box"])
+@pytest.mark.parametrize("case", solve_cases())
+def test_solve_host_loop_gauss_jordan_variants(native, case, lin):
+    """Three-kernel HS with the thread-per-box (k_hs_lin_tps) and the two-threads-per-box
+    (k_hs_lin_tp2) Gauss-Jordan forced at every n <= 12."""
+    from paper_1802_00330_b200 import bnb
+    meta = load_solve(case)
+    spec = golden_spec(meta["system"])
+    eng = bnb.engine_for(spec)
+    eng.set_option("graph", 0)
+    eng.set_option("hs_fused", 0)
+    eng.set_option("lin_tpb", lin)
+    try:
+        out = eng.solve(bnb.native_config(bnb.SolverConfig(**meta["config"])))
+    finally:
+        eng.set_option("graph", 1)
+        eng.set_option("hs_fused", 1)
+        eng.set_option("lin_tpb", 2)
+    check_against_golden(case, out, meta)
+
+
 @pytest.mark.parametrize("case", solve_cases()[:12])
 def test_solve_persistent_small_rounds(native, case):
     """The experimental persistent small-round kernel (grid barriers, ping-pong frontier)."""
