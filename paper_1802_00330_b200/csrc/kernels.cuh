@@ -693,6 +693,12 @@ struct TabEval {
     __device__ __forceinline__ static ival feq(const TermP* tp, const STab& t, int e, const double2* xs2, int stride) {
         return A::exact ? eval_poly_packed_exact(tp, t, e, xs2, stride) : eval_poly_packed<A>(tp, t, e, xs2, stride);
     }
+    // k_filter_wt's per-child equations (the specialised evaluator compiles only those)
+    template <class A>
+    __device__ __forceinline__ static ival feq_direct(const TermP* tp, const STab& t, int e, const double2* xs2,
+                                                      int stride) {
+        return feq<A>(tp, t, e, xs2, stride);
+    }
     // k_filter_wt: f(sum) with sum(c, tb) = tsum of equation e (selected once)
     template <int N, class A, class F>
     __device__ __forceinline__ static void with_tsum(const STab& t, const uint16_t* tbase, int e, F&& f) {
@@ -1397,8 +1403,8 @@ __global__ void RB_FWT_BOUNDS k_filter_wt(TabMeta meta, const uint8_t* __restric
                             xs2[j * blockDim.x] = up ? make_double2(sp[2 * N + j], sp[N + j])
                                                      : make_double2(sp[j], sp[2 * N + j]);
                         }
-                        const ival v = exact ? EV::template feq<Exact>(tp, tab, e, xs2, blockDim.x)
-                                             : EV::template feq<RB_FILTER_FAST>(tp, tab, e, xs2, blockDim.x);
+                        const ival v = exact ? EV::template feq_direct<Exact>(tp, tab, e, xs2, blockDim.x)
+                                             : EV::template feq_direct<RB_FILTER_FAST>(tp, tab, e, xs2, blockDim.x);
                         if (!(v.lo <= 0.0 && 0.0 <= v.hi)) alive &= ~(1u << i);
                     }
                     const unsigned ne = (unsigned)__popc(before), nr = ne - (unsigned)__popc(alive);
